@@ -1,0 +1,152 @@
+/*
+ * fpssft.h -- C ABI of the B200-native FPS-SFT recovery loop.
+ *
+ * Plain pointers and sizes only; every device buffer is owned by the caller.
+ * All entry points are stream-ordered and asynchronous, reentrant across
+ * streams, threads and devices, and keep no global mutable state (the root
+ * tables are built per CTA on chip).  Return value 0 = success; otherwise a
+ * FPSSFT_E* code and fpssft_last_error() (thread-local) says why.
+ *
+ * The reference (fps-sft 0.1.0, pure Python) exposes this path as Python
+ * functions; each entry point below names the reference interface it replaces
+ * (paths under /root/reference/pkg/src/fps_sft/).  The Python mirror of that
+ * interface, paper_1711_11407_b200, binds these symbols with ctypes.
+ */
+#ifndef FPSSFT_H_
+#define FPSSFT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPSSFT_MAX_DIMS 4
+
+/* error codes (the Python mirror maps them to the reference's exceptions) */
+#define FPSSFT_OK 0
+#define FPSSFT_EINVAL 1       /* ValueError   (core.py:225-226, lines.py:30-31, driver.py:55-63) */
+#define FPSSFT_EOVERFLOW 2    /* OverflowError (core.py:53-54, :197-198)                         */
+#define FPSSFT_EUNSUPPORTED 3 /* shape/capacity beyond what one CTA holds on chip                */
+#define FPSSFT_ECUDA 4        /* CUDA runtime error                                              */
+
+/* arithmetic the path computes in (input cubes are always complex64) */
+#define FPSSFT_F32 0
+#define FPSSFT_F64 1
+
+/* terminated_by codes (driver.py:24-26 plus capacity overflow) */
+#define FPSSFT_TERM_RESIDUAL_CLEAN 0
+#define FPSSFT_TERM_STALL 1
+#define FPSSFT_TERM_MAX_ITERATIONS 2
+#define FPSSFT_TERM_K_CAP_OVERFLOW 3
+
+/* CubeShape (core.py:26-73) plus the element strides of one cube. */
+typedef struct fpssft_shape {
+    int32_t ndim;                      /* D, 1..FPSSFT_MAX_DIMS                     */
+    int32_t dims[FPSSFT_MAX_DIMS];     /* N_k                                       */
+    int64_t strides[FPSSFT_MAX_DIMS];  /* element strides (row-major: N_1*..., 1)  */
+} fpssft_shape;
+
+/* FpsSftConfig (driver.py:29-63) minus seed (the schedule is explicit),
+ * plus the recovered-set capacity and the arithmetic precision. */
+typedef struct fpssft_params {
+    int32_t t_max;       /* iteration cap (driver.py:132, default :88-91)  */
+    int32_t stall_limit; /* driver.py:44                                    */
+    int32_t k_cap;       /* recovered-set capacity per instance (power of 2)*/
+    int32_t precision;   /* FPSSFT_F32 | FPSSFT_F64                         */
+    double mag_tol, verify_tol, round_tol, amp_prune_tol;
+    double energy_floor, energy_floor_abs, residual_stop;
+} fpssft_params;
+
+/* RecoveryReport (driver.py:76-85), padded per instance. */
+typedef struct fpssft_out {
+    int32_t *freqs;        /* [B, k_cap, D]  lexicographic order (core.py:102) */
+    double *amps;          /* [B, k_cap, 2]  complex128                         */
+    int32_t *count;        /* [B]            len(recovered)                     */
+    int32_t *iterations;   /* [B]            iterations_run                     */
+    int64_t *samples_used; /* [B]            iterations*(D+1)*L                 */
+    int32_t *terminated_by;/* [B]            FPSSFT_TERM_*                       */
+    int32_t *iter_stats;   /* [B, t_max, 3]  (candidates, accepted, rejected) or NULL (driver.py:66-73) */
+} fpssft_out;
+
+/*
+ * The whole recovery loop for a batch of independent complex64 cubes.
+ * Replaces fps_sft(make_dense_source(cube, shape), config)
+ * (driver.py:121-212, core.py:276-278) for every instance b:
+ *   cube_b    = cubes + b*batch_stride                       (device, complex64)
+ *   schedule  = int32 [n_sched, t_max, 2, D] (alpha, tau)     (device)
+ *               the (alpha_t, tau_t) the reference draws from default_rng(seed)
+ *               (driver.py:131,142-143); see paper_1711_11407_b200.schedule
+ *   sched_index[b] in [0, n_sched) picks instance b's schedule (NULL = 0).
+ */
+int fpssft_run_batch(const void *cubes, int64_t batch, int64_t batch_stride,
+                     const fpssft_shape *shape, const fpssft_params *params,
+                     const int32_t *schedule, const int32_t *sched_index, int32_t n_sched,
+                     const fpssft_out *out, void *stream);
+
+/*
+ * D+1 line spectra of one iteration per instance.  Replaces
+ *   [dft_forward(extract_line(DenseSource(cube), LineParams(alpha, off, L)))
+ *    for off in decoding_offsets(tau)]
+ * (lines.py:36-64, core.py:236-238, transform.py:17-22).
+ * alpha_tau: device int32 [B or 1, 2, D]; per_instance selects which.
+ * spectra: [B, D+1, L] complex64 (F32) or complex128 (F64).
+ */
+int fpssft_line_spectra(const void *cubes, int64_t batch, int64_t batch_stride,
+                        const fpssft_shape *shape, const int32_t *alpha_tau,
+                        int32_t per_instance, void *spectra, int32_t precision, void *stream);
+
+/*
+ * Batched 1/L-normalised forward DFT (transform.py:17-22, dft_forward).
+ * lines/out: [B, L] complex64 (F32) or complex128 (F64); may alias.
+ */
+int fpssft_dft_forward(const void *lines, int64_t batch, int32_t L, void *out,
+                       int32_t precision, void *stream);
+
+/*
+ * Per-bin 1-sparse test + OFDM phase decode + verification, vectorised over
+ * all L bins (decoder.py:127-169, decode_spectra) plus the driver's
+ * bin-consistency guard (driver.py:166-176) when alpha is given.
+ *   spectra: [B, D+1, L] complex (precision); alpha_tau: [B or 1, 2, D].
+ *   floor:   the energy floor handed to decode_spectra (driver.py:156).
+ *   status:  [B, L] int32: 0 not a candidate, 1 candidate rejected,
+ *            2 accepted, 3 decoded but failed the bin guard.
+ *   freqs:   [B, L, D] int32 decoded m (valid where status >= 2).
+ *   amps:    [B, L, 2] double (valid where status >= 2).
+ *   n_candidates: [B] int32.
+ */
+int fpssft_decode_spectra(const void *spectra, int64_t batch, const fpssft_shape *shape,
+                          const int32_t *alpha_tau, int32_t per_instance,
+                          const fpssft_params *params, double floor, int32_t *status,
+                          int32_t *freqs, double *amps, int32_t *n_candidates,
+                          void *stream);
+
+/*
+ * Project a sparse set onto the line bins (decoder.py:172-191,
+ * project_onto_bins; bin map numtheory.py:139-153):
+ *   out[b, bin(m)] += a * exp(2 pi j u_tau(m) / L), summed in entry order.
+ *   freqs [B, k_max, D] int32, amps [B, k_max, 2] double, counts [B] int32,
+ *   alpha_tau [B or 1, 2, D], out [B, L, 2] double.
+ */
+int fpssft_project_onto_bins(const int32_t *freqs, const double *amps, const int32_t *counts,
+                             int64_t batch, int32_t k_max, const fpssft_shape *shape,
+                             const int32_t *alpha_tau, int32_t per_instance, double *out,
+                             int32_t precision, void *stream);
+
+/* Dynamic shared memory one fpssft_run_batch CTA needs (0 if unsupported). */
+size_t fpssft_smem_bytes(const fpssft_shape *shape, const fpssft_params *params);
+
+/* Threads per CTA fpssft_run_batch uses for this shape. */
+int fpssft_block_threads(const fpssft_shape *shape, int32_t precision);
+
+/* Number of kernel launches fpssft_run_batch issues per call (for accounting). */
+int fpssft_launches_per_batch(void);
+
+const char *fpssft_last_error(void);
+int fpssft_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FPSSFT_H_ */

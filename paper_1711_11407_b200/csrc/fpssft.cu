@@ -1,0 +1,893 @@
+// B200-native FPS-SFT: kernels and the C ABI declared in include/fpssft.h.
+//
+// recover_kernel is the product: one CTA per instance runs the whole
+// projection-slice loop of fps_sft (reference driver.py:121-212) on chip --
+// gather D+1 lines from the HBM-resident cube, FFT them in shared memory,
+// peel the recovered set, classify/decode every bin, merge, test termination
+// -- and writes the padded RecoveryReport.  The other kernels expose single
+// steps (line spectra, DFT, classifier, projection) through the same device
+// code so each reference function can be parity-tested on its own.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "../../include/fpssft.h"
+#include "fpssft_device.cuh"
+
+namespace fpssft {
+
+// ------------------------------------------------------------ smem layout
+struct Layout {
+    size_t spec, roots, slot_amp, slot_m, slot_key, slot_live, hash;
+    size_t bin_start, bin_fill, seg, slot_bin, slot_u0;  // projection scratch (union A)
+    size_t dec_amp, dec_m, dec_lin, dec_slot;            // classifier scratch (union B)
+    size_t red, total;
+    int H;
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline Layout make_layout(int D, int L, int k_cap, int cs) {
+    Layout y;
+    const int nl = D + 1;
+    size_t o = 0;
+    y.H = 2 * k_cap;
+    y.spec = o;      o = align16(o + (size_t)nl * L * cs);
+    y.roots = o;     o = align16(o + (size_t)L * cs);
+    y.slot_amp = o;  o = align16(o + (size_t)k_cap * cs);
+    y.slot_m = o;    o = align16(o + (size_t)k_cap * D * 4);
+    y.slot_key = o;  o = align16(o + (size_t)k_cap * 4);
+    y.slot_live = o; o = align16(o + (size_t)k_cap * 4);
+    y.hash = o;      o = align16(o + (size_t)y.H * 4);
+    const size_t u = o;
+    y.bin_start = u; size_t a = align16(u + (size_t)(L + 1) * 4);
+    y.bin_fill = a;  a = align16(a + (size_t)L * 4);
+    y.seg = a;       a = align16(a + (size_t)k_cap * 4);
+    y.slot_bin = a;  a = align16(a + (size_t)k_cap * 4);
+    y.slot_u0 = a;   a = align16(a + (size_t)k_cap * 4);
+    y.dec_amp = u;   size_t b = align16(u + (size_t)L * cs);
+    y.dec_m = b;     b = align16(b + (size_t)L * D * 4);
+    y.dec_lin = b;   b = align16(b + (size_t)L * 4);
+    y.dec_slot = b;  b = align16(b + (size_t)L * 4);
+    o = a > b ? a : b;
+    y.red = o;       o = align16(o + 64 * 8);
+    y.total = o;
+    return y;
+}
+
+struct OutPtrs {
+    int *freqs;
+    double *amps;
+    int *count, *iterations;
+    long long *samples_used;
+    int *terminated_by, *iter_stats;
+};
+
+__device__ __forceinline__ unsigned hash32(int key) { return (unsigned)key * 2654435761u; }
+
+__device__ __forceinline__ int hash_find(const int *hash, const int *slot_key, int H, int key) {
+    unsigned h = hash32(key) & (unsigned)(H - 1);
+    while (true) {
+        const int s = hash[h];
+        if (s < 0) return -1;
+        if (slot_key[s] == key) return s;
+        h = (h + 1) & (unsigned)(H - 1);
+    }
+}
+__device__ __forceinline__ void hash_insert(int *hash, int H, int key, int slot) {
+    unsigned h = hash32(key) & (unsigned)(H - 1);
+    while (atomicCAS(&hash[h], -1, slot) != -1) h = (h + 1) & (unsigned)(H - 1);
+}
+
+__device__ __forceinline__ int linear_index(const int *m, const Geo &g) {
+    int lin = 0;
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k)
+        if (k < g.D) lin = lin * g.N[k] + m[k];
+    return lin;
+}
+
+__device__ __forceinline__ bool line_params_ok(const Geo &g, const int *al, const int *ta) {
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k)
+        if (k < g.D) ok = ok && al[k] >= 0 && al[k] < g.N[k] && ta[k] >= 0 && ta[k] < g.N[k];
+    return ok;
+}
+
+// ------------------------------------------------------------ projection
+// Line spectrum of the recovered set (project_onto_bins, decoder.py:172-191)
+// for `nl` offsets, either subtracted from spec (driver.py:150-154) or
+// stored.  Per-bin sums run in slot order (= insertion order, like
+// np.bincount over the dict arrays) via a counting sort, so the result is
+// deterministic -- no floating-point atomics.
+template <class R>
+__device__ void project_bins(cpx<R> *spec, int nl, const Geo &g, const int *al, const int *ta,
+                             int n_slots, const int *slot_m, const cpx<R> *slot_amp,
+                             const int *slot_live, int *bin_start, int *bin_fill, int *seg,
+                             int *slot_bin, int *slot_u0, const cpx<R> *roots, int *ired,
+                             bool subtract) {
+    const int L = g.L, D = g.D, NT = blockDim.x, tid = threadIdx.x;
+    for (int b = tid; b < L; b += NT) bin_fill[b] = 0;
+    __syncthreads();
+    for (int s = tid; s < n_slots; s += NT) {
+        if (slot_live == nullptr || slot_live[s]) {
+            int m[MAXD];
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k) m[k] = k < D ? slot_m[s * D + k] : 0;
+            const int b = bin_of(m, g, al);
+            slot_bin[s] = b;
+            slot_u0[s] = phase_of(m, g, ta);
+            atomicAdd(&bin_fill[b], 1);
+        } else {
+            slot_bin[s] = -1;
+        }
+    }
+    __syncthreads();
+    int carry = 0;
+    for (int j0 = 0; j0 < L; j0 += NT) {
+        const int b = j0 + tid;
+        const int c = b < L ? bin_fill[b] : 0;
+        int tot;
+        const int pre = block_exscan(c, ired, &tot);
+        if (b < L) {
+            bin_start[b] = carry + pre;
+            bin_fill[b] = 0;
+        }
+        carry += tot;
+    }
+    if (tid == 0) bin_start[L] = carry;
+    __syncthreads();
+    for (int s = tid; s < n_slots; s += NT) {
+        const int b = slot_bin[s];
+        if (b >= 0) seg[bin_start[b] + atomicAdd(&bin_fill[b], 1)] = s;
+    }
+    __syncthreads();
+    for (int b = tid; b < L; b += NT) {
+        const int st = bin_start[b], en = bin_start[b + 1];
+        for (int i = st + 1; i < en; ++i) {  // segments are short: insertion sort
+            const int v = seg[i];
+            int j = i - 1;
+            while (j >= st && seg[j] > v) {
+                seg[j + 1] = seg[j];
+                --j;
+            }
+            seg[j + 1] = v;
+        }
+        for (int i = 0; i < nl; ++i) {
+            cpx<R> P = {(R)0, (R)0};
+            for (int p = st; p < en; ++p) {
+                const int s = seg[p];
+                int m[MAXD];
+#pragma unroll
+                for (int k = 0; k < MAXD; ++k) m[k] = k < D ? slot_m[s * D + k] : 0;
+                P = P + slot_amp[s] * roots[phase_step(slot_u0[s], i, m, g)];
+            }
+            if (subtract) {
+                if (en > st) spec[i * L + b] = spec[i * L + b] - P;
+            } else {
+                spec[i * L + b] = P;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------ fused loop
+template <class R>
+__global__ void __launch_bounds__(1024, 1) recover_kernel(const float2 *__restrict__ cubes,
+                                                       long long batch_stride, Geo g, Knobs kn,
+                                                       const int *__restrict__ schedule,
+                                                       const int *__restrict__ sched_index,
+                                                       int n_sched, OutPtrs out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const Layout lay = make_layout(g.D, g.L, kn.k_cap, (int)sizeof(cpx<R>));
+    cpx<R> *spec = (cpx<R> *)(sm + lay.spec);
+    cpx<R> *roots = (cpx<R> *)(sm + lay.roots);
+    cpx<R> *slot_amp = (cpx<R> *)(sm + lay.slot_amp);
+    int *slot_m = (int *)(sm + lay.slot_m);
+    int *slot_key = (int *)(sm + lay.slot_key);
+    int *slot_live = (int *)(sm + lay.slot_live);
+    int *hash = (int *)(sm + lay.hash);
+    int *bin_start = (int *)(sm + lay.bin_start);
+    int *bin_fill = (int *)(sm + lay.bin_fill);
+    int *seg = (int *)(sm + lay.seg);
+    int *slot_bin = (int *)(sm + lay.slot_bin);
+    int *slot_u0 = (int *)(sm + lay.slot_u0);
+    cpx<R> *dec_amp = (cpx<R> *)(sm + lay.dec_amp);
+    int *dec_m = (int *)(sm + lay.dec_m);
+    int *dec_lin = (int *)(sm + lay.dec_lin);
+    int *dec_slot = (int *)(sm + lay.dec_slot);
+    int *ired = (int *)(sm + lay.red);
+    R *rred = (R *)(sm + lay.red + 256);
+
+    const int L = g.L, D = g.D, nl = g.nlines, NT = blockDim.x, tid = threadIdx.x;
+    const int inst = blockIdx.x;
+    const float2 *cube = cubes + (long long)inst * batch_stride;
+    int sidx = sched_index ? sched_index[inst] : 0;
+    const bool sched_ok = sidx >= 0 && sidx < n_sched;
+    if (!sched_ok) sidx = 0;
+    const int *sched = schedule + (long long)sidx * kn.t_max * 2 * D;
+    const int H = lay.H;
+    const R mag_tol = (R)kn.mag_tol, round_tol = (R)kn.round_tol, verify_tol = (R)kn.verify_tol;
+    const R prune = (R)kn.amp_prune_tol;
+
+    build_roots(roots, L);
+    for (int h = tid; h < H; h += NT) hash[h] = -1;
+    __syncthreads();
+
+    int n_slots = 0, stall = 0, it_run = 0;
+    int term = sched_ok ? FPSSFT_TERM_MAX_ITERATIONS : -1;
+    R amp_sum = (R)0;
+
+    for (int it = 0; it < kn.t_max && term != -1; ++it) {
+        int al[MAXD], ta[MAXD];
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) {
+            al[k] = k < D ? sched[(long long)it * 2 * D + k] : 0;
+            ta[k] = k < D ? sched[(long long)it * 2 * D + D + k] : 0;
+        }
+        if (!line_params_ok(g, al, ta)) {
+            term = -1;
+            break;
+        }
+        it_run = it + 1;
+
+        // (1) gather + (2) DFT of the D+1 lines           driver.py:146-154
+        gather_lines(spec, cube, g, al, ta);
+        __syncthreads();
+        fft_lines(spec, nl, g, roots);
+        // (3) construction-subtraction of the recovered set
+        if (n_slots > 0)
+            project_bins(spec, nl, g, al, ta, n_slots, slot_m, slot_amp, slot_live, bin_start,
+                         bin_fill, seg, slot_bin, slot_u0, roots, ired, true);
+
+        // (4) classify every bin                            driver.py:156-176
+        const R floor = max((R)kn.energy_floor_abs, (R)kn.energy_floor * amp_sum);
+        int my_cand = 0, my_acc = 0;
+        for (int b = tid; b < L; b += NT) {
+            int m[MAXD];
+            cpx<R> a;
+            const int st = classify_bin(spec, g, b, al, ta, roots, mag_tol, round_tol,
+                                        verify_tol, floor, m, &a);
+            my_cand += st > 0;
+            if (st == 2) {
+                ++my_acc;
+                dec_lin[b] = linear_index(m, g);
+#pragma unroll
+                for (int k = 0; k < MAXD; ++k)
+                    if (k < D) dec_m[b * D + k] = m[k];
+                dec_amp[b] = a;
+            } else {
+                dec_lin[b] = -1;
+            }
+        }
+        const int n_cand = block_sum(my_cand, ired);
+        const int n_acc = block_sum(my_acc, ired);
+
+        // (5) merge-by-sum into the recovered set, ascending bin order
+        //     (driver.py:103-108)
+        if (n_acc > 0) {
+            int total_new = 0;
+            for (int j0 = 0; j0 < L; j0 += NT) {
+                const int b = j0 + tid;
+                int isnew = 0;
+                if (b < L && dec_lin[b] >= 0) {
+                    const int s = hash_find(hash, slot_key, H, dec_lin[b]);
+                    isnew = s < 0;
+                    dec_slot[b] = s;
+                }
+                int tot;
+                const int pre = block_exscan(isnew, ired, &tot);
+                if (isnew) dec_slot[b] = (1 << 30) | (n_slots + total_new + pre);
+                total_new += tot;
+            }
+            if (n_slots + total_new > kn.k_cap) {
+                term = FPSSFT_TERM_K_CAP_OVERFLOW;
+                if (tid == 0 && out.iter_stats) {
+                    int *st = out.iter_stats + ((long long)inst * kn.t_max + it) * 3;
+                    st[0] = n_cand;
+                    st[1] = 0;
+                    st[2] = n_cand;
+                }
+                break;
+            }
+            for (int b = tid; b < L; b += NT) {
+                if (dec_lin[b] < 0) continue;
+                const int code = dec_slot[b];
+                const int s = code & ((1 << 30) - 1);
+                const cpx<R> a = dec_amp[b];
+                int m[MAXD];
+#pragma unroll
+                for (int k = 0; k < MAXD; ++k) m[k] = k < D ? dec_m[b * D + k] : 0;
+                cpx<R> v;
+                if (code >> 30) {
+                    slot_key[s] = dec_lin[b];
+#pragma unroll
+                    for (int k = 0; k < MAXD; ++k)
+                        if (k < D) slot_m[s * D + k] = m[k];
+                    hash_insert(hash, H, dec_lin[b], s);
+                    v = a;
+                } else {
+                    v = slot_amp[s] + a;  // a pruned slot holds 0: entries.get(f, 0) + a
+                }
+                const bool keep = !(cabs(v) <= prune);
+                slot_amp[s] = keep ? v : cpx<R>{(R)0, (R)0};
+                slot_live[s] = keep;
+                // remove the new sinusoid from this iteration's spectra
+                // (driver.py:189-194); its bin holds no other new entry
+                const int u0 = phase_of(m, g, ta);
+                for (int i = 0; i < nl; ++i)
+                    spec[i * L + b] = spec[i * L + b] - a * roots[phase_step(u0, i, m, g)];
+            }
+            n_slots += total_new;
+            __syncthreads();
+        }
+
+        // (6) amp_sum = sum |a| over the recovered set        driver.py:108
+        R my = (R)0;
+        for (int s = tid; s < n_slots; s += NT)
+            if (slot_live[s]) my += cabs(slot_amp[s]);
+        amp_sum = block_sum(my, rred);
+        stall = n_acc > 0 ? 0 : stall + 1;
+
+        // (7) termination                                     driver.py:196-204
+        R mx = (R)0;
+        for (int e = tid; e < nl * L; e += NT) mx = max(mx, cabs(spec[e]));
+        mx = block_max(mx, rred);
+        if (tid == 0 && out.iter_stats) {
+            int *st = out.iter_stats + ((long long)inst * kn.t_max + it) * 3;
+            st[0] = n_cand;
+            st[1] = n_acc;
+            st[2] = n_cand - n_acc;
+        }
+        const R clean = max((R)kn.energy_floor_abs, (R)kn.residual_stop * amp_sum);
+        __syncthreads();
+        if (mx <= clean) {
+            term = FPSSFT_TERM_RESIDUAL_CLEAN;
+            break;
+        }
+        if (stall >= kn.stall_limit) {
+            term = FPSSFT_TERM_STALL;
+            break;
+        }
+    }
+
+    // ---- RecoveryReport: live entries in lexicographic (= linear) order
+    __syncthreads();
+    const int P = kn.k_cap;  // power of two
+    int my_live = 0;
+    for (int s = tid; s < P; s += NT) {
+        const bool live = s < n_slots && slot_live[s];
+        my_live += live;
+        seg[s] = live ? slot_key[s] : INT_MAX;
+        slot_bin[s] = s;
+    }
+    const int count = block_sum(my_live, ired);
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < P; i += NT) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const int ki = seg[i], kj = seg[j];
+                    if ((ki > kj) == up) {
+                        seg[i] = kj;
+                        seg[j] = ki;
+                        const int t = slot_bin[i];
+                        slot_bin[i] = slot_bin[j];
+                        slot_bin[j] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int r = tid; r < count; r += NT) {
+        const int s = slot_bin[r];
+        int *fo = out.freqs + ((long long)inst * kn.k_cap + r) * D;
+        for (int k = 0; k < D; ++k) fo[k] = slot_m[s * D + k];
+        double *ao = out.amps + ((long long)inst * kn.k_cap + r) * 2;
+        ao[0] = (double)slot_amp[s].re;
+        ao[1] = (double)slot_amp[s].im;
+    }
+    if (tid == 0) {
+        out.count[inst] = count;
+        out.iterations[inst] = it_run;
+        out.samples_used[inst] = (long long)it_run * nl * L;
+        out.terminated_by[inst] = term;
+    }
+}
+
+// ------------------------------------------------------- per-function kernels
+template <class R>
+__global__ void __launch_bounds__(1024, 1) line_spectra_kernel(const float2 *__restrict__ cubes,
+                                                            long long batch_stride, Geo g,
+                                                            const int *__restrict__ alpha_tau,
+                                                            int per_instance, cpx<R> *out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    cpx<R> *spec = (cpx<R> *)sm;
+    cpx<R> *roots = spec + (size_t)g.nlines * g.L;
+    const int inst = blockIdx.x, D = g.D;
+    const int *at = alpha_tau + (per_instance ? (long long)inst * 2 * D : 0);
+    int al[MAXD], ta[MAXD];
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+        al[k] = k < D ? at[k] : 0;
+        ta[k] = k < D ? at[D + k] : 0;
+    }
+    build_roots(roots, g.L);
+    if (!line_params_ok(g, al, ta)) return;
+    gather_lines(spec, cubes + (long long)inst * batch_stride, g, al, ta);
+    __syncthreads();
+    fft_lines(spec, g.nlines, g, roots);
+    cpx<R> *o = out + (long long)inst * g.nlines * g.L;
+    for (int e = threadIdx.x; e < g.nlines * g.L; e += blockDim.x) o[e] = spec[e];
+}
+
+template <class R>
+__global__ void __launch_bounds__(1024, 1) dft_kernel(const cpx<R> *__restrict__ in, Geo g,
+                                                   cpx<R> *out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    cpx<R> *x = (cpx<R> *)sm;
+    cpx<R> *roots = x + g.L;
+    const long long off = (long long)blockIdx.x * g.L;
+    build_roots(roots, g.L);
+    for (int l = threadIdx.x; l < g.L; l += blockDim.x) x[l] = in[off + l];
+    __syncthreads();
+    fft_lines(x, 1, g, roots);
+    for (int l = threadIdx.x; l < g.L; l += blockDim.x) out[off + l] = x[l];
+}
+
+template <class R>
+__global__ void __launch_bounds__(1024, 1) decode_kernel(const cpx<R> *__restrict__ spectra, Geo g,
+                                                      const int *__restrict__ alpha_tau,
+                                                      int per_instance, Knobs kn, double floor,
+                                                      int *status, int *freqs, double *amps,
+                                                      int *n_candidates) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    cpx<R> *spec = (cpx<R> *)sm;
+    cpx<R> *roots = spec + (size_t)g.nlines * g.L;
+    int *ired = (int *)(roots + g.L);
+    const int inst = blockIdx.x, D = g.D, L = g.L;
+    const int *at = alpha_tau + (per_instance ? (long long)inst * 2 * D : 0);
+    int al[MAXD], ta[MAXD];
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+        al[k] = k < D ? at[k] : 0;
+        ta[k] = k < D ? at[D + k] : 0;
+    }
+    build_roots(roots, L);
+    const cpx<R> *src = spectra + (long long)inst * g.nlines * L;
+    for (int e = threadIdx.x; e < g.nlines * L; e += blockDim.x) spec[e] = src[e];
+    __syncthreads();
+    int my = 0;
+    for (int b = threadIdx.x; b < L; b += blockDim.x) {
+        int m[MAXD] = {0, 0, 0, 0};
+        cpx<R> a = {(R)0, (R)0};
+        const int st = classify_bin(spec, g, b, al, ta, roots, (R)kn.mag_tol, (R)kn.round_tol,
+                                    (R)kn.verify_tol, (R)floor, m, &a);
+        my += st > 0;
+        const long long o = (long long)inst * L + b;
+        status[o] = st;
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k)
+            if (k < D) freqs[o * D + k] = m[k];
+        amps[o * 2] = (double)a.re;
+        amps[o * 2 + 1] = (double)a.im;
+    }
+    const int tot = block_sum(my, ired);
+    if (threadIdx.x == 0) n_candidates[inst] = tot;
+}
+
+template <class R>
+__global__ void __launch_bounds__(1024, 1) project_kernel(const int *__restrict__ freqs,
+                                                       const double *__restrict__ amps,
+                                                       const int *__restrict__ counts, int k_max,
+                                                       Geo g, const int *__restrict__ alpha_tau,
+                                                       int per_instance, double *out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int inst = blockIdx.x, D = g.D, L = g.L, NT = blockDim.x, tid = threadIdx.x;
+    const Layout lay = make_layout(D, L, k_max, (int)sizeof(cpx<R>));
+    cpx<R> *spec = (cpx<R> *)(sm + lay.spec);
+    cpx<R> *roots = (cpx<R> *)(sm + lay.roots);
+    cpx<R> *slot_amp = (cpx<R> *)(sm + lay.slot_amp);
+    int *slot_m = (int *)(sm + lay.slot_m);
+    const int *at = alpha_tau + (per_instance ? (long long)inst * 2 * D : 0);
+    int al[MAXD], ta[MAXD];
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+        al[k] = k < D ? at[k] : 0;
+        ta[k] = k < D ? at[D + k] : 0;
+    }
+    const int n = min(counts[inst], k_max);
+    build_roots(roots, L);
+    for (int s = tid; s < n; s += NT) {
+        const long long o = (long long)inst * k_max + s;
+        for (int k = 0; k < D; ++k) slot_m[s * D + k] = freqs[o * D + k];
+        slot_amp[s] = {(R)amps[o * 2], (R)amps[o * 2 + 1]};
+    }
+    __syncthreads();
+    project_bins(spec, 1, g, al, ta, n, slot_m, slot_amp, (const int *)nullptr,
+                 (int *)(sm + lay.bin_start), (int *)(sm + lay.bin_fill), (int *)(sm + lay.seg),
+                 (int *)(sm + lay.slot_bin), (int *)(sm + lay.slot_u0), roots,
+                 (int *)(sm + lay.red), false);
+    for (int b = tid; b < L; b += NT) {
+        out[((long long)inst * L + b) * 2] = (double)spec[b].re;
+        out[((long long)inst * L + b) * 2 + 1] = (double)spec[b].im;
+    }
+}
+
+// ================================================================== host
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+    return fail(FPSSFT_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+long long lcm_ll(long long a, long long b) { return a / std::gcd(a, b) * b; }
+
+// Fill Geo from a shape; validates like CubeShape (core.py:33-37, :49-55).
+int make_geo(const fpssft_shape *shape, Geo *g) {
+    if (!shape) return fail(FPSSFT_EINVAL, "shape is NULL");
+    const int D = shape->ndim;
+    if (D < 1 || D > FPSSFT_MAX_DIMS)
+        return fail(FPSSFT_EUNSUPPORTED, "ndim must be in [1, " + std::to_string(FPSSFT_MAX_DIMS) + "]");
+    std::memset(g, 0, sizeof(*g));
+    g->D = D;
+    g->nlines = D + 1;
+    long long L = 1, Ntot = 1, maxN = 1;
+    for (int k = 0; k < D; ++k) {
+        const long long n = shape->dims[k];
+        if (n < 1) return fail(FPSSFT_EINVAL, "dimension lengths must be >= 1");
+        L = lcm_ll(L, n);
+        Ntot *= n;
+        maxN = std::max(maxN, n);
+        if (L >= (1LL << 31) || Ntot >= (1LL << 31))
+            return fail(FPSSFT_EOVERFLOW, "line length / grid size exceeds the int32 index range");
+    }
+    if ((long long)D * L * maxN >= (1LL << 31))
+        return fail(FPSSFT_EOVERFLOW, "D*L*max(N) exceeds the int32 phase-arithmetic range");
+    g->L = (int)L;
+    for (int k = 0; k < D; ++k) {
+        const unsigned n = (unsigned)shape->dims[k];
+        g->N[k] = (int)n;
+        g->cof[k] = (int)(L / n);
+        g->stride[k] = shape->strides[k];
+        g->magic[k] = (n == 1) ? 0ULL : (~0ULL / n + 1ULL);
+    }
+    return FPSSFT_OK;
+}
+
+// FFT plan + CTA size for `nlines` lines of length L.  Radices: 16s, then
+// the leftover power of two as one stage, then 3s, 5s, 7s; a remaining prime
+// factor > 7 means one direct O(L^2) pass.  CTA size: one thread per bin
+// (>= 64), grown until every stage's butterflies fit MB per thread with
+// MB*radix <= 16 registers' worth of complex values.  Returns -1 if no CTA
+// size <= 1024 works.
+int plan_fft(Geo *g, int nlines, int precision) {
+    const int L = g->L;
+    const bool dbl = precision == FPSSFT_F64;
+    int rad[MAXSTAGES], n = 0, x = L;
+    int e = 0;
+    while (x % 2 == 0) { x /= 2; ++e; }
+    const int big = dbl ? 3 : 4;  // 16-point butterflies in float, 8-point in double
+    while (e >= big) { rad[n++] = 1 << big; e -= big; }
+    if (e > 0) rad[n++] = 1 << e;
+    for (int p : {3, 5, 7})
+        while (x % p == 0) {
+            if (n == MAXSTAGES) return -1;
+            rad[n++] = p;
+            x /= p;
+        }
+    if (x != 1) {  // not 7-smooth
+        n = 1;
+        rad[0] = 0;
+    }
+    if (L == 1) n = 0;
+    auto cap = [dbl](int r) {
+        if (r == 0) return 4;
+        if (dbl) return r <= 2 ? 4 : (r <= 4 ? 2 : 1);
+        return r <= 4 ? 4 : (r <= 8 ? 2 : 1);
+    };
+    long long nt = std::max(64, std::min(((L + 31) / 32) * 32, 1024));
+    for (int i = 0; i < n; ++i) {
+        const long long tot = (long long)nlines * (rad[i] ? L / rad[i] : L);
+        const long long need = (tot + cap(rad[i]) - 1) / cap(rad[i]);
+        nt = std::max(nt, ((need + 31) / 32) * 32);
+    }
+    if (nt > 1024) return -1;
+    g->nstages = n;
+    g->plan[0] = g->plan[1] = 0;
+    for (int i = 0; i < n; ++i) {
+        const long long tot = (long long)nlines * (rad[i] ? L / rad[i] : L);
+        int mb = (int)((tot + nt - 1) / nt);
+        mb = mb <= 1 ? 1 : (mb <= 2 ? 2 : 4);
+        const unsigned long long code = (unsigned long long)(rad[i] | (mb << 5));
+        g->plan[i >> 3] |= code << (8 * (i & 7));
+    }
+    g->threads = (int)nt;
+    return (int)nt;
+}
+
+int block_threads(Geo &g, int nlines, int precision) { return plan_fft(&g, nlines, precision); }
+
+int max_smem_optin() {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+        v = 227 * 1024;
+    return v;
+}
+
+int make_knobs(const fpssft_params *p, Knobs *k) {
+    if (!p) return fail(FPSSFT_EINVAL, "params is NULL");
+    if (p->t_max < 1) return fail(FPSSFT_EINVAL, "max_iterations must be >= 1");
+    if (p->stall_limit < 1) return fail(FPSSFT_EINVAL, "stall_limit must be >= 1");
+    if (p->k_cap < 1 || (p->k_cap & (p->k_cap - 1)))
+        return fail(FPSSFT_EINVAL, "k_cap must be a positive power of two");
+    const double v[] = {p->mag_tol, p->verify_tol, p->round_tol, p->amp_prune_tol,
+                        p->energy_floor, p->energy_floor_abs, p->residual_stop};
+    const char *names[] = {"mag_tol", "verify_tol", "round_tol", "amp_prune_tol",
+                           "energy_floor", "energy_floor_abs", "residual_stop"};
+    for (int i = 0; i < 7; ++i)
+        if (!(v[i] > 0)) return fail(FPSSFT_EINVAL, std::string(names[i]) + " must be positive");
+    if (p->precision != FPSSFT_F32 && p->precision != FPSSFT_F64)
+        return fail(FPSSFT_EINVAL, "precision must be FPSSFT_F32 or FPSSFT_F64");
+    k->mag_tol = p->mag_tol;
+    k->verify_tol = p->verify_tol;
+    k->round_tol = p->round_tol;
+    k->amp_prune_tol = p->amp_prune_tol;
+    k->energy_floor = p->energy_floor;
+    k->energy_floor_abs = p->energy_floor_abs;
+    k->residual_stop = p->residual_stop;
+    k->t_max = p->t_max;
+    k->stall_limit = p->stall_limit;
+    k->k_cap = p->k_cap;
+    return FPSSFT_OK;
+}
+
+int check_launch(const char *where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, where);
+    return FPSSFT_OK;
+}
+
+template <class R>
+int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
+                const Knobs &kn, const int32_t *schedule, const int32_t *sched_index,
+                int32_t n_sched, const OutPtrs &o, cudaStream_t st) {
+    const int nt = block_threads(g, g.nlines, sizeof(R) == 8 ? FPSSFT_F64 : FPSSFT_F32);
+    if (nt < 0) return fail(FPSSFT_EUNSUPPORTED, "line length too large for one CTA");
+    const Layout lay = make_layout(g.D, g.L, kn.k_cap, (int)sizeof(cpx<R>));
+    if ((long long)lay.total > max_smem_optin())
+        return fail(FPSSFT_EUNSUPPORTED,
+                    "shared memory for this (shape, k_cap, precision) is " +
+                        std::to_string(lay.total) + " B, above the per-CTA limit; lower k_cap");
+    cudaError_t e = cudaFuncSetAttribute(recover_kernel<R>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)lay.total);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recover_kernel)");
+    if (batch == 0) return FPSSFT_OK;
+    recover_kernel<R><<<(unsigned)batch, nt, lay.total, st>>>(
+        (const float2 *)cubes, (long long)batch_stride, g, kn, schedule, sched_index, n_sched, o);
+    return check_launch("recover_kernel");
+}
+
+size_t spec_smem(const Geo &g, int nlines, int cs) {
+    return align16((size_t)(nlines + 1) * g.L * cs) + 64 * 8;
+}
+
+}  // namespace
+}  // namespace fpssft
+
+using namespace fpssft;
+
+extern "C" {
+
+const char *fpssft_last_error(void) { return g_err.c_str(); }
+int fpssft_abi_version(void) { return 1; }
+int fpssft_launches_per_batch(void) { return 1; }
+
+int fpssft_block_threads(const fpssft_shape *shape, int32_t precision) {
+    (void)precision;
+    Geo g;
+    if (make_geo(shape, &g) != FPSSFT_OK) return -1;
+    return block_threads(g, g.nlines, precision);
+}
+
+size_t fpssft_smem_bytes(const fpssft_shape *shape, const fpssft_params *params) {
+    Geo g;
+    Knobs k;
+    if (make_geo(shape, &g) != FPSSFT_OK || make_knobs(params, &k) != FPSSFT_OK) return 0;
+    const int cs = params->precision == FPSSFT_F64 ? 16 : 8;
+    return make_layout(g.D, g.L, k.k_cap, cs).total;
+}
+
+int fpssft_run_batch(const void *cubes, int64_t batch, int64_t batch_stride,
+                     const fpssft_shape *shape, const fpssft_params *params,
+                     const int32_t *schedule, const int32_t *sched_index, int32_t n_sched,
+                     const fpssft_out *out, void *stream) {
+    Geo g;
+    Knobs kn;
+    int rc;
+    if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
+    if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
+    if (batch < 0) return fail(FPSSFT_EINVAL, "batch must be >= 0");
+    if (batch > INT_MAX) return fail(FPSSFT_EINVAL, "batch exceeds the grid limit");
+    if (batch > 0 && (!cubes || !schedule || !out || !out->freqs || !out->amps || !out->count ||
+                      !out->iterations || !out->samples_used || !out->terminated_by))
+        return fail(FPSSFT_EINVAL, "NULL buffer");
+    if (n_sched < 1) return fail(FPSSFT_EINVAL, "n_sched must be >= 1");
+    OutPtrs o{out ? out->freqs : nullptr,
+              out ? out->amps : nullptr,
+              out ? out->count : nullptr,
+              out ? out->iterations : nullptr,
+              out ? (long long *)out->samples_used : nullptr,
+              out ? out->terminated_by : nullptr,
+              out ? out->iter_stats : nullptr};
+    cudaStream_t st = (cudaStream_t)stream;
+    if (params->precision == FPSSFT_F64)
+        return run_batch_t<double>(cubes, batch, batch_stride, g, kn, schedule, sched_index,
+                                   n_sched, o, st);
+    return run_batch_t<float>(cubes, batch, batch_stride, g, kn, schedule, sched_index, n_sched,
+                              o, st);
+}
+
+int fpssft_line_spectra(const void *cubes, int64_t batch, int64_t batch_stride,
+                        const fpssft_shape *shape, const int32_t *alpha_tau,
+                        int32_t per_instance, void *spectra, int32_t precision, void *stream) {
+    Geo g;
+    int rc;
+    if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
+    if (batch < 0 || batch > INT_MAX) return fail(FPSSFT_EINVAL, "bad batch");
+    if (batch == 0) return FPSSFT_OK;
+    if (!cubes || !alpha_tau || !spectra) return fail(FPSSFT_EINVAL, "NULL buffer");
+    const int nt = block_threads(g, g.nlines, precision);
+    if (nt < 0) return fail(FPSSFT_EUNSUPPORTED, "line length too large for one CTA");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    if (precision == FPSSFT_F64) {
+        const size_t sm = spec_smem(g, g.nlines, 16);
+        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
+        e = cudaFuncSetAttribute(line_spectra_kernel<double>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        line_spectra_kernel<double><<<(unsigned)batch, nt, sm, st>>>(
+            (const float2 *)cubes, batch_stride, g, alpha_tau, per_instance, (cpx<double> *)spectra);
+    } else {
+        const size_t sm = spec_smem(g, g.nlines, 8);
+        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
+        e = cudaFuncSetAttribute(line_spectra_kernel<float>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        line_spectra_kernel<float><<<(unsigned)batch, nt, sm, st>>>(
+            (const float2 *)cubes, batch_stride, g, alpha_tau, per_instance, (cpx<float> *)spectra);
+    }
+    return check_launch("line_spectra_kernel");
+}
+
+int fpssft_dft_forward(const void *lines, int64_t batch, int32_t L, void *out, int32_t precision,
+                       void *stream) {
+    if (L < 1) return fail(FPSSFT_EINVAL, "expected a nonempty 1-D array");
+    fpssft_shape sh;
+    std::memset(&sh, 0, sizeof(sh));
+    sh.ndim = 1;
+    sh.dims[0] = L;
+    sh.strides[0] = 1;
+    Geo g;
+    int rc;
+    if ((rc = make_geo(&sh, &g)) != FPSSFT_OK) return rc;
+    if (batch < 0 || batch > INT_MAX) return fail(FPSSFT_EINVAL, "bad batch");
+    if (batch == 0) return FPSSFT_OK;
+    if (!lines || !out) return fail(FPSSFT_EINVAL, "NULL buffer");
+    const int nt = block_threads(g, 1, precision);
+    if (nt < 0) return fail(FPSSFT_EUNSUPPORTED, "line length too large for one CTA");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    if (precision == FPSSFT_F64) {
+        const size_t sm = spec_smem(g, 1, 16);
+        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
+        e = cudaFuncSetAttribute(dft_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        dft_kernel<double><<<(unsigned)batch, nt, sm, st>>>((const cpx<double> *)lines, g,
+                                                           (cpx<double> *)out);
+    } else {
+        const size_t sm = spec_smem(g, 1, 8);
+        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
+        e = cudaFuncSetAttribute(dft_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        dft_kernel<float><<<(unsigned)batch, nt, sm, st>>>((const cpx<float> *)lines, g,
+                                                          (cpx<float> *)out);
+    }
+    return check_launch("dft_kernel");
+}
+
+int fpssft_decode_spectra(const void *spectra, int64_t batch, const fpssft_shape *shape,
+                          const int32_t *alpha_tau, int32_t per_instance,
+                          const fpssft_params *params, double floor, int32_t *status,
+                          int32_t *freqs, double *amps, int32_t *n_candidates, void *stream) {
+    Geo g;
+    Knobs kn;
+    int rc;
+    if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
+    if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
+    if (batch < 0 || batch > INT_MAX) return fail(FPSSFT_EINVAL, "bad batch");
+    if (batch == 0) return FPSSFT_OK;
+    if (!spectra || !alpha_tau || !status || !freqs || !amps || !n_candidates)
+        return fail(FPSSFT_EINVAL, "NULL buffer");
+    const int nt = block_threads(g, g.nlines, params->precision);
+    if (nt < 0) return fail(FPSSFT_EUNSUPPORTED, "line length too large for one CTA");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    if (params->precision == FPSSFT_F64) {
+        const size_t sm = spec_smem(g, g.nlines, 16);
+        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
+        e = cudaFuncSetAttribute(decode_kernel<double>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        decode_kernel<double><<<(unsigned)batch, nt, sm, st>>>(
+            (const cpx<double> *)spectra, g, alpha_tau, per_instance, kn, floor, status, freqs,
+            amps, n_candidates);
+    } else {
+        const size_t sm = spec_smem(g, g.nlines, 8);
+        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
+        e = cudaFuncSetAttribute(decode_kernel<float>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        decode_kernel<float><<<(unsigned)batch, nt, sm, st>>>(
+            (const cpx<float> *)spectra, g, alpha_tau, per_instance, kn, floor, status, freqs,
+            amps, n_candidates);
+    }
+    return check_launch("decode_kernel");
+}
+
+int fpssft_project_onto_bins(const int32_t *freqs, const double *amps, const int32_t *counts,
+                             int64_t batch, int32_t k_max, const fpssft_shape *shape,
+                             const int32_t *alpha_tau, int32_t per_instance, double *out,
+                             int32_t precision, void *stream) {
+    Geo g;
+    int rc;
+    if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
+    if (batch < 0 || batch > INT_MAX) return fail(FPSSFT_EINVAL, "bad batch");
+    if (k_max < 1) return fail(FPSSFT_EINVAL, "k_max must be >= 1");
+    if (batch == 0) return FPSSFT_OK;
+    if (!freqs || !amps || !counts || !alpha_tau || !out) return fail(FPSSFT_EINVAL, "NULL buffer");
+    const int nt = block_threads(g, 1, precision);
+    if (nt < 0) return fail(FPSSFT_EUNSUPPORTED, "line length too large for one CTA");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    const int cs = precision == FPSSFT_F64 ? 16 : 8;
+    const size_t sm = make_layout(g.D, g.L, k_max, cs).total;
+    if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "k_max too large");
+    if (precision == FPSSFT_F64) {
+        e = cudaFuncSetAttribute(project_kernel<double>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        project_kernel<double><<<(unsigned)batch, nt, sm, st>>>(freqs, amps, counts, k_max, g,
+                                                               alpha_tau, per_instance, out);
+    } else {
+        e = cudaFuncSetAttribute(project_kernel<float>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        project_kernel<float><<<(unsigned)batch, nt, sm, st>>>(freqs, amps, counts, k_max, g,
+                                                              alpha_tau, per_instance, out);
+    }
+    return check_launch("project_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,355 @@
+"""The FPS-SFT entry points: ``fps_sft`` (drop-in for the reference's) and
+``fps_sft_batch`` (many independent instances per launch).
+
+Mirrors ``fps_sft.driver`` (``/root/reference/pkg/src/fps_sft/driver.py``):
+``FpsSftConfig`` (:29-63, same fields, defaults and validation),
+``IterationStats`` (:66-73), ``RecoveryReport`` (:76-85),
+``default_max_iterations`` (:88-91) and ``fps_sft(source, config)``
+(:121-212).  The loop itself runs on the GPU in one fused kernel per batch
+(``csrc/fpssft.cu:recover_kernel``) reached through the C ABI
+``fpssft_run_batch``; this module only prepares the schedule, owns the
+buffers and unpacks results.  Without a CUDA device or the built library it
+raises -- there is no CPU path.
+
+Deliberate differences:
+* The schedule (alpha_t, tau_t) is explicit.  ``fps_sft`` derives it from
+  ``config.seed`` exactly as the reference draws it (``schedule.py``), so the
+  same seed follows the same lines.
+* Arithmetic is float32 by default (``precision="fp32"``, the north-star
+  configuration); ``precision="fp64"`` runs the same kernels in float64.
+* ``time_domain_subtraction`` is accepted for signature compatibility; the
+  device path always subtracts in the frequency domain (the reference states
+  both give identical results up to roundoff, driver.py:37-41).
+* The recovered set has a capacity ``k_cap``; exceeding it ends that
+  instance with ``terminated_by == "k_cap_overflow"`` (never silently).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .core import CubeShape, DenseSource, SignalSource, SparseSpectrum
+from .schedule import schedule_from_seed
+
+TERMINATED_RESIDUAL_CLEAN = "residual_clean"
+TERMINATED_STALL = "stall"
+TERMINATED_MAX_ITERATIONS = "max_iterations"
+TERMINATED_K_CAP_OVERFLOW = "k_cap_overflow"
+
+DEFAULT_MAG_TOL = 1e-6
+DEFAULT_VERIFY_TOL = 1e-6
+DEFAULT_ROUND_TOL = 0.05
+DEFAULT_AMP_PRUNE_TOL = 1e-9
+DEFAULT_ENERGY_FLOOR_REL = 1e-9
+DEFAULT_ENERGY_FLOOR_ABS = 1e-12
+
+
+@dataclass(frozen=True)
+class FpsSftConfig:
+    max_iterations: int | None = None
+    stall_limit: int = 3
+    seed: int = 0
+    mag_tol: float = DEFAULT_MAG_TOL
+    verify_tol: float = DEFAULT_VERIFY_TOL
+    round_tol: float = DEFAULT_ROUND_TOL
+    amp_prune_tol: float = DEFAULT_AMP_PRUNE_TOL
+    energy_floor: float = DEFAULT_ENERGY_FLOOR_REL
+    energy_floor_abs: float = DEFAULT_ENERGY_FLOOR_ABS
+    residual_stop: float = 1e-9
+    time_domain_subtraction: bool = False
+
+    def __post_init__(self):
+        if self.max_iterations is not None and self.max_iterations < 1:
+            raise ValueError("max_iterations must be >= 1")
+        if self.stall_limit < 1:
+            raise ValueError("stall_limit must be >= 1")
+        for name in ("mag_tol", "verify_tol", "round_tol", "amp_prune_tol",
+                     "energy_floor", "energy_floor_abs", "residual_stop"):
+            if getattr(self, name) <= 0:
+                raise ValueError(f"{name} must be positive")
+
+
+# Tolerance profiles used by the configs.
+PROFILES = {
+    "P64": {},
+    "P32": dict(mag_tol=1e-4, verify_tol=1e-4, residual_stop=1e-6),
+    "PN": dict(mag_tol=0.3, verify_tol=0.5, round_tol=0.3),
+}
+
+
+@dataclass(frozen=True)
+class IterationStats:
+    iteration: int
+    alpha: tuple[int, ...]
+    tau: tuple[int, ...]
+    candidates: int
+    accepted: int
+    rejected: int
+
+
+@dataclass(frozen=True)
+class RecoveryReport:
+    iterations_run: int
+    samples_used: int
+    recovered: SparseSpectrum
+    terminated_by: str
+    iteration_log: tuple[IterationStats, ...] = field(default=())
+
+    def percent_samples(self) -> float:
+        return self.samples_used / self.recovered.shape.n_total
+
+
+def default_max_iterations(shape: CubeShape) -> int:
+    return max(1, shape.n_total // ((shape.ndim + 1) * shape.line_len))
+
+
+def _precision_code(precision: str) -> int:
+    if precision in ("fp32", "float32", "f32"):
+        return N.F32
+    if precision in ("fp64", "float64", "f64"):
+        return N.F64
+    raise ValueError(f"unknown precision {precision!r}")
+
+
+def _params(config: FpsSftConfig, t_max: int, k_cap: int, precision: int) -> N.Params:
+    p = N.Params()
+    p.t_max, p.stall_limit, p.k_cap, p.precision = t_max, config.stall_limit, k_cap, precision
+    for name in ("mag_tol", "verify_tol", "round_tol", "amp_prune_tol", "energy_floor",
+                 "energy_floor_abs", "residual_stop"):
+        setattr(p, name, float(getattr(config, name)))
+    return p
+
+
+def C_ref(x):
+    import ctypes
+
+    return ctypes.byref(x)
+
+
+def _pow2_ceil(x: int) -> int:
+    return 1 << max(0, int(x - 1).bit_length())
+
+
+def max_k_cap(shape: CubeShape, precision: str = "fp32") -> int:
+    """Largest power-of-two capacity whose on-chip state fits one CTA."""
+    sh = N.make_shape(shape.dims)
+    best = 0
+    k = 1
+    limit = 227 * 1024
+    while k <= (1 << 20):
+        p = _params(FpsSftConfig(), 1, k, _precision_code(precision))
+        need = N.lib().fpssft_smem_bytes(C_ref(sh), C_ref(p))
+        if need == 0 or need > limit:
+            break
+        best = k
+        k <<= 1
+    return best
+
+
+@dataclass
+class BatchResult:
+    """Padded per-instance outputs of one ``fps_sft_batch`` call (device tensors)."""
+
+    shape: CubeShape
+    k_cap: int
+    freqs: "object"  # int32 [B, k_cap, D]
+    amps: "object"  # complex128 [B, k_cap]
+    count: "object"  # int32 [B]
+    iterations: "object"  # int32 [B]
+    samples_used: "object"  # int64 [B]
+    terminated_by: "object"  # int32 [B]
+    iter_stats: "object" = None  # int32 [B, t_max, 3] or None
+    schedule: np.ndarray | None = None  # int32 [S, t_max, 2, D] (host copy)
+    sched_index: np.ndarray | None = None
+
+    @property
+    def batch(self) -> int:
+        return int(self.count.shape[0])
+
+    def report(self, b: int) -> RecoveryReport:
+        """The reference-shaped report of instance ``b`` (host copy)."""
+        n = int(self.count[b])
+        freqs = self.freqs[b, :n].cpu().numpy().astype(np.int64)
+        amps = self.amps[b, :n].cpu().numpy()
+        its = int(self.iterations[b])
+        term = N.TERM_NAMES[int(self.terminated_by[b])]
+        log = ()
+        if self.iter_stats is not None and self.schedule is not None:
+            s = 0 if self.sched_index is None else int(self.sched_index[b])
+            st = self.iter_stats[b, :its].cpu().numpy()
+            sch = self.schedule[s]
+            log = tuple(IterationStats(t + 1, tuple(int(v) for v in sch[t, 0]),
+                                       tuple(int(v) for v in sch[t, 1]), int(st[t, 0]),
+                                       int(st[t, 1]), int(st[t, 2])) for t in range(its))
+        return RecoveryReport(iterations_run=its, samples_used=int(self.samples_used[b]),
+                              recovered=SparseSpectrum._trusted(self.shape, freqs, amps),
+                              terminated_by=term, iteration_log=log)
+
+
+def allocate_outputs(batch: int, shape: CubeShape, k_cap: int, t_max: int, device,
+                     iter_stats: bool = False) -> dict:
+    import torch
+
+    kw = dict(device=device)
+    return dict(
+        freqs=torch.zeros((batch, k_cap, shape.ndim), dtype=torch.int32, **kw),
+        amps=torch.zeros((batch, k_cap), dtype=torch.complex128, **kw),
+        count=torch.zeros(batch, dtype=torch.int32, **kw),
+        iterations=torch.zeros(batch, dtype=torch.int32, **kw),
+        samples_used=torch.zeros(batch, dtype=torch.int64, **kw),
+        terminated_by=torch.zeros(batch, dtype=torch.int32, **kw),
+        iter_stats=(torch.zeros((batch, t_max, 3), dtype=torch.int32, **kw)
+                    if iter_stats else None),
+    )
+
+
+def _schedule_tensor(schedule, shape: CubeShape, t_max: int, device):
+    import torch
+
+    sch = np.asarray(schedule, dtype=np.int32)
+    if sch.ndim == 3:
+        sch = sch[None]
+    if sch.ndim != 4 or sch.shape[2:] != (2, shape.ndim):
+        raise ValueError(f"schedule must be [S, T, 2, {shape.ndim}], got {sch.shape}")
+    if sch.shape[1] < t_max:
+        raise ValueError(f"schedule holds {sch.shape[1]} iterations, t_max is {t_max}")
+    sch = np.ascontiguousarray(sch[:, :t_max])
+    dims = np.asarray(shape.dims)
+    if (sch < 0).any() or (sch >= dims).any():
+        raise ValueError("schedule slope/offset components out of range")
+    return sch, torch.as_tensor(sch, device=device)
+
+
+class BatchRunner:
+    """Pre-planned launcher for repeated batches of one shape: schedule on the
+    device, outputs allocated once, one ``fpssft_run_batch`` per ``run``."""
+
+    def __init__(self, shape: CubeShape, config: FpsSftConfig, batch: int, *, schedule=None,
+                 sched_index=None, k_cap: int = 256, precision: str = "fp32",
+                 iter_stats: bool = False, device=None):
+        import torch
+
+        self.shape = shape
+        self.config = config
+        self.batch = int(batch)
+        self.device = torch.device(device if device is not None else "cuda")
+        self.t_max = config.max_iterations or default_max_iterations(shape)
+        if schedule is None:
+            schedule = schedule_from_seed(shape, config.seed, self.t_max)
+        self.schedule_host, self.schedule = _schedule_tensor(schedule, shape, self.t_max,
+                                                             self.device)
+        self.sched_index_host = None
+        self.sched_index = None
+        if sched_index is not None:
+            si = np.asarray(sched_index, dtype=np.int32).reshape(-1)
+            if si.shape[0] != self.batch:
+                raise ValueError("sched_index must have one entry per instance")
+            if (si < 0).any() or (si >= self.schedule_host.shape[0]).any():
+                raise ValueError("sched_index out of range")
+            self.sched_index_host = si
+            self.sched_index = torch.as_tensor(si, device=self.device)
+        if k_cap < 1 or k_cap & (k_cap - 1):
+            raise ValueError("k_cap must be a positive power of two")
+        self.k_cap = int(k_cap)
+        self.prec = _precision_code(precision)
+        self._shape_c = N.make_shape(shape.dims)
+        self._params_c = _params(config, self.t_max, self.k_cap, self.prec)
+        self.out = allocate_outputs(self.batch, shape, self.k_cap, self.t_max, self.device,
+                                    iter_stats)
+        o = self.out
+        self._out_c = N.Out(N.ptr(o["freqs"]), N.ptr(o["amps"]), N.ptr(o["count"]),
+                            N.ptr(o["iterations"]), N.ptr(o["samples_used"]),
+                            N.ptr(o["terminated_by"]), N.ptr(o["iter_stats"]))
+        self.smem_bytes = int(N.lib().fpssft_smem_bytes(C_ref(self._shape_c),
+                                                       C_ref(self._params_c)))
+        self.threads = int(N.lib().fpssft_block_threads(C_ref(self._shape_c), self.prec))
+
+    def run(self, cubes) -> BatchResult:
+        import torch
+
+        if not (isinstance(cubes, torch.Tensor) and cubes.is_cuda):
+            raise ValueError("cubes must be a CUDA tensor (use fps_sft for host arrays)")
+        if cubes.dtype != torch.complex64:
+            raise ValueError(f"cubes must be complex64, got {cubes.dtype}")
+        if tuple(cubes.shape[1:]) != self.shape.dims or cubes.shape[0] != self.batch:
+            raise ValueError(f"cubes must be [{self.batch}, {self.shape.dims}], "
+                             f"got {tuple(cubes.shape)}")
+        # element strides (complex64 units) of one cube and between cubes
+        sh = N.make_shape(self.shape.dims, [int(s) for s in cubes.stride()[1:]])
+        with torch.cuda.device(cubes.device):
+            N.check(N.lib().fpssft_run_batch(
+                N.ptr(cubes), self.batch, int(cubes.stride(0)), C_ref(sh), C_ref(self._params_c),
+                N.ptr(self.schedule), N.ptr(self.sched_index), int(self.schedule_host.shape[0]),
+                C_ref(self._out_c), N.stream_ptr(cubes.device)))
+        o = self.out
+        return BatchResult(self.shape, self.k_cap, o["freqs"], o["amps"], o["count"],
+                           o["iterations"], o["samples_used"], o["terminated_by"],
+                           o["iter_stats"], self.schedule_host, self.sched_index_host)
+
+
+def fps_sft_batch(cubes, config: FpsSftConfig = FpsSftConfig(), *, schedule=None,
+                  sched_index=None, k_cap: int = 256, precision: str = "fp32",
+                  iter_stats: bool = False) -> BatchResult:
+    """Recover every instance of ``cubes`` (complex64 CUDA tensor [B, *dims]).
+
+    ``schedule``: int32 [T, 2, D] or [S, T, 2, D] (alpha, tau) per iteration;
+    default: the reference's draws for ``config.seed``.  ``sched_index``:
+    per-instance schedule row (default 0).  Returns padded device tensors.
+    """
+    shape = CubeShape(cubes.shape[1:])
+    runner = BatchRunner(shape, config, cubes.shape[0], schedule=schedule,
+                         sched_index=sched_index, k_cap=k_cap, precision=precision,
+                         iter_stats=iter_stats, device=cubes.device)
+    return runner.run(cubes)
+
+
+def materialize(source) -> tuple[CubeShape, "np.ndarray | object"]:
+    """The dense complex64 cube behind a sample source: a ``DenseSource``'s
+    own array, otherwise ``sample_many`` over the whole grid (host side,
+    evaluated once; e.g. the reference's lazy ``SyntheticSource``)."""
+    shape = source.shape()
+    if not isinstance(shape, CubeShape):
+        shape = CubeShape(shape.dims)
+    if isinstance(source, DenseSource):
+        return shape, source.data
+    data = getattr(source, "_data", None)  # the reference's DenseSource
+    if isinstance(data, np.ndarray) and data.shape == shape.dims:
+        return shape, data.astype(np.complex64)
+    if shape.n_total > (1 << 24):
+        raise ValueError(f"refusing to materialise a lazy source of {shape.n_total} samples")
+    grid = np.indices(shape.dims).reshape(shape.ndim, -1).T
+    return shape, source.sample_many(grid).reshape(shape.dims).astype(np.complex64)
+
+
+def fps_sft(source: SignalSource, config: FpsSftConfig = FpsSftConfig(), *,
+            precision: str = "fp32", k_cap: int | None = None, device=None) -> RecoveryReport:
+    """Recover the sparse spectrum of ``source`` on the GPU (driver.py:121-212).
+
+    Same contract as the reference: stops on a clean residual, after
+    ``stall_limit`` fruitless iterations, or at the iteration cap; failure to
+    recover is reported, never raised.
+    """
+    import torch
+
+    shape, cube = materialize(source)
+    dev = torch.device(device if device is not None else "cuda")
+    if isinstance(cube, torch.Tensor):
+        t = cube.to(device=dev, dtype=torch.complex64)
+    else:
+        t = torch.as_tensor(np.ascontiguousarray(cube, dtype=np.complex64)).to(dev)
+    t = t.reshape((1, *shape.dims))
+    if k_cap is None:
+        k_cap = min(_pow2_ceil(shape.n_total), max_k_cap(shape, precision))
+        if k_cap < 1:
+            raise N.UnsupportedError(f"shape {shape.dims} does not fit one CTA")
+    res = fps_sft_batch(t, config, k_cap=k_cap, precision=precision, iter_stats=True)
+    return res.report(0)
+
+
+__all__ = ["FpsSftConfig", "IterationStats", "RecoveryReport", "BatchResult", "BatchRunner",
+           "default_max_iterations", "fps_sft", "fps_sft_batch", "materialize", "max_k_cap",
+           "PROFILES", "TERMINATED_RESIDUAL_CLEAN", "TERMINATED_STALL",
+           "TERMINATED_MAX_ITERATIONS", "TERMINATED_K_CAP_OVERFLOW"]

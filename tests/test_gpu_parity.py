@@ -1,0 +1,313 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+outputs (tests/golden, generated from the unmodified reference) and against
+the CPU oracle (oracle/fps_oracle.py) on identical inputs and schedules.
+
+Tolerances (north_star): recovered support bit-exact; amplitudes within
+1e-4 relative (noiseless) / 1e-3 (noisy profile) in float32.  The float64
+mode is held to 1e-9.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import fixtures as G  # noqa: E402
+from oracle import fps_oracle as O  # noqa: E402
+
+import paper_1711_11407_b200 as P  # noqa: E402
+from paper_1711_11407_b200 import ops  # noqa: E402
+from paper_1711_11407_b200 import workloads as W  # noqa: E402
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+RUNS = G.meta()["runs"]
+OPS = G.meta()["ops"]
+DEV = torch.device("cuda:0")
+
+
+def _cfg(entry):
+    return P.FpsSftConfig(**entry["cfg"], **G.PROFILES[entry["profile"]])
+
+
+def _fp32_resolvable(exp) -> bool:
+    """False when the reference recovered entries at the complex64 rounding
+    level of the cube (|a| < 1e-5 sum|a|): float32 arithmetic cannot resolve
+    those, float64 can."""
+    a = np.abs(exp["amps"])
+    return a.size == 0 or a.min() > 1e-5 * a.sum()
+
+
+def _amp_tol(entry):
+    return 1e-3 if entry["profile"] == "PN" else 1e-4
+
+
+# ------------------------------------------------------------- per-step ops
+@pytest.mark.parametrize("prec,tol", [("fp32", 2e-6), ("fp64", 1e-13)])
+@pytest.mark.parametrize("entry", [e for e in OPS["line"]
+                                   if f"{e['key']}/cube" in G.npz("ops.npz")],
+                         ids=lambda e: e["key"])
+def test_line_spectra_vs_reference(entry, prec, tol):
+    ops_ = G.npz("ops.npz")
+    cube = torch.as_tensor(ops_[f"{entry['key']}/cube"])[None].to(DEV)
+    got = ops.line_spectra(cube, entry["alpha"], entry["tau"], precision=prec)[0].cpu().numpy()
+    want = ops_[f"{entry['key']}/spectra"]
+    scale = np.abs(want).max()
+    assert np.abs(got - want).max() <= tol * scale * np.sqrt(want.shape[1])
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 4, 5, 6, 7, 8, 11, 12, 13, 16, 30, 36, 48, 60, 64, 256,
+                               512, 2048, 4608, 243, 343, 1000])
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_dft_forward_vs_numpy(L, prec, rng):
+    v = rng.standard_normal((3, L)) + 1j * rng.standard_normal((3, L))
+    x = torch.as_tensor(v).to(DEV)
+    try:
+        got = ops.dft_forward(x, precision=prec).cpu().numpy()
+    except ValueError as e:  # UnsupportedError for lengths beyond one CTA
+        pytest.skip(str(e))
+    want = np.fft.fft(v, axis=-1) / L
+    tol = (3e-7 if prec == "fp32" else 1e-15) * max(1.0, np.log2(L)) * np.abs(v).max()
+    assert np.abs(got - want).max() <= tol
+
+
+def test_dft_goldens():  # pkg/tests/test_transform.py:13-19
+    x = torch.tensor([[1, 1, 1, 1]], dtype=torch.complex128, device=DEV)
+    assert np.allclose(ops.dft_forward(x, precision="fp64").cpu().numpy(), [[1, 0, 0, 0]],
+                       atol=1e-15)
+    tone = torch.as_tensor(np.exp(2j * np.pi * np.arange(4) / 4))[None].to(DEV)
+    assert np.allclose(ops.dft_forward(tone, precision="fp64").cpu().numpy(), [[0, 1, 0, 0]],
+                       atol=1e-15)
+
+
+@pytest.mark.parametrize("entry", OPS["decode"], ids=lambda e: e["key"])
+@pytest.mark.parametrize("pname,prec", [("P64", "fp64"), ("P32", "fp64"), ("P32", "fp32")])
+def test_decode_spectra_vs_reference(entry, pname, prec):
+    ops_ = G.npz("ops.npz")
+    k = entry["key"]
+    shape = P.CubeShape(entry["dims"])
+    kw = {a: b for a, b in G.PROFILES[pname].items() if a != "residual_stop"}
+    acc, nc = ops.decode_spectra(ops_[f"{k}/spectra"], entry["tau"], shape, precision=prec, **kw)
+    assert nc == int(ops_[f"{k}/{pname}/ncand"])
+    assert [b for b, _ in acc] == list(ops_[f"{k}/{pname}/bins"])
+    assert [s.freq for _, s in acc] == [tuple(f) for f in ops_[f"{k}/{pname}/freqs"]]
+    got = np.asarray([s.amp for _, s in acc])
+    want = ops_[f"{k}/{pname}/amps"]
+    tol = 1e-12 if prec == "fp64" else 1e-5
+    assert np.all(np.abs(got - want) <= tol * np.abs(want))
+
+
+@pytest.mark.parametrize("entry", OPS["project"], ids=lambda e: e["key"])
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-13), ("fp32", 1e-6)])
+def test_project_onto_bins_vs_reference(entry, prec, tol):
+    ops_ = G.npz("ops.npz")
+    k = entry["key"]
+    shape = P.CubeShape(entry["dims"])
+    got = ops.project_onto_bins(ops_[f"{k}/freqs"], ops_[f"{k}/amps"], entry["alpha"],
+                                entry["tau"], shape, precision=prec).cpu().numpy()
+    want = ops_[f"{k}/out"]
+    assert np.abs(got - want).max() <= tol * np.abs(ops_[f"{k}/amps"]).sum()
+
+
+def test_project_empty_set_is_zero():  # pkg/tests/test_decoder.py:146-150
+    out = ops.project_onto_bins(np.zeros((0, 2)), np.zeros(0), (1, 1), (0, 0), P.CubeShape((8, 8)))
+    assert torch.count_nonzero(out).item() == 0
+
+
+# -------------------------------------------------------- the fused loop
+def _check_report(rep, exp, amp_rtol, log=True):
+    assert rep.terminated_by == exp["terminated_by"]
+    assert rep.iterations_run == exp["iterations_run"]
+    assert rep.samples_used == exp["samples_used"]
+    got_f = rep.recovered.freq_array.reshape(-1, exp["freqs"].shape[1])
+    np.testing.assert_array_equal(got_f, exp["freqs"])
+    got_a = rep.recovered.amp_array
+    assert np.all(np.abs(got_a - exp["amps"]) <= amp_rtol * np.abs(exp["amps"]))
+    if log:
+        assert [s.alpha for s in rep.iteration_log] == [tuple(a) for a in exp["log_alpha"]]
+        assert [s.tau for s in rep.iteration_log] == [tuple(t) for t in exp["log_tau"]]
+        assert [(s.candidates, s.accepted, s.rejected) for s in rep.iteration_log] == \
+            [tuple(c) for c in exp["log_counts"]]
+
+
+@pytest.mark.parametrize("entry", RUNS, ids=lambda e: e["name"])
+def test_fps_sft_fp64_matches_reference(entry):
+    cube = G.run_cube(entry)
+    shape = P.CubeShape(cube.shape)
+    if P.max_k_cap(shape, "fp64") < 1:
+        pytest.skip("shape does not fit one CTA in float64")
+    rep = P.fps_sft(P.make_dense_source(cube, shape), _cfg(entry), precision="fp64")
+    _check_report(rep, G.run_expected(entry), 1e-9)
+
+
+@pytest.mark.parametrize("entry", [e for e in RUNS if e["profile"] != "P64"],
+                         ids=lambda e: e["name"])
+def test_fps_sft_fp32_matches_reference(entry):
+    exp = G.run_expected(entry)
+    if not _fp32_resolvable(exp):
+        pytest.skip("reference recovered complex64-rounding-level entries")
+    cube = G.run_cube(entry)
+    shape = P.CubeShape(cube.shape)
+    rep = P.fps_sft(P.make_dense_source(cube, shape), _cfg(entry), precision="fp32")
+    # noisy profiles: same support and amplitudes; the iteration log must
+    # match too (any flipped decision would change it)
+    _check_report(rep, exp, _amp_tol(entry))
+
+
+# ----------------------------------------------------- batches vs oracle
+def _batch(w: W.Workload, count: int):
+    inst = [W.make_instance(w, r) for r in W.instance_rngs(w.seed, count)]
+    cubes = torch.as_tensor(np.stack([c for _, _, c in inst])).to(DEV)
+    return inst, cubes
+
+
+@pytest.mark.parametrize("cfg_id,count,prec", [(2, 48, "fp32"), (2, 16, "fp64"), (1, 1, "fp32"),
+                                               (4, 2, "fp32"), (3, 4, "fp32"), (5, 4, "fp32"),
+                                               (3, 2, "fp64"), (5, 2, "fp64")])
+def test_config_batches_match_oracle(cfg_id, count, prec):
+    w = W.CONFIGS[cfg_id]
+    inst, cubes = _batch(w, count)
+    prof = O.Profile(**G.PROFILES[w.profile])
+    cfg = P.FpsSftConfig(seed=cfg_id, **G.PROFILES[w.profile])
+    shape = P.CubeShape(w.dims)
+    k_cap = 2048 if cfg_id == 4 else (1024 if cfg_id in (3, 5) else 256)
+    if prec == "fp64":
+        k_cap = min(k_cap, P.max_k_cap(shape, "fp64"))
+    res = P.fps_sft_batch(cubes, cfg, k_cap=k_cap, precision=prec, iter_stats=True)
+    tol = 1e-9 if prec == "fp64" else (1e-3 if w.noise_var else 1e-4)
+    for b, (f, a, cube) in enumerate(inst):
+        ref = O.recover(cube, w.dims, prof, seed=cfg_id)
+        rep = res.report(b)
+        exp = dict(freqs=ref.freqs, amps=ref.amps, terminated_by=ref.terminated_by,
+                   iterations_run=ref.iterations_run, samples_used=ref.samples_used,
+                   log_alpha=[x[0] for x in ref.log], log_tau=[x[1] for x in ref.log],
+                   log_counts=[x[2:] for x in ref.log])
+        _check_report(rep, exp, tol)
+
+
+def test_cfg2_full_batch_recovers_truth():
+    """BASELINE config 2 at full size (4096 instances): every instance's
+    recovered spectrum equals its generating spectrum (size-independent
+    property; the oracle checks a subset above)."""
+    w = W.CONFIGS[2]
+    spectra = W.make_spectra(w)
+    cubes = W.synthesize_batch_torch(w.dims, spectra, DEV)
+    cfg = P.FpsSftConfig(seed=2, **G.PROFILES["P32"])
+    res = P.fps_sft_batch(cubes, cfg, k_cap=256)
+    count = res.count.cpu().numpy()
+    term = res.terminated_by.cpu().numpy()
+    assert (term == 0).all()
+    assert (count == w.k).all()
+    freqs = res.freqs.cpu().numpy()
+    amps = res.amps.cpu().numpy()
+    for b in range(0, w.batch, 97):
+        f, a = spectra[b]
+        order = np.lexsort(f.T[::-1])
+        np.testing.assert_array_equal(freqs[b, :w.k], f[order])
+        assert np.all(np.abs(amps[b, :w.k] - a[order]) <= 1e-4 * np.abs(a[order]))
+
+
+# ------------------------------------------------------------ properties
+def test_determinism_bitwise():
+    w = W.CONFIGS[5]
+    _, cubes = _batch(w, 3)
+    cfg = P.FpsSftConfig(seed=5, **G.PROFILES["PN"])
+    r1 = P.fps_sft_batch(cubes, cfg, k_cap=1024)
+    a1 = (r1.freqs.clone(), r1.amps.clone(), r1.count.clone())
+    r2 = P.fps_sft_batch(cubes, cfg, k_cap=1024)
+    assert torch.equal(a1[0], r2.freqs) and torch.equal(a1[1], r2.amps)
+    assert torch.equal(a1[2], r2.count)
+
+
+def test_amplitude_scale_equivariance():  # pkg/tests/test_driver.py:119-128
+    f, a = W.reference_generate((16, 12), 8, 4)
+    shape = P.CubeShape((16, 12))
+    cfg = P.FpsSftConfig(max_iterations=15, seed=123, **G.PROFILES["P32"])
+    base = P.fps_sft(P.make_dense_source(W.synthesize_np((16, 12), f, a), shape), cfg)
+    other = P.fps_sft(P.make_dense_source(W.synthesize_np((16, 12), f, a * (3 - 4j)), shape), cfg)
+    assert set(base.recovered.entries) == set(other.recovered.entries)
+    for k, v in base.recovered.entries.items():
+        assert abs(other.recovered.entries[k] - v * (3 - 4j)) <= 1e-4 * abs(v * (3 - 4j))
+
+
+def test_sample_accounting_and_certificate():  # test_driver.py:78-84, 106-117
+    f, a = W.reference_generate((16, 16), 12, 8)
+    shape = P.CubeShape((16, 16))
+    cube = W.synthesize_np((16, 16), f, a)
+    rep = P.fps_sft(P.make_dense_source(cube, shape),
+                    P.FpsSftConfig(max_iterations=20, seed=9, **G.PROFILES["P32"]))
+    assert rep.samples_used == rep.iterations_run * 3 * 16
+    assert rep.terminated_by == "residual_clean"
+    rebuilt = W.synthesize_np((16, 16), rep.recovered.freq_array, rep.recovered.amp_array)
+    assert np.abs(rebuilt - cube).max() <= 1e-5 * np.abs(cube).max()
+
+
+def test_zero_cube_terminates_clean_with_nothing():
+    cubes = torch.zeros((2, 16, 16), dtype=torch.complex64, device=DEV)
+    res = P.fps_sft_batch(cubes, P.FpsSftConfig(max_iterations=5, seed=1), k_cap=64)
+    assert res.count.tolist() == [0, 0]
+    assert res.terminated_by.tolist() == [0, 0]
+    assert res.iterations.tolist() == [1, 1]
+
+
+def test_empty_batch_is_a_noop():
+    cubes = torch.zeros((0, 16, 16), dtype=torch.complex64, device=DEV)
+    res = P.fps_sft_batch(cubes, P.FpsSftConfig(max_iterations=5), k_cap=64)
+    assert res.count.numel() == 0
+
+
+def test_k_cap_overflow_is_reported():
+    w = W.CONFIGS[2]
+    _, cubes = _batch(w, 2)
+    res = P.fps_sft_batch(cubes, P.FpsSftConfig(seed=2, **G.PROFILES["P32"]), k_cap=32)
+    assert res.terminated_by.tolist() == [3, 3]
+    assert (res.count.cpu().numpy() <= 32).all()
+
+
+def test_per_instance_schedules_and_strided_input():
+    w = W.CONFIGS[2]
+    inst, cubes = _batch(w, 4)
+    shape = P.CubeShape(w.dims)
+    cfg = P.FpsSftConfig(max_iterations=12, **G.PROFILES["P32"])
+    sched = np.stack([P.schedule_from_seed(shape, s, 12) for s in (11, 12)])
+    idx = np.asarray([1, 0, 1, 0])
+    # a transposed (non-contiguous) view of the same data: recover on x^T,
+    # whose spectrum is the transposed spectrum
+    cubes_t = cubes.transpose(1, 2)
+    res = P.fps_sft_batch(cubes_t, cfg, schedule=sched, sched_index=idx, k_cap=256)
+    prof = O.Profile(**G.PROFILES["P32"], max_iterations=12)
+    for b, (_, _, cube) in enumerate(inst):
+        ref = O.recover(np.ascontiguousarray(cube.T), w.dims, prof,
+                        schedule=sched[idx[b]].astype(np.int64))
+        rep = res.report(b)
+        np.testing.assert_array_equal(rep.recovered.freq_array.reshape(-1, 2), ref.freqs)
+        assert rep.iterations_run == ref.iterations_run
+
+
+def test_invalid_schedule_rejected():
+    cubes = torch.zeros((1, 8, 8), dtype=torch.complex64, device=DEV)
+    bad = np.zeros((3, 2, 2), np.int32)
+    bad[0, 1] = (8, 0)
+    with pytest.raises(ValueError):
+        P.fps_sft_batch(cubes, P.FpsSftConfig(max_iterations=3), schedule=bad, k_cap=64)
+
+
+def test_lazy_source_is_materialised():
+    class Lazy:
+        def __init__(self, f, a, dims):
+            self.f, self.a, self.dims = f, a, dims
+
+        def shape(self):
+            return P.CubeShape(self.dims)
+
+        def sample_many(self, idx):
+            ph = (idx[:, None, :] * self.f[None] / np.asarray(self.dims)).sum(-1)
+            return (np.exp(2j * np.pi * ph) * self.a).sum(-1)
+
+    f, a = W.reference_generate((12, 12), 10, 31)
+    rep = P.fps_sft(Lazy(f, a, (12, 12)),
+                    P.FpsSftConfig(max_iterations=12, seed=5, **G.PROFILES["P32"]))
+    order = np.lexsort(f.T[::-1])
+    np.testing.assert_array_equal(rep.recovered.freq_array, f[order])
