@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
@@ -239,16 +240,22 @@ __global__ void __launch_bounds__(1024, 1) recover_kernel(const float2 *__restri
         it_run = it + 1;
 
         // (1) gather + (2) DFT of the D+1 lines           driver.py:146-154
-        gather_lines(spec, cube, g, al, ta);
+        const R my_energy = gather_lines(spec, cube, g, al, ta);
         __syncthreads();
         fft_lines(spec, nl, g, roots);
+        // float32 only: bins below the transform's own rounding floor are
+        // numerically empty ("precision floor")
+        R noise_floor = (R)0;
+        if (sizeof(R) == 4 && kn.noise_coef > 0)
+            noise_floor = (R)kn.noise_coef * sqrt(block_sum(my_energy, rred));
         // (3) construction-subtraction of the recovered set
         if (n_slots > 0)
             project_bins(spec, nl, g, al, ta, n_slots, slot_m, slot_amp, slot_live, bin_start,
                          bin_fill, seg, slot_bin, slot_u0, roots, ired, true);
 
         // (4) classify every bin                            driver.py:156-176
-        const R floor = max((R)kn.energy_floor_abs, (R)kn.energy_floor * amp_sum);
+        const R floor =
+            max(max((R)kn.energy_floor_abs, (R)kn.energy_floor * amp_sum), noise_floor);
         int my_cand = 0, my_acc = 0;
         for (int b = tid; b < L; b += NT) {
             int m[MAXD];
@@ -464,14 +471,21 @@ __global__ void __launch_bounds__(1024, 1) decode_kernel(const cpx<R> *__restric
     }
     build_roots(roots, L);
     const cpx<R> *src = spectra + (long long)inst * g.nlines * L;
-    for (int e = threadIdx.x; e < g.nlines * L; e += blockDim.x) spec[e] = src[e];
+    R my_e = (R)0;
+    for (int e = threadIdx.x; e < g.nlines * L; e += blockDim.x) {
+        spec[e] = src[e];
+        my_e += spec[e].re * spec[e].re + spec[e].im * spec[e].im;
+    }
     __syncthreads();
+    R fl = (R)floor;
+    if (sizeof(R) == 4 && kn.noise_coef > 0)  // sum |x|^2 = L sum |S|^2 (Parseval)
+        fl = max(fl, (R)kn.noise_coef * sqrt((R)L * block_sum(my_e, (R *)(ired + 32))));
     int my = 0;
     for (int b = threadIdx.x; b < L; b += blockDim.x) {
         int m[MAXD] = {0, 0, 0, 0};
         cpx<R> a = {(R)0, (R)0};
         const int st = classify_bin(spec, g, b, al, ta, roots, (R)kn.mag_tol, (R)kn.round_tol,
-                                    (R)kn.verify_tol, (R)floor, m, &a);
+                                    (R)kn.verify_tol, fl, m, &a);
         my += st > 0;
         const long long o = (long long)inst * L + b;
         status[o] = st;
@@ -653,10 +667,23 @@ int make_knobs(const fpssft_params *p, Knobs *k) {
     k->energy_floor = p->energy_floor;
     k->energy_floor_abs = p->energy_floor_abs;
     k->residual_stop = p->residual_stop;
+    k->noise_coef = 0.0;
     k->t_max = p->t_max;
     k->stall_limit = p->stall_limit;
     k->k_cap = p->k_cap;
     return FPSSFT_OK;
+}
+
+// Float32 rounding floor ("precision floor"): a length-L
+// transform's per-bin error is ~ eps sqrt(log2 L + 1) ||x_line|| / L; bins
+// below kappa times that are treated as empty.  Zero in float64 mode, where
+// the reference's own floors are far above the rounding level.
+void set_noise_floor(Knobs *k, const Geo &g, int precision) {
+    const double kappa = 8.0, eps32 = 5.9604644775390625e-08;
+    k->noise_coef = precision == FPSSFT_F64
+                        ? 0.0
+                        : kappa * eps32 * std::sqrt(std::log2((double)g.L) + 1.0) /
+                              ((double)g.L * std::sqrt((double)g.nlines));
 }
 
 int check_launch(const char *where) {
@@ -725,6 +752,7 @@ int fpssft_run_batch(const void *cubes, int64_t batch, int64_t batch_stride,
     int rc;
     if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
     if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
+    set_noise_floor(&kn, g, params->precision);
     if (batch < 0) return fail(FPSSFT_EINVAL, "batch must be >= 0");
     if (batch > INT_MAX) return fail(FPSSFT_EINVAL, "batch exceeds the grid limit");
     if (batch > 0 && (!cubes || !schedule || !out || !out->freqs || !out->amps || !out->count ||
@@ -826,6 +854,7 @@ int fpssft_decode_spectra(const void *spectra, int64_t batch, const fpssft_shape
     int rc;
     if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
     if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
+    set_noise_floor(&kn, g, params->precision);
     if (batch < 0 || batch > INT_MAX) return fail(FPSSFT_EINVAL, "bad batch");
     if (batch == 0) return FPSSFT_OK;
     if (!spectra || !alpha_tau || !status || !freqs || !amps || !n_candidates)

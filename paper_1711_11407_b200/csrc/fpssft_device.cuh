@@ -66,6 +66,7 @@ __host__ __device__ __forceinline__ int stage_code(const Geo &g, int s) {
 struct Knobs {
     double mag_tol, verify_tol, round_tol, amp_prune_tol;
     double energy_floor, energy_floor_abs, residual_stop;
+    double noise_coef;  // float32 rounding floor: coef * sqrt(sum |x|^2 over the D+1 lines)
     int t_max, stall_limit, k_cap;
 };
 
@@ -151,10 +152,12 @@ __device__ __forceinline__ void build_roots(cpx<R> *roots, int L) {
 // (lines.py:36-64).  Row l of offset k+1 differs from offset 0 only in
 // coordinate k, advanced by one with wrap, so each thread issues its D+1
 // loads from one base address.  Index math is fastmod, no division.
+// Returns this thread's share of sum |x|^2 over the gathered samples.
 template <class R>
-__device__ __forceinline__ void gather_lines(cpx<R> *spec, const float2 *__restrict__ cube,
-                                             const Geo &g, const int *al, const int *ta) {
+__device__ __forceinline__ R gather_lines(cpx<R> *spec, const float2 *__restrict__ cube,
+                                          const Geo &g, const int *al, const int *ta) {
     const int L = g.L, D = g.D;
+    R energy = (R)0;
     for (int l = threadIdx.x; l < L; l += blockDim.x) {
         long long base = 0;
         long long delta[MAXD];
@@ -173,10 +176,15 @@ __device__ __forceinline__ void gather_lines(cpx<R> *spec, const float2 *__restr
         for (int k = 0; k < MAXD; ++k)
             if (k < D) v[k + 1] = __ldcs(cube + base + delta[k]);
         spec[l] = {(R)v[0].x, (R)v[0].y};
+        energy += (R)v[0].x * (R)v[0].x + (R)v[0].y * (R)v[0].y;
 #pragma unroll
         for (int k = 0; k < MAXD; ++k)
-            if (k < D) spec[(k + 1) * L + l] = {(R)v[k + 1].x, (R)v[k + 1].y};
+            if (k < D) {
+                spec[(k + 1) * L + l] = {(R)v[k + 1].x, (R)v[k + 1].y};
+                energy += (R)v[k + 1].x * (R)v[k + 1].x + (R)v[k + 1].y * (R)v[k + 1].y;
+            }
     }
+    return energy;
 }
 
 // ------------------------------------------------------------------- FFT
