@@ -35,6 +35,11 @@ extern "C" {
 #define FPSSFT_F32 0
 #define FPSSFT_F64 1
 
+/* execution mode: one warp or one whole CTA per instance (AUTO picks) */
+#define FPSSFT_MODE_AUTO 0
+#define FPSSFT_MODE_CTA 1
+#define FPSSFT_MODE_WARP 2
+
 /* terminated_by codes (driver.py:24-26 plus capacity overflow) */
 #define FPSSFT_TERM_RESIDUAL_CLEAN 0
 #define FPSSFT_TERM_STALL 1
@@ -55,6 +60,7 @@ typedef struct fpssft_params {
     int32_t stall_limit; /* driver.py:44                                    */
     int32_t k_cap;       /* recovered-set capacity per instance (power of 2)*/
     int32_t precision;   /* FPSSFT_F32 | FPSSFT_F64                         */
+    int32_t mode;        /* FPSSFT_MODE_*: which kernel owns an instance    */
     double mag_tol, verify_tol, round_tol, amp_prune_tol;
     double energy_floor, energy_floor_abs, residual_stop;
 } fpssft_params;
@@ -137,11 +143,26 @@ int fpssft_project_onto_bins(const int32_t *freqs, const double *amps, const int
 /* Dynamic shared memory one fpssft_run_batch CTA needs (0 if unsupported). */
 size_t fpssft_smem_bytes(const fpssft_shape *shape, const fpssft_params *params);
 
-/* Threads per CTA fpssft_run_batch uses for this shape. */
+/* Threads per CTA of the CTA-per-instance kernel for this shape. */
 int fpssft_block_threads(const fpssft_shape *shape, int32_t precision);
+
+/* Launch plan fpssft_run_batch would use: mode (FPSSFT_MODE_CTA/WARP),
+ * threads per CTA, instances per CTA, dynamic shared memory per CTA.
+ * Returns 0, or an error code if the shape/params cannot run. */
+int fpssft_plan(const fpssft_shape *shape, const fpssft_params *params, int32_t *mode,
+                int32_t *threads_per_cta, int32_t *instances_per_cta, size_t *smem_bytes);
 
 /* Number of kernel launches fpssft_run_batch issues per call (for accounting). */
 int fpssft_launches_per_batch(void);
+
+/*
+ * Device-wide L2 fetch granularity (cudaLimitMaxL2FetchGranularity) for the
+ * current device, in bytes (0 = driver default, else 32/64/128).  The line
+ * gather touches isolated 8-byte samples, so 32 B keeps DRAM traffic near
+ * one sector per sample.  Process-wide side effect: opt-in, never implicit.
+ */
+int fpssft_set_l2_fetch_granularity(int32_t bytes);
+int fpssft_get_l2_fetch_granularity(void);
 
 const char *fpssft_last_error(void);
 int fpssft_abi_version(void);

@@ -14,12 +14,15 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfpssft.s
 MAX_DIMS = 4
 
 F32, F64 = 0, 1
+MODE_AUTO, MODE_CTA, MODE_WARP = 0, 1, 2
+MODES = {"auto": MODE_AUTO, "cta": MODE_CTA, "warp": MODE_WARP}
 TERM_NAMES = {0: "residual_clean", 1: "stall", 2: "max_iterations", 3: "k_cap_overflow",
               -1: "invalid_schedule"}
 
 EXPORTS = ("fpssft_run_batch", "fpssft_line_spectra", "fpssft_dft_forward",
            "fpssft_decode_spectra", "fpssft_project_onto_bins", "fpssft_smem_bytes",
-           "fpssft_block_threads", "fpssft_launches_per_batch", "fpssft_last_error",
+           "fpssft_block_threads", "fpssft_plan", "fpssft_launches_per_batch",
+           "fpssft_set_l2_fetch_granularity", "fpssft_get_l2_fetch_granularity", "fpssft_last_error",
            "fpssft_abi_version")
 
 
@@ -30,7 +33,7 @@ class Shape(C.Structure):
 
 class Params(C.Structure):
     _fields_ = [("t_max", C.c_int32), ("stall_limit", C.c_int32), ("k_cap", C.c_int32),
-                ("precision", C.c_int32), ("mag_tol", C.c_double), ("verify_tol", C.c_double),
+                ("precision", C.c_int32), ("mode", C.c_int32), ("mag_tol", C.c_double), ("verify_tol", C.c_double),
                 ("round_tol", C.c_double), ("amp_prune_tol", C.c_double),
                 ("energy_floor", C.c_double), ("energy_floor_abs", C.c_double),
                 ("residual_stop", C.c_double)]
@@ -72,6 +75,10 @@ def lib() -> C.CDLL:
         h.fpssft_smem_bytes.argtypes = [C.POINTER(Shape), C.POINTER(Params)]
         h.fpssft_smem_bytes.restype = C.c_size_t
         h.fpssft_block_threads.argtypes = [C.POINTER(Shape), I32]
+        h.fpssft_plan.argtypes = [C.POINTER(Shape), C.POINTER(Params), C.POINTER(I32),
+                                  C.POINTER(I32), C.POINTER(I32), C.POINTER(C.c_size_t)]
+        h.fpssft_set_l2_fetch_granularity.argtypes = [I32]
+        h.fpssft_get_l2_fetch_granularity.argtypes = []
         h.fpssft_last_error.restype = C.c_char_p
         for name in EXPORTS:
             if name not in ("fpssft_smem_bytes", "fpssft_last_error"):
@@ -119,3 +126,18 @@ def stream_ptr(device=None) -> int:
     import torch
 
     return int(torch.cuda.current_stream(device).cuda_stream)
+
+
+def set_l2_fetch_granularity(nbytes: int, device=None) -> None:
+    """cudaLimitMaxL2FetchGranularity for ``device`` (process-wide, opt-in)."""
+    import torch
+
+    with torch.cuda.device(device if device is not None else torch.cuda.current_device()):
+        check(lib().fpssft_set_l2_fetch_granularity(int(nbytes)))
+
+
+def get_l2_fetch_granularity(device=None) -> int:
+    import torch
+
+    with torch.cuda.device(device if device is not None else torch.cuda.current_device()):
+        return int(lib().fpssft_get_l2_fetch_granularity())

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <functional>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
@@ -240,9 +241,17 @@ __global__ void __launch_bounds__(1024, 1) recover_kernel(const float2 *__restri
         it_run = it + 1;
 
         // (1) gather + (2) DFT of the D+1 lines           driver.py:146-154
-        const R my_energy = gather_lines(spec, cube, g, al, ta);
-        __syncthreads();
-        fft_lines(spec, nl, g, roots);
+        R my_energy;
+        if constexpr (sizeof(R) == 4) {
+            gather_lines_async(spec, cube, g, al, ta, tid, NT);
+            cp_async_wait_all();
+            __syncthreads();
+            my_energy = kn.noise_coef > 0 ? line_energy(spec, nl * L, tid, NT) : (R)0;
+        } else {
+            my_energy = gather_lines(spec, cube, g, al, ta, tid, NT);
+            __syncthreads();
+        }
+        fft_lines<R, BlockTeam>(spec, nl, g, roots, tid, NT);
         // float32 only: bins below the transform's own rounding floor are
         // numerically empty ("precision floor")
         R noise_floor = (R)0;
@@ -411,6 +420,355 @@ __global__ void __launch_bounds__(1024, 1) recover_kernel(const float2 *__restri
     }
 }
 
+// ------------------------------------------------------ warp-per-instance
+// For short lines ((D+1) L <= 2048) one warp owns one instance: the same loop
+// as recover_kernel, but every step is warp-synchronous (__syncwarp, ballots,
+// match_any) and a CTA hosts several independent instances that share one
+// root table.  Many more instances are in flight per SM, which is what hides
+// the gather latency of this short, latency-bound loop.
+//
+// Per-warp shared memory: spectra (or the final sort's scratch, whichever is
+// larger), the slot table (packed key, amplitude, live flag), a 16-bit
+// open-addressing hash, and 32-entry scratch for the projection step.
+struct WarpLayout {
+    size_t spec, slot_amp, slot_key, hash, slot_live, cand, scr_u, scr_amp;
+    size_t per_warp, roots;
+    int H;
+};
+
+__host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, int cs) {
+    WarpLayout y;
+    const size_t spec_bytes = (size_t)(D + 1) * L * cs, sort_bytes = (size_t)k_cap * 8;
+    size_t o = 0;
+    y.H = 2 * k_cap;
+    y.spec = o;      o = align16(o + (spec_bytes > sort_bytes ? spec_bytes : sort_bytes));
+    y.slot_amp = o;  o = align16(o + (size_t)k_cap * cs);
+    y.slot_key = o;  o = align16(o + (size_t)k_cap * 4);
+    y.hash = o;      o = align16(o + (size_t)y.H * 2);
+    y.slot_live = o; o = align16(o + (size_t)k_cap);
+    y.cand = o;      o = align16(o + (size_t)L * 2);
+    y.scr_u = o;     o = align16(o + 32 * 4 * (size_t)(D + 1));
+    y.scr_amp = o;   o = align16(o + 32 * (size_t)cs);
+    y.per_warp = o;
+    y.roots = align16((size_t)L * cs);
+    return y;
+}
+
+__device__ __forceinline__ void unpack_key(int key, const Geo &g, int *m) {
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) m[k] = k < g.D ? (key >> g.key_shift[k]) & g.key_mask[k] : 0;
+}
+__device__ __forceinline__ int pack_key(const int *m, const Geo &g) {
+    int key = 0;
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k)
+        if (k < g.D) key |= m[k] << g.key_shift[k];
+    return key;
+}
+
+constexpr unsigned short HASH_EMPTY = 0xFFFF;
+
+__device__ __forceinline__ int hash16_find(const unsigned short *hash, const int *slot_key, int H,
+                                           int key) {
+    unsigned h = hash32(key) & (unsigned)(H - 1);
+    while (true) {
+        const unsigned short s = hash[h];
+        if (s == HASH_EMPTY) return -1;
+        if (slot_key[s] == key) return s;
+        h = (h + 1) & (unsigned)(H - 1);
+    }
+}
+__device__ __forceinline__ void hash16_insert(unsigned short *hash, int H, int key, int slot) {
+    unsigned h = hash32(key) & (unsigned)(H - 1);
+    while (atomicCAS(hash + h, HASH_EMPTY, (unsigned short)slot) != HASH_EMPTY)
+        h = (h + 1) & (unsigned)(H - 1);
+}
+
+template <class R>
+__global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__restrict__ cubes,
+                                                           long long batch, long long batch_stride,
+                                                           Geo g, Knobs kn,
+                                                           const int *__restrict__ schedule,
+                                                           const int *__restrict__ sched_index,
+                                                           int n_sched, OutPtrs out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const WarpLayout lay = make_warp_layout(g.D, g.L, kn.k_cap, (int)sizeof(cpx<R>));
+    cpx<R> *roots = (cpx<R> *)sm;
+    build_roots(roots, g.L);
+    __syncthreads();  // the only block-wide barrier: warps run independently below
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long inst = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (inst >= batch) return;
+    unsigned char *base = sm + lay.roots + (size_t)warp * lay.per_warp;
+    cpx<R> *spec = (cpx<R> *)(base + lay.spec);
+    cpx<R> *slot_amp = (cpx<R> *)(base + lay.slot_amp);
+    int *slot_key = (int *)(base + lay.slot_key);
+    unsigned short *hash = (unsigned short *)(base + lay.hash);
+    unsigned char *slot_live = base + lay.slot_live;
+    unsigned short *cand = (unsigned short *)(base + lay.cand);
+    int *scr_u = (int *)(base + lay.scr_u);
+    cpx<R> *scr_amp = (cpx<R> *)(base + lay.scr_amp);
+
+    const int L = g.L, D = g.D, nl = g.nlines, H = lay.H;
+    const float2 *cube = cubes + inst * batch_stride;
+    int sidx = sched_index ? sched_index[inst] : 0;
+    const bool sched_ok = sidx >= 0 && sidx < n_sched;
+    if (!sched_ok) sidx = 0;
+    const int *sched = schedule + (long long)sidx * kn.t_max * 2 * D;
+    const R mag_tol = (R)kn.mag_tol, round_tol = (R)kn.round_tol, verify_tol = (R)kn.verify_tol;
+    const R prune = (R)kn.amp_prune_tol;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    for (int h = lane; h < H; h += 32) hash[h] = HASH_EMPTY;
+    __syncwarp();
+
+    int n_slots = 0, stall = 0, it_run = 0;
+    int term = sched_ok ? FPSSFT_TERM_MAX_ITERATIONS : -1;
+    R amp_sum = (R)0;
+
+    // the schedule is data-independent: iteration t+1's (alpha, tau) load
+    // while iteration t runs
+    int nal[MAXD], nta[MAXD];
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+        nal[k] = k < D ? sched[k] : 0;
+        nta[k] = k < D ? sched[D + k] : 0;
+    }
+    for (int it = 0; it < kn.t_max && term != -1; ++it) {
+        int al[MAXD], ta[MAXD];
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) {
+            al[k] = nal[k];
+            ta[k] = nta[k];
+        }
+        if (!line_params_ok(g, al, ta)) {
+            term = -1;
+            break;
+        }
+        it_run = it + 1;
+
+        // (1) gather + (2) DFT of the D+1 lines           driver.py:146-154
+        R my_energy;
+        if constexpr (sizeof(R) == 4) {
+            gather_lines_async(spec, cube, g, al, ta, lane, 32);
+            if (it + 1 < kn.t_max) {
+#pragma unroll
+                for (int k = 0; k < MAXD; ++k) {
+                    nal[k] = k < D ? sched[(long long)(it + 1) * 2 * D + k] : 0;
+                    nta[k] = k < D ? sched[(long long)(it + 1) * 2 * D + D + k] : 0;
+                }
+            }
+            cp_async_wait_all();
+            __syncwarp();
+            my_energy = kn.noise_coef > 0 ? line_energy(spec, nl * L, lane, 32) : (R)0;
+        } else {
+            my_energy = gather_lines(spec, cube, g, al, ta, lane, 32);
+            if (it + 1 < kn.t_max) {
+#pragma unroll
+                for (int k = 0; k < MAXD; ++k) {
+                    nal[k] = k < D ? sched[(long long)(it + 1) * 2 * D + k] : 0;
+                    nta[k] = k < D ? sched[(long long)(it + 1) * 2 * D + D + k] : 0;
+                }
+            }
+            __syncwarp();
+        }
+        fft_lines_warp<R>(spec, nl, g, roots, lane);
+        R noise_floor = (R)0;
+        if (sizeof(R) == 4 && kn.noise_coef > 0)
+            noise_floor = (R)kn.noise_coef * sqrt(__shfl_sync(FULL, warp_sum(my_energy), 0));
+
+        // (3) construction-subtraction, 32 slots at a time in slot order;
+        //     each lane stages its slot's phase on every line, slots sharing
+        //     a bin are summed by their lowest lane in lane (= slot) order
+        for (int c0 = 0; c0 < n_slots; c0 += 32) {
+            const int s = c0 + lane;
+            const bool valid = s < n_slots && slot_live[s];
+            int b = -1 - lane;
+            if (valid) {
+                int m[MAXD];
+                unpack_key(slot_key[s], g, m);
+                b = bin_of(m, g, al);
+                const int u0 = phase_of(m, g, ta);
+#pragma unroll
+                for (int i = 0; i < MAXD + 1; ++i)
+                    if (i < nl) scr_u[i * 32 + lane] = phase_step(u0, i, m, g);
+                scr_amp[lane] = slot_amp[s];
+            }
+            __syncwarp();
+            const unsigned grp = __match_any_sync(FULL, b);
+            if (valid && lane == __ffs(grp) - 1) {
+                cpx<R> P[MAXD + 1];
+#pragma unroll
+                for (int i = 0; i < MAXD + 1; ++i) P[i] = {(R)0, (R)0};
+                for (unsigned rest = grp; rest; rest &= rest - 1) {
+                    const int j = __ffs(rest) - 1;
+                    const cpx<R> aj = scr_amp[j];
+#pragma unroll
+                    for (int i = 0; i < MAXD + 1; ++i)
+                        if (i < nl) P[i] = P[i] + aj * roots[scr_u[i * 32 + j]];
+                }
+#pragma unroll
+                for (int i = 0; i < MAXD + 1; ++i)
+                    if (i < nl) spec[i * L + b] = spec[i * L + b] - P[i];
+            }
+            __syncwarp();
+        }
+
+        // (4) classify + (5) merge, 32 bins at a time in ascending order
+        const R floor =
+            max(max((R)kn.energy_floor_abs, (R)kn.energy_floor * amp_sum), noise_floor);
+        // 1-sparse magnitude test on every bin, candidates compacted in
+        // ascending order so the decode runs on dense batches of 32.  The
+        // termination residual (max |S|) is folded in: non-candidate bins keep
+        // their values, candidates are re-read after the merge below.
+        int n_cand = 0, n_acc = 0;
+        R resid = (R)0;
+        for (int c0 = 0; c0 < L; c0 += 32) {
+            const int b = c0 + lane;
+            R top = (R)0;
+            const bool ok = b < L && bin_is_candidate(spec, g, b, mag_tol, floor, &top);
+            if (!ok) resid = max(resid, top);
+            const unsigned msk = __ballot_sync(FULL, ok);
+            if (ok) cand[n_cand + __popc(msk & lt_mask)] = (unsigned short)b;
+            n_cand += __popc(msk);
+        }
+        __syncwarp();
+        bool overflow = false;
+        for (int c0 = 0; c0 < n_cand; c0 += 32) {
+            const int b = c0 + lane < n_cand ? cand[c0 + lane] : -1;
+            int m[MAXD];
+            cpx<R> a;
+            int st = 0;
+            if (b >= 0) st = decode_candidate(spec, g, b, al, ta, roots, round_tol, verify_tol, m, &a);
+            const unsigned acc = __ballot_sync(FULL, st == 2);
+            int key = 0, found = -1;
+            if (st == 2) {
+                key = pack_key(m, g);
+                found = hash16_find(hash, slot_key, H, key);
+            }
+            const unsigned fresh = __ballot_sync(FULL, st == 2 && found < 0);
+            if (n_slots + __popc(fresh) > kn.k_cap) {
+                overflow = true;
+                break;
+            }
+            n_acc += __popc(acc);
+            if (st == 2) {
+                cpx<R> v = a;
+                int s;
+                if (found < 0) {
+                    s = n_slots + __popc(fresh & lt_mask);
+                    slot_key[s] = key;
+                    hash16_insert(hash, H, key, s);
+                } else {
+                    s = found;
+                    v = slot_amp[s] + a;  // a pruned slot holds 0: entries.get(f, 0) + a
+                }
+                const bool keep = !(cabs(v) <= prune);
+                slot_amp[s] = keep ? v : cpx<R>{(R)0, (R)0};
+                slot_live[s] = keep;
+                const int u0 = phase_of(m, g, ta);  // driver.py:189-194
+                for (int i = 0; i < nl; ++i)
+                    spec[i * L + b] = spec[i * L + b] - a * roots[phase_step(u0, i, m, g)];
+            }
+            if (b >= 0) resid = max(resid, bin_residual(spec, g, b));
+            n_slots += __popc(fresh);
+            __syncwarp();
+        }
+        if (overflow) {
+            term = FPSSFT_TERM_K_CAP_OVERFLOW;
+            if (lane == 0 && out.iter_stats) {
+                int *st = out.iter_stats + (inst * kn.t_max + it) * 3;
+                st[0] = n_cand;
+                st[1] = 0;
+                st[2] = n_cand;
+            }
+            break;
+        }
+        __syncwarp();
+
+        // (6) amp_sum = sum |a| over the recovered set        driver.py:108
+        R my = (R)0;
+        for (int s = lane; s < n_slots; s += 32)
+            if (slot_live[s]) my += cabs(slot_amp[s]);
+        amp_sum = __shfl_sync(FULL, warp_sum(my), 0);
+        stall = n_acc > 0 ? 0 : stall + 1;
+
+        // (7) termination                                     driver.py:196-204
+        const R clean = max((R)kn.energy_floor_abs, (R)kn.residual_stop * amp_sum);
+        const R worst = warp_max(resid);  // |S|^2 (float) or |S| (double)
+        const bool is_clean = sizeof(R) == 8 ? worst <= clean : worst <= clean * clean;
+        if (lane == 0 && out.iter_stats) {
+            int *st = out.iter_stats + (inst * kn.t_max + it) * 3;
+            st[0] = n_cand;
+            st[1] = n_acc;
+            st[2] = n_cand - n_acc;
+        }
+        __syncwarp();
+        if (is_clean) {
+            term = FPSSFT_TERM_RESIDUAL_CLEAN;
+            break;
+        }
+        if (stall >= kn.stall_limit) {
+            term = FPSSFT_TERM_STALL;
+            break;
+        }
+    }
+
+    // ---- RecoveryReport: live entries sorted by packed key (= lexicographic)
+    __syncwarp();
+    int P = 1;
+    while (P < n_slots) P <<= 1;
+    int *skey = (int *)spec;
+    int *sslot = skey + P;
+    int my_live = 0;
+    for (int s = lane; s < P; s += 32) {
+        const bool live = s < n_slots && slot_live[s];
+        my_live += live;
+        skey[s] = live ? slot_key[s] : INT_MAX;
+        sslot[s] = s;
+    }
+    const int count = __shfl_sync(FULL, warp_sum(my_live), 0);
+    __syncwarp();
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = lane; i < P; i += 32) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const int ki = skey[i], kj = skey[j];
+                    if ((ki > kj) == up) {
+                        skey[i] = kj;
+                        skey[j] = ki;
+                        const int t = sslot[i];
+                        sslot[i] = sslot[j];
+                        sslot[j] = t;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    for (int r = lane; r < count; r += 32) {
+        const int s = sslot[r];
+        int m[MAXD];
+        unpack_key(slot_key[s], g, m);
+        int *fo = out.freqs + (inst * kn.k_cap + r) * D;
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k)
+            if (k < D) fo[k] = m[k];
+        double *ao = out.amps + (inst * kn.k_cap + r) * 2;
+        ao[0] = (double)slot_amp[s].re;
+        ao[1] = (double)slot_amp[s].im;
+    }
+    if (lane == 0) {
+        out.count[inst] = count;
+        out.iterations[inst] = it_run;
+        out.samples_used[inst] = (long long)it_run * nl * L;
+        out.terminated_by[inst] = term;
+    }
+}
+
 // ------------------------------------------------------- per-function kernels
 template <class R>
 __global__ void __launch_bounds__(1024, 1) line_spectra_kernel(const float2 *__restrict__ cubes,
@@ -430,9 +788,10 @@ __global__ void __launch_bounds__(1024, 1) line_spectra_kernel(const float2 *__r
     }
     build_roots(roots, g.L);
     if (!line_params_ok(g, al, ta)) return;
-    gather_lines(spec, cubes + (long long)inst * batch_stride, g, al, ta);
+    gather_lines(spec, cubes + (long long)inst * batch_stride, g, al, ta, threadIdx.x,
+                 blockDim.x);
     __syncthreads();
-    fft_lines(spec, g.nlines, g, roots);
+    fft_lines<R, BlockTeam>(spec, g.nlines, g, roots, threadIdx.x, blockDim.x);
     cpx<R> *o = out + (long long)inst * g.nlines * g.L;
     for (int e = threadIdx.x; e < g.nlines * g.L; e += blockDim.x) o[e] = spec[e];
 }
@@ -447,7 +806,7 @@ __global__ void __launch_bounds__(1024, 1) dft_kernel(const cpx<R> *__restrict__
     build_roots(roots, g.L);
     for (int l = threadIdx.x; l < g.L; l += blockDim.x) x[l] = in[off + l];
     __syncthreads();
-    fft_lines(x, 1, g, roots);
+    fft_lines<R, BlockTeam>(x, 1, g, roots, threadIdx.x, blockDim.x);
     for (int l = threadIdx.x; l < g.L; l += blockDim.x) out[off + l] = x[l];
 }
 
@@ -582,24 +941,90 @@ int make_geo(const fpssft_shape *shape, Geo *g) {
         g->stride[k] = shape->strides[k];
         g->magic[k] = (n == 1) ? 0ULL : (~0ULL / n + 1ULL);
     }
+    // 32-bit element offsets when the whole cube is addressable with them
+    long long span = 0;
+    for (int k = 0; k < D; ++k) span += (long long)(shape->dims[k] - 1) * std::llabs(shape->strides[k]);
+    g->off32 = span < (1LL << 31) ? 1 : 0;
+    for (int k = 0; k < D; ++k) g->stride32[k] = g->off32 ? (int)shape->strides[k] : 0;
+    // packed frequency key (warp mode): bit_length(N_k - 1) bits per dim,
+    // dim 0 most significant, so key order is lexicographic order
+    int shift = 0;
+    for (int k = D - 1; k >= 0; --k) {
+        int bits = 0;
+        while ((1LL << bits) < shape->dims[k]) ++bits;
+        g->key_shift[k] = shift;
+        g->key_mask[k] = (int)((1LL << bits) - 1);
+        shift += bits;
+    }
+    g->key_bits_ = shift;
     return FPSSFT_OK;
 }
 
-// FFT plan + CTA size for `nlines` lines of length L.  Radices: 16s, then
-// the leftover power of two as one stage, then 3s, 5s, 7s; a remaining prime
-// factor > 7 means one direct O(L^2) pass.  CTA size: one thread per bin
-// (>= 64), grown until every stage's butterflies fit MB per thread with
-// MB*radix <= 16 registers' worth of complex values.  Returns -1 if no CTA
-// size <= 1024 works.
-int plan_fft(Geo *g, int nlines, int precision) {
+// FFT plan for `nlines` lines of length L owned by `team` threads (32 = one
+// warp per instance; 0 = one CTA per instance, size chosen here).  Radices:
+// the largest power of two allowed (16 in float, 8 in double or for warp
+// teams), the leftover power of two as one stage, then 3s, 5s, 7s; a
+// remaining prime factor > 7 means one direct O(L^2) pass.  A stage's
+// butterflies are spread MB per thread with MB*radix complex values held in
+// registers (<= 16 float / 8 double); lines are transformed G at a time so
+// that fits.  Returns the thread count, or -1 if no plan fits.
+int plan_fft(Geo *g, int nlines, int precision, int team) {
     const int L = g->L;
     const bool dbl = precision == FPSSFT_F64;
-    int rad[MAXSTAGES], n = 0, x = L;
-    int e = 0;
+    auto cap = [dbl](int r) {
+        if (r == 0) return 4;
+        if (dbl) return r <= 2 ? 4 : (r <= 4 ? 2 : 1);
+        return r <= 4 ? 4 : (r <= 8 ? 2 : 1);
+    };
+    int x = L, e = 0;
     while (x % 2 == 0) { x /= 2; ++e; }
-    const int big = dbl ? 3 : 4;  // 16-point butterflies in float, 8-point in double
-    while (e >= big) { rad[n++] = 1 << big; e -= big; }
-    if (e > 0) rad[n++] = 1 << e;
+    int rad[MAXSTAGES], n = 0;
+    if (team && x == 1) {
+        // warp teams: choose how to split 2^e into radix 2..16 stages by a
+        // cost model (per group step: MB butterflies of r log2 r work plus a
+        // fixed sync/index overhead); stages must fit MB <= cap(r)
+        const int maxbits = dbl ? 3 : 4;
+        double best = 1e300;
+        int best_parts[MAXSTAGES], best_n = -1;
+        int parts[MAXSTAGES];
+        // iterate compositions of e into parts in [1, maxbits], larger first
+        std::function<void(int, int)> rec = [&](int left, int k) {
+            if (k > MAXSTAGES) return;
+            if (left == 0) {
+                double cost = 0;
+                for (int i = 0; i < k; ++i) {
+                    const int r = 1 << parts[i];
+                    const long long m = L / r;
+                    const long long G = std::max(1LL, std::min<long long>(nlines, cap(r) * team / m));
+                    const long long mb = (G * m + team - 1) / team;
+                    if (mb > cap(r)) return;
+                    const long long groups = (nlines + G - 1) / G;
+                    cost += groups * (mb * r * parts[i] + 24.0);
+                }
+                if (cost < best) {
+                    best = cost;
+                    best_n = k;
+                    for (int i = 0; i < k; ++i) best_parts[i] = parts[i];
+                }
+                return;
+            }
+            for (int b = std::min(maxbits, left); b >= 1; --b) {
+                parts[k] = b;
+                rec(left - b, k + 1);
+            }
+        };
+        rec(e, 0);
+        if (best_n < 0) return -1;
+        for (int i = 0; i < best_n; ++i) rad[n++] = 1 << best_parts[i];
+    } else {
+        const int big = (dbl || team) ? 3 : 4;
+        while (e >= big) {
+            if (n == MAXSTAGES) return -1;
+            rad[n++] = 1 << big;
+            e -= big;
+        }
+        if (e > 0) rad[n++] = 1 << e;
+    }
     for (int p : {3, 5, 7})
         while (x % p == 0) {
             if (n == MAXSTAGES) return -1;
@@ -611,32 +1036,36 @@ int plan_fft(Geo *g, int nlines, int precision) {
         rad[0] = 0;
     }
     if (L == 1) n = 0;
-    auto cap = [dbl](int r) {
-        if (r == 0) return 4;
-        if (dbl) return r <= 2 ? 4 : (r <= 4 ? 2 : 1);
-        return r <= 4 ? 4 : (r <= 8 ? 2 : 1);
-    };
-    long long nt = std::max(64, std::min(((L + 31) / 32) * 32, 1024));
-    for (int i = 0; i < n; ++i) {
-        const long long tot = (long long)nlines * (rad[i] ? L / rad[i] : L);
-        const long long need = (tot + cap(rad[i]) - 1) / cap(rad[i]);
-        nt = std::max(nt, ((need + 31) / 32) * 32);
+    long long nt = team;
+    if (!team) {
+        nt = std::max(64, std::min(((L + 31) / 32) * 32, 1024));
+        for (int i = 0; i < n; ++i) {
+            const long long tot = (long long)nlines * (rad[i] ? L / rad[i] : L);
+            const long long need = (tot + cap(rad[i]) - 1) / cap(rad[i]);
+            nt = std::max(nt, ((need + 31) / 32) * 32);
+        }
+        if (nt > 1024) return -1;
     }
-    if (nt > 1024) return -1;
     g->nstages = n;
-    g->plan[0] = g->plan[1] = 0;
+    g->plan[0] = g->plan[1] = g->plan[2] = g->plan[3] = 0;
     for (int i = 0; i < n; ++i) {
-        const long long tot = (long long)nlines * (rad[i] ? L / rad[i] : L);
-        int mb = (int)((tot + nt - 1) / nt);
+        const long long m = rad[i] ? L / rad[i] : L;  // butterflies per line
+        long long G = team ? std::max(1LL, std::min<long long>(nlines, cap(rad[i]) * nt / m))
+                           : nlines;
+        long long mb = (G * m + nt - 1) / nt;
+        if (mb > cap(rad[i])) return -1;
         mb = mb <= 1 ? 1 : (mb <= 2 ? 2 : 4);
-        const unsigned long long code = (unsigned long long)(rad[i] | (mb << 5));
-        g->plan[i >> 3] |= code << (8 * (i & 7));
+        const unsigned long long code =
+            (unsigned long long)(rad[i] | (mb << 5) | (G << 8));
+        g->plan[i >> 2] |= code << (16 * (i & 3));
     }
     g->threads = (int)nt;
     return (int)nt;
 }
 
-int block_threads(Geo &g, int nlines, int precision) { return plan_fft(&g, nlines, precision); }
+int block_threads(Geo &g, int nlines, int precision) {
+    return plan_fft(&g, nlines, precision, 0);
+}
 
 int max_smem_optin() {
     int dev = 0, v = 0;
@@ -660,6 +1089,8 @@ int make_knobs(const fpssft_params *p, Knobs *k) {
         if (!(v[i] > 0)) return fail(FPSSFT_EINVAL, std::string(names[i]) + " must be positive");
     if (p->precision != FPSSFT_F32 && p->precision != FPSSFT_F64)
         return fail(FPSSFT_EINVAL, "precision must be FPSSFT_F32 or FPSSFT_F64");
+    if (p->mode < FPSSFT_MODE_AUTO || p->mode > FPSSFT_MODE_WARP)
+        return fail(FPSSFT_EINVAL, "mode must be FPSSFT_MODE_AUTO, _CTA or _WARP");
     k->mag_tol = p->mag_tol;
     k->verify_tol = p->verify_tol;
     k->round_tol = p->round_tol;
@@ -692,23 +1123,89 @@ int check_launch(const char *where) {
     return FPSSFT_OK;
 }
 
-template <class R>
-int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
-                const Knobs &kn, const int32_t *schedule, const int32_t *sched_index,
-                int32_t n_sched, const OutPtrs &o, cudaStream_t st) {
-    const int nt = block_threads(g, g.nlines, sizeof(R) == 8 ? FPSSFT_F64 : FPSSFT_F32);
+constexpr long long SMEM_PER_SM = 228 * 1024;    // B200 shared memory per SM
+constexpr long long SMEM_PER_CTA = 227 * 1024;   // opt-in limit per CTA
+constexpr long long SMEM_RESERVED = 1024;        // per-CTA system reservation
+
+struct LaunchPlan {
+    int mode, threads, per_cta;
+    size_t smem;
+};
+
+// Pick the kernel for a shape: warp-per-instance when the lines are short
+// enough ((D+1) L <= 2048), the packed key fits 31 bits and the per-warp state
+// fits; warps per CTA chosen to maximise resident instances per SM.  Else one
+// CTA per instance.  `g` receives the FFT plan of the chosen mode.
+int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) {
+    const int cs = precision == FPSSFT_F64 ? 16 : 8;
+    if (want != FPSSFT_MODE_CTA) {
+        Geo gw = g;
+        bool ok = g.key_bits_ <= 31 && kn.k_cap <= 32768 && (long long)g.nlines * g.L <= 2048 &&
+                  (g.L & (g.L - 1)) == 0 && plan_fft(&gw, g.nlines, precision, 32) > 0;
+        if (ok) {
+            const WarpLayout wl = make_warp_layout(g.D, g.L, kn.k_cap, cs);
+            int best_w = 0;
+            long long best_warps = 0;
+            for (int w : {8, 4, 2, 1}) {
+                const long long smem = (long long)wl.roots + w * (long long)wl.per_warp;
+                if (smem > SMEM_PER_CTA) continue;
+                const long long ctas =
+                    std::min<long long>({32, SMEM_PER_SM / (smem + SMEM_RESERVED), 64 / w});
+                if (ctas * w > best_warps) {
+                    best_warps = ctas * w;
+                    best_w = w;
+                }
+            }
+            if (best_w) {
+                g = gw;
+                lp->mode = FPSSFT_MODE_WARP;
+                lp->threads = 32 * best_w;
+                lp->per_cta = best_w;
+                lp->smem = wl.roots + (size_t)best_w * wl.per_warp;
+                return FPSSFT_OK;
+            }
+        }
+        if (want == FPSSFT_MODE_WARP)
+            return fail(FPSSFT_EUNSUPPORTED, "shape/k_cap does not fit the warp-per-instance kernel");
+    }
+    const int nt = plan_fft(&g, g.nlines, precision, 0);
     if (nt < 0) return fail(FPSSFT_EUNSUPPORTED, "line length too large for one CTA");
-    const Layout lay = make_layout(g.D, g.L, kn.k_cap, (int)sizeof(cpx<R>));
-    if ((long long)lay.total > max_smem_optin())
+    const Layout lay = make_layout(g.D, g.L, kn.k_cap, cs);
+    if ((long long)lay.total > SMEM_PER_CTA)
         return fail(FPSSFT_EUNSUPPORTED,
                     "shared memory for this (shape, k_cap, precision) is " +
                         std::to_string(lay.total) + " B, above the per-CTA limit; lower k_cap");
-    cudaError_t e = cudaFuncSetAttribute(recover_kernel<R>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)lay.total);
+    lp->mode = FPSSFT_MODE_CTA;
+    lp->threads = nt;
+    lp->per_cta = 1;
+    lp->smem = lay.total;
+    return FPSSFT_OK;
+}
+
+template <class R>
+int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
+                const Knobs &kn, int want_mode, const int32_t *schedule,
+                const int32_t *sched_index, int32_t n_sched, const OutPtrs &o, cudaStream_t st) {
+    LaunchPlan lp;
+    int rc = make_plan(g, kn, sizeof(R) == 8 ? FPSSFT_F64 : FPSSFT_F32, want_mode, &lp);
+    if (rc != FPSSFT_OK) return rc;
+    cudaError_t e;
+    if (lp.mode == FPSSFT_MODE_WARP) {
+        e = cudaFuncSetAttribute(recover_warp_kernel<R>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lp.smem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recover_warp_kernel)");
+        if (batch == 0) return FPSSFT_OK;
+        const long long grid = (batch + lp.per_cta - 1) / lp.per_cta;
+        recover_warp_kernel<R><<<(unsigned)grid, lp.threads, lp.smem, st>>>(
+            (const float2 *)cubes, (long long)batch, (long long)batch_stride, g, kn, schedule,
+            sched_index, n_sched, o);
+        return check_launch("recover_warp_kernel");
+    }
+    e = cudaFuncSetAttribute(recover_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)lp.smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recover_kernel)");
     if (batch == 0) return FPSSFT_OK;
-    recover_kernel<R><<<(unsigned)batch, nt, lay.total, st>>>(
+    recover_kernel<R><<<(unsigned)batch, lp.threads, lp.smem, st>>>(
         (const float2 *)cubes, (long long)batch_stride, g, kn, schedule, sched_index, n_sched, o);
     return check_launch("recover_kernel");
 }
@@ -728,6 +1225,20 @@ const char *fpssft_last_error(void) { return g_err.c_str(); }
 int fpssft_abi_version(void) { return 1; }
 int fpssft_launches_per_batch(void) { return 1; }
 
+int fpssft_set_l2_fetch_granularity(int32_t bytes) {
+    if (bytes < 0 || bytes > 128 || (bytes & (bytes - 1)))
+        return fail(FPSSFT_EINVAL, "L2 fetch granularity must be 0 or a power of two <= 128");
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSetLimit(MaxL2FetchGranularity)");
+    return FPSSFT_OK;
+}
+
+int fpssft_get_l2_fetch_granularity(void) {
+    size_t v = 0;
+    if (cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity) != cudaSuccess) return -1;
+    return (int)v;
+}
+
 int fpssft_block_threads(const fpssft_shape *shape, int32_t precision) {
     (void)precision;
     Geo g;
@@ -736,11 +1247,9 @@ int fpssft_block_threads(const fpssft_shape *shape, int32_t precision) {
 }
 
 size_t fpssft_smem_bytes(const fpssft_shape *shape, const fpssft_params *params) {
-    Geo g;
-    Knobs k;
-    if (make_geo(shape, &g) != FPSSFT_OK || make_knobs(params, &k) != FPSSFT_OK) return 0;
-    const int cs = params->precision == FPSSFT_F64 ? 16 : 8;
-    return make_layout(g.D, g.L, k.k_cap, cs).total;
+    size_t smem = 0;
+    if (fpssft_plan(shape, params, nullptr, nullptr, nullptr, &smem) != FPSSFT_OK) return 0;
+    return smem;
 }
 
 int fpssft_run_batch(const void *cubes, int64_t batch, int64_t batch_stride,
@@ -768,10 +1277,26 @@ int fpssft_run_batch(const void *cubes, int64_t batch, int64_t batch_stride,
               out ? out->iter_stats : nullptr};
     cudaStream_t st = (cudaStream_t)stream;
     if (params->precision == FPSSFT_F64)
-        return run_batch_t<double>(cubes, batch, batch_stride, g, kn, schedule, sched_index,
-                                   n_sched, o, st);
-    return run_batch_t<float>(cubes, batch, batch_stride, g, kn, schedule, sched_index, n_sched,
-                              o, st);
+        return run_batch_t<double>(cubes, batch, batch_stride, g, kn, params->mode, schedule,
+                                   sched_index, n_sched, o, st);
+    return run_batch_t<float>(cubes, batch, batch_stride, g, kn, params->mode, schedule,
+                              sched_index, n_sched, o, st);
+}
+
+int fpssft_plan(const fpssft_shape *shape, const fpssft_params *params, int32_t *mode,
+                int32_t *threads_per_cta, int32_t *instances_per_cta, size_t *smem_bytes) {
+    Geo g;
+    Knobs kn;
+    int rc;
+    if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
+    if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
+    LaunchPlan lp;
+    if ((rc = make_plan(g, kn, params->precision, params->mode, &lp)) != FPSSFT_OK) return rc;
+    if (mode) *mode = lp.mode;
+    if (threads_per_cta) *threads_per_cta = lp.threads;
+    if (instances_per_cta) *instances_per_cta = lp.per_cta;
+    if (smem_bytes) *smem_bytes = lp.smem;
+    return FPSSFT_OK;
 }
 
 int fpssft_line_spectra(const void *cubes, int64_t batch, int64_t batch_stride,

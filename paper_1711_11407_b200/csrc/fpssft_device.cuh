@@ -40,9 +40,22 @@ template <class R>
 __device__ __forceinline__ cpx<R> mulc(cpx<R> a, cpx<R> b) {
     return {a.re * b.re + a.im * b.im, a.im * b.re - a.re * b.im};
 }
+// |z|: hypot in float64 (what np.abs computes); sqrt(x^2 + y^2) in float32,
+// whose inputs never approach overflow here.
 template <class R>
 __device__ __forceinline__ R cabs(cpx<R> a) { return hypot(a.re, a.im); }
-__device__ __forceinline__ float cabs(cpx<float> a) { return hypotf(a.re, a.im); }
+__device__ __forceinline__ float cabs(cpx<float> a) { return sqrtf(a.re * a.re + a.im * a.im); }
+template <class R>
+__device__ __forceinline__ R cabs2(cpx<R> a) { return a.re * a.re + a.im * a.im; }
+
+// Synchronisation of the threads that own one instance: the whole CTA, or
+// one warp (team of 32 lanes).
+struct BlockTeam {
+    __device__ __forceinline__ static void sync() { __syncthreads(); }
+};
+struct WarpTeam {
+    __device__ __forceinline__ static void sync() { __syncwarp(); }
+};
 
 // ---------------------------------------------------------------- geometry
 // CubeShape (core.py:26-73) as the kernels see it.
@@ -51,15 +64,23 @@ struct Geo {
     int N[MAXD];                    // extents
     int cof[MAXD];                  // c_k = L / N_k
     long long stride[MAXD];         // element strides of one cube
+    int stride32[MAXD];             // the same as int32 when off32
+    int off32;                      // every element offset of a cube fits int32
     unsigned long long magic[MAXD]; // fastmod multipliers for N_k
-    int nstages;                    // FFT plan, 8 bits per stage s in plan[s/8] >> 8(s%8):
-    unsigned long long plan[2];     //   low 5 bits radix {2,3,4,5,7,8,16} (0 = direct O(L^2)),
-                                    //   high 3 bits butterflies per thread {1,2,4}
-    int threads;                    // CTA size the plan was made for
+    int nstages;                    // FFT plan, 16 bits per stage s in plan[s/4] >> 16(s%4):
+    unsigned long long plan[4];     //   bits 0-4 radix {2,3,4,5,7,8,16} (0 = direct O(L^2)),
+                                    //   bits 5-7 butterflies per thread {1,2,4},
+                                    //   bits 8-10 lines transformed together (1..D+1)
+    int threads;                    // threads per instance the plan was made for
+    int key_shift[MAXD];            // packed frequency key: m_k << key_shift[k]
+    int key_mask[MAXD];             //   (lexicographic order = key order)
+    int key_bits_;                  // total bits of the packed key
 };
 __host__ __device__ __forceinline__ int stage_code(const Geo &g, int s) {
-    const unsigned long long w = s < 8 ? g.plan[0] : g.plan[1];  // no dynamic indexing
-    return (int)((w >> (8 * (s & 7))) & 255ULL);
+    const int q = s >> 2;  // selects, not dynamic indexing, keep g in registers
+    const unsigned long long w = q == 0 ? g.plan[0] : q == 1 ? g.plan[1] : q == 2 ? g.plan[2]
+                                                                              : g.plan[3];
+    return (int)((w >> (16 * (s & 3))) & 0xFFFFULL);
 }
 
 // Tolerances / knobs (FpsSftConfig, driver.py:29-63).
@@ -155,10 +176,11 @@ __device__ __forceinline__ void build_roots(cpx<R> *roots, int L) {
 // Returns this thread's share of sum |x|^2 over the gathered samples.
 template <class R>
 __device__ __forceinline__ R gather_lines(cpx<R> *spec, const float2 *__restrict__ cube,
-                                          const Geo &g, const int *al, const int *ta) {
+                                          const Geo &g, const int *al, const int *ta, int tid,
+                                          int nth) {
     const int L = g.L, D = g.D;
     R energy = (R)0;
-    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    for (int l = tid; l < L; l += nth) {
         long long base = 0;
         long long delta[MAXD];
 #pragma unroll
@@ -185,6 +207,138 @@ __device__ __forceinline__ R gather_lines(cpx<R> *spec, const float2 *__restrict
             }
     }
     return energy;
+}
+
+// float32 path: the gather as asynchronous 8-byte global->shared copies
+// (cp.async, LDGSTS): every sample of every line of an iteration is in flight
+// at once, no registers held, so one warp per instance still has its whole
+// line set outstanding against DRAM.  Caller: cp_async_wait_all(), team sync,
+// then line_energy() if the rounding floor is needed.
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+__device__ __forceinline__ void gather_lines_async(cpx<float> *spec,
+                                                   const float2 *__restrict__ cube, const Geo &g,
+                                                   const int *al, const int *ta, int tid,
+                                                   int nth) {
+    const int L = g.L, D = g.D;
+    if (g.off32) {
+        // n_k(l) advanced incrementally by alpha_k * nth mod N_k: no division,
+        // 32-bit offsets
+        int n[MAXD], step[MAXD];
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) {
+            n[k] = k < D ? (int)fastmod((unsigned)al[k] * (unsigned)tid + (unsigned)ta[k],
+                                        g.magic[k], (unsigned)g.N[k])
+                         : 0;
+            step[k] = k < D ? (int)fastmod((unsigned)al[k] * (unsigned)nth, g.magic[k],
+                                           (unsigned)g.N[k])
+                            : 0;
+        }
+        for (int l = tid; l < L; l += nth) {
+            int base = 0;
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k)
+                if (k < D) base += n[k] * g.stride32[k];
+            cp_async8(spec + l, cube + base);
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k) {
+                if (k < D) {
+                    const int d = (n[k] + 1 == g.N[k]) ? -n[k] * g.stride32[k] : g.stride32[k];
+                    cp_async8(spec + (k + 1) * L + l, cube + (base + d));
+                    n[k] += step[k];
+                    if (n[k] >= g.N[k]) n[k] -= g.N[k];
+                }
+            }
+        }
+        return;
+    }
+    for (int l = tid; l < L; l += nth) {
+        long long base = 0;
+        long long delta[MAXD];
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) {
+            if (k < D) {
+                unsigned n = fastmod((unsigned)al[k] * (unsigned)l + (unsigned)ta[k], g.magic[k],
+                                     (unsigned)g.N[k]);
+                base += (long long)n * g.stride[k];
+                delta[k] = (n + 1 == (unsigned)g.N[k]) ? -(long long)n * g.stride[k] : g.stride[k];
+            }
+        }
+        cp_async8(spec + l, cube + base);
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k)
+            if (k < D) cp_async8(spec + (k + 1) * L + l, cube + base + delta[k]);
+    }
+}
+// Register-staged variant: samples read with non-L1-allocating loads
+// (ld.global.nc.L1::no_allocate), CH rows of every line in flight per thread,
+// then stored to shared memory.  An L1-allocating fill (cp.async.ca) pulls
+// whole 128-byte lines through L2 for one 8-byte sample; this path moves
+// only the 32-byte sectors that hold samples.
+__device__ __forceinline__ float2 ld_stream(const float2 *p) {
+    float2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];"
+                 : "=f"(v.x), "=f"(v.y)
+                 : "l"(p));
+    return v;
+}
+template <class R, int CH>
+__device__ __forceinline__ R gather_lines_reg(cpx<R> *spec, const float2 *__restrict__ cube,
+                                              const Geo &g, const int *al, const int *ta, int tid,
+                                              int nth) {
+    const int L = g.L, D = g.D;
+    R energy = (R)0;
+    for (int l0 = tid; l0 < L; l0 += CH * nth) {
+        float2 v[CH][MAXD + 1];
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int l = l0 + c * nth;
+            if (l < L) {
+                long long base = 0;
+                long long delta[MAXD];
+#pragma unroll
+                for (int k = 0; k < MAXD; ++k) {
+                    if (k < D) {
+                        unsigned n = fastmod((unsigned)al[k] * (unsigned)l + (unsigned)ta[k],
+                                             g.magic[k], (unsigned)g.N[k]);
+                        base += (long long)n * g.stride[k];
+                        delta[k] = (n + 1 == (unsigned)g.N[k]) ? -(long long)n * g.stride[k]
+                                                                : g.stride[k];
+                    }
+                }
+                v[c][0] = ld_stream(cube + base);
+#pragma unroll
+                for (int k = 0; k < MAXD; ++k)
+                    if (k < D) v[c][k + 1] = ld_stream(cube + base + delta[k]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int l = l0 + c * nth;
+            if (l < L) {
+#pragma unroll
+                for (int k = 0; k < MAXD + 1; ++k) {
+                    if (k <= D) {
+                        spec[k * L + l] = {(R)v[c][k].x, (R)v[c][k].y};
+                        energy += (R)v[c][k].x * (R)v[c][k].x + (R)v[c][k].y * (R)v[c][k].y;
+                    }
+                }
+            }
+        }
+    }
+    return energy;
+}
+
+template <class R>
+__device__ __forceinline__ R line_energy(const cpx<R> *spec, int n, int tid, int nth) {
+    R e = (R)0;
+    for (int i = tid; i < n; i += nth) e += spec[i].re * spec[i].re + spec[i].im * spec[i].im;
+    return e;
 }
 
 // ------------------------------------------------------------------- FFT
@@ -284,150 +438,240 @@ struct Bfly<R, 16> {
     }
 };
 
-// One Stockham stage: butterfly q (of nlines*L/RAD) reads x[line][j + k L/RAD],
-// twiddles by W_{Ns RAD}^{(j mod Ns) k}, and writes y[line][(j - j mod Ns) RAD
-// + j mod Ns + k Ns].  Each thread owns MB butterflies (q = tid + i*NT); the
-// host sizes NT so MB*NT covers the stage.
-template <class R, int RAD, int MB>
-__device__ __forceinline__ void fft_stage(cpx<R> *x, int nlines, int L, int Ns,
-                                          const cpx<R> *roots, bool last) {
-    const int m = L / RAD, total = nlines * m, NT = blockDim.x;
-    const int step = L / (Ns * RAD);
-    cpx<R> v[MB][RAD];
-    int ob[MB];
+// One Stockham stage: butterfly q (of G*L/RAD for a group of G lines) reads
+// x[line][j + k L/RAD], twiddles by W_{Ns RAD}^{(j mod Ns) k}, and writes
+// x[line][(j - j mod Ns) RAD + j mod Ns + k Ns].  Each of the team's `nth`
+// threads owns up to MB butterflies of a group; lines are processed G at a
+// time so that a group's butterflies fit the team's registers.
+template <class R, int RAD, int MB, class Team>
+__device__ __forceinline__ void fft_stage(cpx<R> *x, int nlines, int G, int L, int Ns,
+                                          const cpx<R> *roots, bool last, int tid, int nth) {
+    const int m = L / RAD, step = L / (Ns * RAD);
+    const R inv = (R)1 / (R)L;
+    const bool pow2 = (L & (L - 1)) == 0;  // then x * (1/L) == x / L exactly
+    for (int l0 = 0; l0 < nlines; l0 += G) {
+        const int total = min(G, nlines - l0) * m;
+        cpx<R> v[MB][RAD];
+        int ob[MB];
 #pragma unroll
-    for (int j = 0; j < MB; ++j) {
-        const int q = threadIdx.x + j * NT;
-        ob[j] = -1;
-        if (q < total) {
-            const int line = q / m, jj = q - line * m;
-            const cpx<R> *xl = x + line * L;
+        for (int j = 0; j < MB; ++j) {
+            const int q = tid + j * nth;
+            ob[j] = -1;
+            if (q < total) {
+                const int line = l0 + q / m, jj = q % m;
+                const cpx<R> *xl = x + line * L;
 #pragma unroll
-            for (int k = 0; k < RAD; ++k) v[j][k] = xl[jj + k * m];
-            const int jm = jj % Ns;
-            if (jm) {
+                for (int k = 0; k < RAD; ++k) v[j][k] = xl[jj + k * m];
+                const int jm = jj % Ns;
+                if (jm) {
 #pragma unroll
-                for (int k = 1; k < RAD; ++k) v[j][k] = mulc(v[j][k], roots[jm * k * step]);
-            }
-            Bfly<R, RAD>::run(v[j], roots, L);
-            ob[j] = line * L + (jj - jm) * RAD + jm;
-        }
-    }
-    __syncthreads();
-    const R fl = (R)L;
-#pragma unroll
-    for (int j = 0; j < MB; ++j) {
-        if (ob[j] >= 0) {
-#pragma unroll
-            for (int k = 0; k < RAD; ++k) {
-                cpx<R> o = v[j][k];
-                if (last) o = {o.re / fl, o.im / fl};
-                x[ob[j] + k * Ns] = o;
+                    for (int k = 1; k < RAD; ++k) v[j][k] = mulc(v[j][k], roots[jm * k * step]);
+                }
+                Bfly<R, RAD>::run(v[j], roots, L);
+                ob[j] = line * L + (jj - jm) * RAD + jm;
             }
         }
+        Team::sync();
+#pragma unroll
+        for (int j = 0; j < MB; ++j) {
+            if (ob[j] >= 0) {
+#pragma unroll
+                for (int k = 0; k < RAD; ++k) {
+                    cpx<R> o = v[j][k];
+                    if (last && pow2) o = {o.re * inv, o.im * inv};
+                    x[ob[j] + k * Ns] = o;
+                }
+            }
+        }
+        Team::sync();
     }
-    __syncthreads();
 }
 
 // Direct O(L^2) pass for lengths with a prime factor > 7 (test-size L only).
-template <class R, int MB>
-__device__ __forceinline__ void dft_direct(cpx<R> *x, int nlines, int L, const cpx<R> *roots) {
-    const int total = nlines * L, NT = blockDim.x;
-    cpx<R> acc[MB];
-#pragma unroll
-    for (int j = 0; j < MB; ++j) {
-        const int q = threadIdx.x + j * NT;
-        if (q < total) {
-            const int line = q / L, k = q - line * L;
-            const cpx<R> *xl = x + line * L;
-            cpx<R> a = {(R)0, (R)0};
-            int idx = 0;
-            for (int l = 0; l < L; ++l) {
-                a = a + mulc(xl[l], roots[idx]);
-                idx += k;
-                if (idx >= L) idx -= L;
-            }
-            acc[j] = a;
-        }
-    }
-    __syncthreads();
+template <class R, int MB, class Team>
+__device__ __forceinline__ void dft_direct(cpx<R> *x, int nlines, int G, int L,
+                                          const cpx<R> *roots, int tid, int nth) {
     const R fl = (R)L;
+    for (int l0 = 0; l0 < nlines; l0 += G) {
+        const int total = min(G, nlines - l0) * L;
+        cpx<R> acc[MB];
 #pragma unroll
-    for (int j = 0; j < MB; ++j) {
-        const int q = threadIdx.x + j * NT;
-        if (q < total) x[q] = {acc[j].re / fl, acc[j].im / fl};
+        for (int j = 0; j < MB; ++j) {
+            const int q = tid + j * nth;
+            if (q < total) {
+                const int line = l0 + q / L, k = q % L;
+                const cpx<R> *xl = x + line * L;
+                cpx<R> a = {(R)0, (R)0};
+                int idx = 0;
+                for (int l = 0; l < L; ++l) {
+                    a = a + mulc(xl[l], roots[idx]);
+                    idx += k;
+                    if (idx >= L) idx -= L;
+                }
+                acc[j] = a;
+            }
+        }
+        Team::sync();
+#pragma unroll
+        for (int j = 0; j < MB; ++j) {
+            const int q = tid + j * nth;
+            if (q < total) x[l0 * L + q] = {acc[j].re / fl, acc[j].im / fl};
+        }
+        Team::sync();
     }
-    __syncthreads();
 }
 
-template <class R, int RAD>
-__device__ __forceinline__ void fft_stage_mb(cpx<R> *x, int nlines, int L, int Ns, int mb,
-                                             const cpx<R> *roots, bool last) {
+// 1/L for lengths that are not powers of two, as a true division (what
+// fft(s)/L computes); kept out of the butterfly code so the division's slow
+// path does not force the butterfly registers to spill.
+template <class R, class Team>
+__device__ __noinline__ void divide_by_length(cpx<R> *x, int n, int L, int tid, int nth) {
+    const R fl = (R)L;
+    for (int i = tid; i < n; i += nth) x[i] = {x[i].re / fl, x[i].im / fl};
+    Team::sync();
+}
+
+template <class R, int RAD, class Team>
+__device__ __forceinline__ void fft_stage_mb(cpx<R> *x, int nlines, int G, int L, int Ns,
+                                             int mb, const cpx<R> *roots, bool last, int tid,
+                                             int nth) {
     // register budget (matches plan_fft's caps): complex values per thread
     // <= 16 (float) / 8 (double)
-    constexpr int R4 = sizeof(R) == 4 ? (RAD <= 4 ? 4 : (RAD <= 8 ? 2 : 1))
-                                      : (RAD <= 2 ? 4 : (RAD <= 4 ? 2 : 1));
-    if (mb <= 1) fft_stage<R, RAD, 1>(x, nlines, L, Ns, roots, last);
-    else if (mb <= 2 || R4 < 4) fft_stage<R, RAD, (R4 < 2 ? 1 : 2)>(x, nlines, L, Ns, roots, last);
-    else fft_stage<R, RAD, R4>(x, nlines, L, Ns, roots, last);
+    constexpr int CAP = sizeof(R) == 4 ? (RAD <= 4 ? 4 : (RAD <= 8 ? 2 : 1))
+                                       : (RAD <= 2 ? 4 : (RAD <= 4 ? 2 : 1));
+    if (mb <= 1) fft_stage<R, RAD, 1, Team>(x, nlines, G, L, Ns, roots, last, tid, nth);
+    else if (mb <= 2 || CAP < 4)
+        fft_stage<R, RAD, (CAP < 2 ? 1 : 2), Team>(x, nlines, G, L, Ns, roots, last, tid, nth);
+    else fft_stage<R, RAD, CAP, Team>(x, nlines, G, L, Ns, roots, last, tid, nth);
 }
 
-template <class R>
+// Forward DFT (1/L normalised) of `nlines` contiguous lines per the plan in g.
+template <class R, class Team>
 __device__ __forceinline__ void fft_lines(cpx<R> *x, int nlines, const Geo &g,
-                                          const cpx<R> *roots) {
+                                          const cpx<R> *roots, int tid, int nth) {
     int Ns = 1;
     for (int s = 0; s < g.nstages; ++s) {
         const int code = stage_code(g, s);
-        const int r = code & 31, mb = code >> 5;
+        const int r = code & 31, mb = (code >> 5) & 7, G = (code >> 8) & 7;
         const bool last = (s == g.nstages - 1);
         switch (r) {
-            case 16: fft_stage_mb<R, 16>(x, nlines, g.L, Ns, mb, roots, last); break;
-            case 8: fft_stage_mb<R, 8>(x, nlines, g.L, Ns, mb, roots, last); break;
-            case 4: fft_stage_mb<R, 4>(x, nlines, g.L, Ns, mb, roots, last); break;
-            case 2: fft_stage_mb<R, 2>(x, nlines, g.L, Ns, mb, roots, last); break;
-            case 3: fft_stage_mb<R, 3>(x, nlines, g.L, Ns, mb, roots, last); break;
-            case 5: fft_stage_mb<R, 5>(x, nlines, g.L, Ns, mb, roots, last); break;
-            case 7: fft_stage_mb<R, 7>(x, nlines, g.L, Ns, mb, roots, last); break;
+            case 16: fft_stage_mb<R, 16, Team>(x, nlines, G, g.L, Ns, mb, roots, last, tid, nth); break;
+            case 8: fft_stage_mb<R, 8, Team>(x, nlines, G, g.L, Ns, mb, roots, last, tid, nth); break;
+            case 4: fft_stage_mb<R, 4, Team>(x, nlines, G, g.L, Ns, mb, roots, last, tid, nth); break;
+            case 2: fft_stage_mb<R, 2, Team>(x, nlines, G, g.L, Ns, mb, roots, last, tid, nth); break;
+            case 3: fft_stage_mb<R, 3, Team>(x, nlines, G, g.L, Ns, mb, roots, last, tid, nth); break;
+            case 5: fft_stage_mb<R, 5, Team>(x, nlines, G, g.L, Ns, mb, roots, last, tid, nth); break;
+            case 7: fft_stage_mb<R, 7, Team>(x, nlines, G, g.L, Ns, mb, roots, last, tid, nth); break;
             default:
-                if (mb <= 1) dft_direct<R, 1>(x, nlines, g.L, roots);
-                else if (mb <= 2) dft_direct<R, 2>(x, nlines, g.L, roots);
-                else dft_direct<R, 4>(x, nlines, g.L, roots);
+                if (mb <= 1) dft_direct<R, 1, Team>(x, nlines, G, g.L, roots, tid, nth);
+                else if (mb <= 2) dft_direct<R, 2, Team>(x, nlines, G, g.L, roots, tid, nth);
+                else dft_direct<R, 4, Team>(x, nlines, G, g.L, roots, tid, nth);
                 break;
         }
         Ns *= (r > 0 ? r : g.L);
     }
-    if (g.nstages == 0) {  // L == 1: the DFT of one sample is itself
-        __syncthreads();
+    if (g.nstages == 0) Team::sync();  // L == 1: the DFT of one sample is itself
+    const int r0 = stage_code(g, 0) & 31;
+    if (g.nstages > 0 && r0 != 0 && (g.L & (g.L - 1)) != 0)
+        divide_by_length<R, Team>(x, nlines * g.L, g.L, tid, nth);
+}
+
+// Warp-team FFT for power-of-two L: radices 8/4/2 only, each stage with its
+// full register batch (guarded), which keeps the warp kernel's code small.
+template <class R>
+__device__ __forceinline__ void fft_lines_warp(cpx<R> *x, int nlines, const Geo &g,
+                                               const cpx<R> *roots, int lane) {
+    constexpr bool F = sizeof(R) == 4;
+    int Ns = 1;
+    for (int s = 0; s < g.nstages; ++s) {
+        const int code = stage_code(g, s);
+        const int r = code & 31, G = (code >> 8) & 7;
+        const bool last = (s == g.nstages - 1);
+        if (F && r == 16) fft_stage<R, 16, 1, WarpTeam>(x, nlines, G, g.L, Ns, roots, last, lane, 32);
+        else if (r == 8) fft_stage<R, 8, F ? 2 : 1, WarpTeam>(x, nlines, G, g.L, Ns, roots, last, lane, 32);
+        else if (r == 4) fft_stage<R, 4, F ? 4 : 2, WarpTeam>(x, nlines, G, g.L, Ns, roots, last, lane, 32);
+        else fft_stage<R, 2, 4, WarpTeam>(x, nlines, G, g.L, Ns, roots, last, lane, 32);
+        Ns *= r;
     }
+    if (g.nstages == 0) __syncwarp();
 }
 
 // ------------------------------------------------------------- bin map
-// bin(m) = sum_k (c_k alpha_k mod L) m_k mod L (numtheory.py:139-153);
-// u_tau(m) = sum_k c_k tau_k m_k mod L (decoder.py:41-46).  The host guards
-// D * L * max N_k < 2^31 so int32 products are exact.
+// bin(m) = sum_k c_k alpha_k m_k mod L (numtheory.py:139-153);
+// u_tau(m) = sum_k c_k tau_k m_k mod L (decoder.py:41-46).  Every term is
+// < L * N_k and the host guards D * L * max N_k < 2^31, so int32 is exact.
 __device__ __forceinline__ int bin_of(const int *m, const Geo &g, const int *al) {
     int acc = 0;
 #pragma unroll
     for (int k = 0; k < MAXD; ++k)
-        if (k < g.D) acc += ((g.cof[k] * al[k]) % g.L) * m[k];
+        if (k < g.D) acc += g.cof[k] * al[k] * m[k];
     return acc % g.L;
 }
 __device__ __forceinline__ int phase_of(const int *m, const Geo &g, const int *ta) {
     int acc = 0;
 #pragma unroll
     for (int k = 0; k < MAXD; ++k)
-        if (k < g.D) acc += ((g.cof[k] * ta[k]) % g.L) * m[k];
+        if (k < g.D) acc += g.cof[k] * ta[k] * m[k];
     return acc % g.L;
 }
 // Phase of offset i (0 = tau, i = tau + e_{i-1}) from u_0: the step adds
-// c_{i-1} m_{i-1} (a wrap of tau adds L m, which vanishes mod L).
-// (Selects instead of indexing with i keeps m and g in registers.)
+// c_{i-1} m_{i-1} < L (a wrap of tau adds L m, which vanishes mod L).
+// (Selects instead of indexing with i keep m and g in registers.)
 __device__ __forceinline__ int phase_step(int u0, int i, const int *m, const Geo &g) {
     int add = 0;
 #pragma unroll
     for (int k = 0; k < MAXD; ++k)
         if (k == i - 1) add = g.cof[k] * m[k];
-    return (int)(((long long)u0 + add) % g.L);
+    const int u = u0 + add;
+    return u >= g.L ? u - g.L : u;
+}
+
+// The magnitude half of the 1-sparse test (decoder.py:146-148): occupied
+// (|S_0| > floor) and all D+1 magnitudes within mag_tol of the largest.
+// Float64 evaluates it exactly as the reference (hypot magnitudes); float32
+// compares squared magnitudes (no square roots): top - low <= t top  <=>
+// low^2 >= (1 - t)^2 top^2 for t < 1.  `res` receives the bin's largest
+// |S_i|^2 (float) / |S_i| (double) for the termination test.
+template <class R>
+__device__ __forceinline__ bool bin_is_candidate(const cpx<R> *spec, const Geo &g, int b,
+                                                 R mag_tol, R floor, R *res) {
+    if constexpr (sizeof(R) == 4) {
+        const R q0 = cabs2(spec[b]);
+        R top = q0, low = q0;
+#pragma unroll
+        for (int i = 1; i < MAXD + 1; ++i) {
+            if (i <= g.D) {
+                const R qi = cabs2(spec[i * g.L + b]);
+                top = max(top, qi);
+                low = min(low, qi);
+            }
+        }
+        *res = top;
+        const R c = (R)1 - mag_tol;
+        return q0 > floor * floor && (mag_tol >= (R)1 || low >= c * c * top);
+    } else {
+        const R m0 = cabs(spec[b]);
+        R top = m0, low = m0;
+#pragma unroll
+        for (int i = 1; i < MAXD + 1; ++i) {
+            if (i <= g.D) {
+                const R mi = cabs(spec[i * g.L + b]);
+                top = max(top, mi);
+                low = min(low, mi);
+            }
+        }
+        *res = top;
+        return m0 > floor && (top - low) <= mag_tol * top;
+    }
+}
+// Largest |S_i[b]|^2 (float) or |S_i[b]| (double) over the D+1 lines.
+template <class R>
+__device__ __forceinline__ R bin_residual(const cpx<R> *spec, const Geo &g, int b) {
+    R top = (R)0;
+#pragma unroll
+    for (int i = 0; i < MAXD + 1; ++i)
+        if (i <= g.D) top = max(top, sizeof(R) == 4 ? cabs2(spec[i * g.L + b]) : cabs(spec[i * g.L + b]));
+    return top;
 }
 
 // ---------------------------------------------------------- classifier
@@ -483,6 +727,52 @@ __device__ __forceinline__ int classify_bin(const cpx<R> *spec, const Geo &g, in
         if (i <= D) {
             cpx<R> d = amp * roots[phase_step(u0, i, m, g)] - s[i];
             ok = ok && (cabs(d) <= lim);
+        }
+    }
+    if (!ok) return 1;
+    *amp_out = amp;
+    if (al != nullptr && bin_of(m, g, al) != b) return 3;
+    return 2;
+}
+
+// As classify_bin for a bin already known to pass the magnitude test.
+template <class R>
+__device__ __forceinline__ int decode_candidate(const cpx<R> *spec, const Geo &g, int b,
+                                            const int *al, const int *ta, const cpx<R> *roots,
+                                            R round_tol, R verify_tol,
+                                            int *m, cpx<R> *amp_out) {
+    const int L = g.L, D = g.D;
+    cpx<R> s[MAXD + 1];
+#pragma unroll
+    for (int i = 0; i < MAXD + 1; ++i)
+        if (i <= D) s[i] = spec[i * L + b];
+    const R mag0 = cabs(s[0]);
+    const R two_pi = (R)6.283185307179586476925286766559;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+        if (k < D) {
+            cpx<R> z = mulc(s[k + 1], s[0]);
+            R theta = atan2(z.im, z.re);
+            // float64: the reference's n * angle / (2 pi); float32 multiplies
+            // by the reciprocal (no division slow path)
+            R raw = sizeof(R) == 8 ? (R)g.N[k] * theta / two_pi
+                                   : (R)g.N[k] * theta * (R)0.15915494309189533577;
+            R near = rint(raw);
+            ok = ok && (fabs(raw - near) <= round_tol);
+            int mk = ((int)near) % g.N[k];
+            m[k] = mk < 0 ? mk + g.N[k] : mk;
+        }
+    }
+    if (!ok) return 1;
+    const int u0 = phase_of(m, g, ta);
+    const cpx<R> amp = mulc(s[0], roots[u0]);
+    const R lim = verify_tol * mag0;
+#pragma unroll
+    for (int i = 0; i < MAXD + 1; ++i) {
+        if (i <= D) {
+            cpx<R> d = amp * roots[phase_step(u0, i, m, g)] - s[i];
+            ok = ok && (sizeof(R) == 8 ? cabs(d) <= lim : cabs2(d) <= lim * lim);
         }
     }
     if (!ok) return 1;

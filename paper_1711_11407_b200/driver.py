@@ -114,9 +114,13 @@ def _precision_code(precision: str) -> int:
     raise ValueError(f"unknown precision {precision!r}")
 
 
-def _params(config: FpsSftConfig, t_max: int, k_cap: int, precision: int) -> N.Params:
+def _params(config: FpsSftConfig, t_max: int, k_cap: int, precision: int,
+            mode: str = "auto") -> N.Params:
     p = N.Params()
     p.t_max, p.stall_limit, p.k_cap, p.precision = t_max, config.stall_limit, k_cap, precision
+    if mode not in N.MODES:
+        raise ValueError(f"mode must be one of {sorted(N.MODES)}")
+    p.mode = N.MODES[mode]
     for name in ("mag_tol", "verify_tol", "round_tol", "amp_prune_tol", "energy_floor",
                  "energy_floor_abs", "residual_stop"):
         setattr(p, name, float(getattr(config, name)))
@@ -133,16 +137,14 @@ def _pow2_ceil(x: int) -> int:
     return 1 << max(0, int(x - 1).bit_length())
 
 
-def max_k_cap(shape: CubeShape, precision: str = "fp32") -> int:
-    """Largest power-of-two capacity whose on-chip state fits one CTA."""
+def max_k_cap(shape: CubeShape, precision: str = "fp32", mode: str = "auto") -> int:
+    """Largest power-of-two capacity whose on-chip state fits (in ``mode``)."""
     sh = N.make_shape(shape.dims)
     best = 0
     k = 1
-    limit = 227 * 1024
     while k <= (1 << 20):
-        p = _params(FpsSftConfig(), 1, k, _precision_code(precision))
-        need = N.lib().fpssft_smem_bytes(C_ref(sh), C_ref(p))
-        if need == 0 or need > limit:
+        p = _params(FpsSftConfig(), 1, k, _precision_code(precision), mode)
+        if N.lib().fpssft_smem_bytes(C_ref(sh), C_ref(p)) == 0:  # no plan fits
             break
         best = k
         k <<= 1
@@ -229,7 +231,7 @@ class BatchRunner:
 
     def __init__(self, shape: CubeShape, config: FpsSftConfig, batch: int, *, schedule=None,
                  sched_index=None, k_cap: int = 256, precision: str = "fp32",
-                 iter_stats: bool = False, device=None):
+                 iter_stats: bool = False, device=None, mode: str = "auto"):
         import torch
 
         self.shape = shape
@@ -256,16 +258,16 @@ class BatchRunner:
         self.k_cap = int(k_cap)
         self.prec = _precision_code(precision)
         self._shape_c = N.make_shape(shape.dims)
-        self._params_c = _params(config, self.t_max, self.k_cap, self.prec)
+        self._params_c = _params(config, self.t_max, self.k_cap, self.prec, mode)
+        self.plan = launch_plan(shape, self._params_c)
         self.out = allocate_outputs(self.batch, shape, self.k_cap, self.t_max, self.device,
                                     iter_stats)
         o = self.out
         self._out_c = N.Out(N.ptr(o["freqs"]), N.ptr(o["amps"]), N.ptr(o["count"]),
                             N.ptr(o["iterations"]), N.ptr(o["samples_used"]),
                             N.ptr(o["terminated_by"]), N.ptr(o["iter_stats"]))
-        self.smem_bytes = int(N.lib().fpssft_smem_bytes(C_ref(self._shape_c),
-                                                       C_ref(self._params_c)))
-        self.threads = int(N.lib().fpssft_block_threads(C_ref(self._shape_c), self.prec))
+        self.smem_bytes = self.plan["smem_bytes"]
+        self.threads = self.plan["threads_per_cta"]
 
     def run(self, cubes) -> BatchResult:
         import torch
@@ -290,9 +292,23 @@ class BatchRunner:
                            o["iter_stats"], self.schedule_host, self.sched_index_host)
 
 
+def launch_plan(shape: CubeShape, params: N.Params) -> dict:
+    """The kernel/launch shape ``fpssft_run_batch`` will use (raises if the
+    shape cannot run)."""
+    import ctypes
+
+    mode, thr, per = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    smem = ctypes.c_size_t()
+    N.check(N.lib().fpssft_plan(C_ref(N.make_shape(shape.dims)), C_ref(params), C_ref(mode),
+                                C_ref(thr), C_ref(per), C_ref(smem)))
+    return {"mode": {N.MODE_CTA: "cta", N.MODE_WARP: "warp"}[mode.value],
+            "threads_per_cta": thr.value, "instances_per_cta": per.value,
+            "smem_bytes": smem.value}
+
+
 def fps_sft_batch(cubes, config: FpsSftConfig = FpsSftConfig(), *, schedule=None,
                   sched_index=None, k_cap: int = 256, precision: str = "fp32",
-                  iter_stats: bool = False) -> BatchResult:
+                  iter_stats: bool = False, mode: str = "auto") -> BatchResult:
     """Recover every instance of ``cubes`` (complex64 CUDA tensor [B, *dims]).
 
     ``schedule``: int32 [T, 2, D] or [S, T, 2, D] (alpha, tau) per iteration;
@@ -302,7 +318,7 @@ def fps_sft_batch(cubes, config: FpsSftConfig = FpsSftConfig(), *, schedule=None
     shape = CubeShape(cubes.shape[1:])
     runner = BatchRunner(shape, config, cubes.shape[0], schedule=schedule,
                          sched_index=sched_index, k_cap=k_cap, precision=precision,
-                         iter_stats=iter_stats, device=cubes.device)
+                         iter_stats=iter_stats, device=cubes.device, mode=mode)
     return runner.run(cubes)
 
 
@@ -325,7 +341,8 @@ def materialize(source) -> tuple[CubeShape, "np.ndarray | object"]:
 
 
 def fps_sft(source: SignalSource, config: FpsSftConfig = FpsSftConfig(), *,
-            precision: str = "fp32", k_cap: int | None = None, device=None) -> RecoveryReport:
+            precision: str = "fp32", k_cap: int | None = None, device=None,
+            mode: str = "auto") -> RecoveryReport:
     """Recover the sparse spectrum of ``source`` on the GPU (driver.py:121-212).
 
     Same contract as the reference: stops on a clean residual, after
@@ -342,14 +359,15 @@ def fps_sft(source: SignalSource, config: FpsSftConfig = FpsSftConfig(), *,
         t = torch.as_tensor(np.ascontiguousarray(cube, dtype=np.complex64)).to(dev)
     t = t.reshape((1, *shape.dims))
     if k_cap is None:
-        k_cap = min(_pow2_ceil(shape.n_total), max_k_cap(shape, precision))
+        k_cap = min(_pow2_ceil(shape.n_total), max_k_cap(shape, precision, mode))
         if k_cap < 1:
             raise N.UnsupportedError(f"shape {shape.dims} does not fit one CTA")
-    res = fps_sft_batch(t, config, k_cap=k_cap, precision=precision, iter_stats=True)
+    res = fps_sft_batch(t, config, k_cap=k_cap, precision=precision, iter_stats=True, mode=mode)
     return res.report(0)
 
 
 __all__ = ["FpsSftConfig", "IterationStats", "RecoveryReport", "BatchResult", "BatchRunner",
-           "default_max_iterations", "fps_sft", "fps_sft_batch", "materialize", "max_k_cap",
+           "default_max_iterations", "fps_sft", "fps_sft_batch", "launch_plan", "materialize",
+           "max_k_cap",
            "PROFILES", "TERMINATED_RESIDUAL_CLEAN", "TERMINATED_STALL",
            "TERMINATED_MAX_ITERATIONS", "TERMINATED_K_CAP_OVERFLOW"]

@@ -130,31 +130,35 @@ def make_spectra(w: Workload, count: int | None = None, start: int = 0):
 def synthesize_batch_torch(dims, spectra, device, noise_var=0.0, noise_seed=0, out=None):
     """Device-side batch synthesis for the big configs (untimed data
     generation; cuFFT is used here only to build inputs).  Returns a
-    complex64 tensor [B, *dims] on ``device``."""
+    complex64 tensor [B, *dims] on ``device``.  Noise comes from a torch
+    generator seeded with ``noise_seed`` (deterministic for a given device
+    type and chunking)."""
     import torch
 
+    dims = tuple(int(d) for d in dims)
     B = len(spectra)
     if out is None:
         out = torch.empty((B, *dims), dtype=torch.complex64, device=device)
     N = math.prod(dims)
     chunk = max(1, min(B, (1 << 28) // (N * 16)))
     gen = torch.Generator(device=device)
-    gen.manual_seed(noise_seed)
+    gen.manual_seed(int(noise_seed))
     for s in range(0, B, chunk):
         e = min(B, s + chunk)
-        grid = torch.zeros((e - s, N), dtype=torch.complex128, device=device)
-        for j, (f, a) in enumerate(spectra[s:e]):
-            lin = np.ravel_multi_index(tuple(np.asarray(f).T), dims)
-            grid[j].index_put_((torch.as_tensor(lin, device=device),),
-                               torch.as_tensor(a, dtype=torch.complex128, device=device),
-                               accumulate=True)
+        lin = np.concatenate([np.ravel_multi_index(tuple(np.asarray(f).T), dims) + j * N
+                              for j, (f, _) in enumerate(spectra[s:e])])
+        amp = np.concatenate([np.asarray(a, np.complex128) for _, a in spectra[s:e]])
+        grid = torch.zeros((e - s) * N, dtype=torch.complex128, device=device)
+        grid.index_put_((torch.as_tensor(lin, device=device),),
+                        torch.as_tensor(amp, device=device), accumulate=True)
         grid = grid.view(e - s, *dims)
         cube = torch.fft.ifftn(grid, dim=tuple(range(1, len(dims) + 1))) * N
+        del grid
         if noise_var > 0:
             sd = math.sqrt(noise_var / 2)
-            cube = cube + torch.complex(
-                torch.randn(cube.shape, dtype=torch.float64, device=device, generator=gen),
-                torch.randn(cube.shape, dtype=torch.float64, device=device, generator=gen)) * sd
-        out[s:e].copy_(cube.to(torch.complex64))
-        del grid, cube
+            nz = torch.randn((2, *cube.shape), dtype=torch.float64, device=device, generator=gen)
+            cube += torch.complex(nz[0], nz[1]) * sd
+            del nz
+        out[s:e].copy_(cube)
+        del cube
     return out

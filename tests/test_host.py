@@ -142,3 +142,15 @@ def test_smem_budget_fits_configs():
         p = P.driver._params(P.FpsSftConfig(), 8, k_cap, N.F32)
         need = N.lib().fpssft_smem_bytes(_byref(N.make_shape(dims)), _byref(p))
         assert 0 < need <= 227 * 1024, (dims, need)
+
+
+@pytest.mark.parametrize("dims,k_cap,mode", [((256, 256), 256, "warp"), ((512, 512), 1024, "warp"),
+                                           ((64, 64, 64), 512, "warp"), ((1024, 2048), 2048, "cta"),
+                                           ((12, 18), 64, "cta")])
+def test_launch_plan_picks_kernel(dims, k_cap, mode):
+    p = P.driver._params(P.FpsSftConfig(), 8, k_cap, N.F32)
+    plan = P.driver.launch_plan(P.CubeShape(dims), p)
+    assert plan["mode"] == mode
+    assert 0 < plan["smem_bytes"] <= 227 * 1024
+    if mode == "warp":
+        assert plan["threads_per_cta"] == 32 * plan["instances_per_cta"]
