@@ -484,14 +484,22 @@ __device__ __forceinline__ void hash16_insert(unsigned short *hash, int H, int k
         h = (h + 1) & (unsigned)(H - 1);
 }
 
-template <class R>
+// LC / DC: compile-time line length and dimensionality (0 = runtime), so the
+// benchmark shapes get fully unrolled gathers, FFTs and bin loops.
+template <class R, int LC, int DC>
 __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__restrict__ cubes,
                                                            long long batch, long long batch_stride,
-                                                           Geo g, Knobs kn,
+                                                           Geo g_in, Knobs kn,
                                                            const int *__restrict__ schedule,
                                                            const int *__restrict__ sched_index,
                                                            int n_sched, OutPtrs out) {
     extern __shared__ __align__(16) unsigned char sm[];
+    Geo g = g_in;
+    if (LC) g.L = LC;
+    if (DC) {
+        g.D = DC;
+        g.nlines = DC + 1;
+    }
     const WarpLayout lay = make_warp_layout(g.D, g.L, kn.k_cap, (int)sizeof(cpx<R>));
     cpx<R> *roots = (cpx<R> *)sm;
     build_roots(roots, g.L);
@@ -551,7 +559,7 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
         // (1) gather + (2) DFT of the D+1 lines           driver.py:146-154
         R my_energy;
         if constexpr (sizeof(R) == 4) {
-            gather_lines_async(spec, cube, g, al, ta, lane, 32);
+            gather_lines_async<LC>(spec, cube, g, al, ta, lane, 32);
             if (it + 1 < kn.t_max) {
 #pragma unroll
                 for (int k = 0; k < MAXD; ++k) {
@@ -573,7 +581,10 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
             }
             __syncwarp();
         }
-        fft_lines_warp<R>(spec, nl, g, roots, lane);
+        if constexpr (LC != 0)
+            fft_static<R, LC, DC + 1>(spec, roots, lane);
+        else
+            fft_lines_warp<R>(spec, nl, g, roots, lane);
         R noise_floor = (R)0;
         if (sizeof(R) == 4 && kn.noise_coef > 0)
             noise_floor = (R)kn.noise_coef * sqrt(__shfl_sync(FULL, warp_sum(my_energy), 0));
@@ -1191,12 +1202,17 @@ int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
     if (rc != FPSSFT_OK) return rc;
     cudaError_t e;
     if (lp.mode == FPSSFT_MODE_WARP) {
-        e = cudaFuncSetAttribute(recover_warp_kernel<R>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lp.smem);
+        // compile-time specialisations for the benchmark shapes
+        auto kernel = recover_warp_kernel<R, 0, 0>;
+        if (g.off32 && g.D == 2 && g.L == 256) kernel = recover_warp_kernel<R, 256, 2>;
+        else if (g.off32 && g.D == 2 && g.L == 512) kernel = recover_warp_kernel<R, 512, 2>;
+        else if (g.off32 && g.D == 3 && g.L == 64) kernel = recover_warp_kernel<R, 64, 3>;
+        e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lp.smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recover_warp_kernel)");
         if (batch == 0) return FPSSFT_OK;
         const long long grid = (batch + lp.per_cta - 1) / lp.per_cta;
-        recover_warp_kernel<R><<<(unsigned)grid, lp.threads, lp.smem, st>>>(
+        kernel<<<(unsigned)grid, lp.threads, lp.smem, st>>>(
             (const float2 *)cubes, (long long)batch, (long long)batch_stride, g, kn, schedule,
             sched_index, n_sched, o);
         return check_launch("recover_warp_kernel");

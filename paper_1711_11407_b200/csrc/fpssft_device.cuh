@@ -221,11 +221,42 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
+template <int LC = 0>
 __device__ __forceinline__ void gather_lines_async(cpx<float> *spec,
                                                    const float2 *__restrict__ cube, const Geo &g,
                                                    const int *al, const int *ta, int tid,
                                                    int nth) {
     const int L = g.L, D = g.D;
+    if (LC && g.off32) {  // compile-time line length, one warp: fixed trip count
+        int n[MAXD], step[MAXD];
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) {
+            n[k] = k < D ? (int)fastmod((unsigned)al[k] * (unsigned)tid + (unsigned)ta[k],
+                                        g.magic[k], (unsigned)g.N[k])
+                         : 0;
+            step[k] = k < D ? (int)fastmod((unsigned)al[k] * 32u, g.magic[k], (unsigned)g.N[k])
+                            : 0;
+        }
+#pragma unroll 4
+        for (int j = 0; j < LC / 32; ++j) {
+            const int l = tid + 32 * j;
+            int base = 0;
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k)
+                if (k < D) base += n[k] * g.stride32[k];
+            cp_async8(spec + l, cube + base);
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k) {
+                if (k < D) {
+                    const int d = (n[k] + 1 == g.N[k]) ? -n[k] * g.stride32[k] : g.stride32[k];
+                    cp_async8(spec + (k + 1) * LC + l, cube + (base + d));
+                    n[k] += step[k];
+                    if (n[k] >= g.N[k]) n[k] -= g.N[k];
+                }
+            }
+        }
+        return;
+    }
     if (g.off32) {
         // n_k(l) advanced incrementally by alpha_k * nth mod N_k: no division,
         // 32-bit offsets
@@ -594,6 +625,82 @@ __device__ __forceinline__ void fft_lines_warp(cpx<R> *x, int nlines, const Geo 
         Ns *= r;
     }
     if (g.nstages == 0) __syncwarp();
+}
+
+// Compile-time FFT for the line lengths of the benchmark configs (warp
+// teams): every index, group and twiddle stride is a constant, so the stage
+// loops fully unroll.  Stage: radix RAD after NS points have been combined.
+template <class R, int L, int NL, int RAD, int NS, bool LAST>
+__device__ __forceinline__ void stage_static(cpx<R> *x, const cpx<R> *roots, int lane) {
+    constexpr int M = L / RAD;                                   // butterflies per line
+    constexpr int CAPB = RAD == 16 ? 1 : (RAD == 8 ? 2 : 4);     // per lane (registers)
+    constexpr int G0 = CAPB * 32 / M;
+    constexpr int G = G0 < 1 ? 1 : (G0 > NL ? NL : G0);          // lines per group
+    constexpr int MB = (G * M + 31) / 32;
+    static_assert(MB <= CAPB, "stage does not fit the warp's registers");
+    constexpr int STEP = L / (NS * RAD);
+    const R inv = (R)1 / (R)L;
+#pragma unroll
+    for (int l0 = 0; l0 < NL; l0 += G) {
+        const int total = (NL - l0 < G ? NL - l0 : G) * M;
+        cpx<R> v[MB][RAD];
+        int ob[MB];
+#pragma unroll
+        for (int j = 0; j < MB; ++j) {
+            const int q = lane + 32 * j;
+            ob[j] = -1;
+            if (q < total) {
+                const int line = l0 + q / M, jj = q % M;
+                const cpx<R> *xl = x + line * L;
+#pragma unroll
+                for (int k = 0; k < RAD; ++k) v[j][k] = xl[jj + k * M];
+                if (NS > 1) {
+                    const int jm = jj % NS;
+#pragma unroll
+                    for (int k = 1; k < RAD; ++k) v[j][k] = mulc(v[j][k], roots[jm * k * STEP]);
+                    ob[j] = line * L + (jj - jm) * RAD + jm;
+                } else {
+                    ob[j] = line * L + jj * RAD;
+                }
+                Bfly<R, RAD>::run(v[j], roots, L);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < MB; ++j) {
+            if (ob[j] >= 0) {
+#pragma unroll
+                for (int k = 0; k < RAD; ++k) {
+                    cpx<R> o = v[j][k];
+                    if (LAST) o = {o.re * inv, o.im * inv};  // L is a power of two: exact
+                    x[ob[j] + k * NS] = o;
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <class R, int L, int NL>
+__device__ __forceinline__ void fft_static(cpx<R> *x, const cpx<R> *roots, int lane) {
+    constexpr bool F = sizeof(R) == 4;
+    if constexpr (L == 256 && F) {
+        stage_static<R, L, NL, 16, 1, false>(x, roots, lane);
+        stage_static<R, L, NL, 16, 16, true>(x, roots, lane);
+    } else if constexpr (L == 256) {
+        stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
+        stage_static<R, L, NL, 8, 8, false>(x, roots, lane);
+        stage_static<R, L, NL, 4, 64, true>(x, roots, lane);
+    } else if constexpr (L == 512) {
+        stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
+        stage_static<R, L, NL, 8, 8, false>(x, roots, lane);
+        stage_static<R, L, NL, 8, 64, true>(x, roots, lane);
+    } else if constexpr (L == 64) {
+        stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
+        stage_static<R, L, NL, 8, 8, true>(x, roots, lane);
+    } else {
+        static_assert(L == 64 || L == 256 || L == 512, "no static plan for this L");
+    }
 }
 
 // ------------------------------------------------------------- bin map
