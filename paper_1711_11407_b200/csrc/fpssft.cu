@@ -438,7 +438,7 @@ struct WarpLayout {
 
 __host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, int cs) {
     WarpLayout y;
-    const size_t spec_bytes = (size_t)(D + 1) * L * cs, sort_bytes = (size_t)k_cap * 8;
+    const size_t spec_bytes = (size_t)(D + 1) * L * cs, sort_bytes = 1024 + (size_t)k_cap * 4;
     size_t o = 0;
     y.H = 2 * k_cap;
     y.spec = o;      o = align16(o + (spec_bytes > sort_bytes ? spec_bytes : sort_bytes));
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
             }
             cp_async_wait_all();
             __syncwarp();
-            my_energy = kn.noise_coef > 0 ? line_energy(spec, nl * L, lane, 32) : (R)0;
+            my_energy = (LC == 0 && kn.noise_coef > 0) ? line_energy(spec, nl * L, lane, 32) : (R)0;
         } else {
             my_energy = gather_lines(spec, cube, g, al, ta, lane, 32);
             if (it + 1 < kn.t_max) {
@@ -581,9 +581,10 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
             }
             __syncwarp();
         }
-        if constexpr (LC != 0)
-            fft_static<R, LC, DC + 1>(spec, roots, lane);
-        else
+        if constexpr (LC != 0) {
+            const R e = fft_static<R, LC, DC + 1>(spec, roots, lane);
+            if (sizeof(R) == 4) my_energy = e;
+        } else
             fft_lines_warp<R>(spec, nl, g, roots, lane);
         R noise_floor = (R)0;
         if (sizeof(R) == 4 && kn.noise_coef > 0)
@@ -726,40 +727,63 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
         }
     }
 
-    // ---- RecoveryReport: live entries sorted by packed key (= lexicographic)
+    // ---- RecoveryReport: live entries sorted by packed key (= lexicographic).
+    // Counting sort on the key's top 8 bits (shared-memory histogram, warp
+    // scan, scatter), then insertion sort inside the (short) buckets.
     __syncwarp();
-    int P = 1;
-    while (P < n_slots) P <<= 1;
-    int *skey = (int *)spec;
-    int *sslot = skey + P;
+    int *hist = (int *)spec;          // 256 buckets
+    int *sslot = hist + 256;          // n_slots entries
+    const int kb = g.key_bits_;
+    const int shift = kb > 8 ? kb - 8 : 0;
+    for (int i = lane; i < 256; i += 32) hist[i] = 0;
+    __syncwarp();
     int my_live = 0;
-    for (int s = lane; s < P; s += 32) {
-        const bool live = s < n_slots && slot_live[s];
-        my_live += live;
-        skey[s] = live ? slot_key[s] : INT_MAX;
-        sslot[s] = s;
-    }
+    for (int s = lane; s < n_slots; s += 32)
+        if (slot_live[s]) {
+            ++my_live;
+            atomicAdd(&hist[slot_key[s] >> shift], 1);
+        }
     const int count = __shfl_sync(FULL, warp_sum(my_live), 0);
     __syncwarp();
-    for (int size = 2; size <= P; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = lane; i < P; i += 32) {
-                const int j = i ^ stride;
-                if (j > i) {
-                    const bool up = (i & size) == 0;
-                    const int ki = skey[i], kj = skey[j];
-                    if ((ki > kj) == up) {
-                        skey[i] = kj;
-                        skey[j] = ki;
-                        const int t = sslot[i];
-                        sslot[i] = sslot[j];
-                        sslot[j] = t;
-                    }
-                }
-            }
-            __syncwarp();
+    {   // exclusive scan of the 256 bucket counts: 8 consecutive per lane
+        int c[8], run = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            c[i] = hist[lane * 8 + i];
+            run += c[i];
+        }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int start = incl - run;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            hist[lane * 8 + i] = start;  // becomes the bucket's fill cursor
+            start += c[i];
         }
     }
+    __syncwarp();
+    for (int s = lane; s < n_slots; s += 32)
+        if (slot_live[s]) sslot[atomicAdd(&hist[slot_key[s] >> shift], 1)] = s;
+    __syncwarp();
+    // buckets end at hist[b] (cursor after the scatter); sort each in place
+    for (int bkt = lane; bkt < 256; bkt += 32) {
+        const int en = hist[bkt], st = bkt ? hist[bkt - 1] : 0;
+        for (int i = st + 1; i < en; ++i) {
+            const int v = sslot[i], kv = slot_key[v];
+            int j = i - 1;
+            while (j >= st && slot_key[sslot[j]] > kv) {
+                sslot[j + 1] = sslot[j];
+                --j;
+            }
+            sslot[j + 1] = v;
+        }
+    }
+    __syncwarp();
     for (int r = lane; r < count; r += 32) {
         const int s = sslot[r];
         int m[MAXD];

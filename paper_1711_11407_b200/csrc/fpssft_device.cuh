@@ -630,8 +630,10 @@ __device__ __forceinline__ void fft_lines_warp(cpx<R> *x, int nlines, const Geo 
 // Compile-time FFT for the line lengths of the benchmark configs (warp
 // teams): every index, group and twiddle stride is a constant, so the stage
 // loops fully unroll.  Stage: radix RAD after NS points have been combined.
+// The first stage (NS == 1) also returns this lane's share of sum |x|^2 over
+// the raw samples it reads (each sample is read exactly once there).
 template <class R, int L, int NL, int RAD, int NS, bool LAST>
-__device__ __forceinline__ void stage_static(cpx<R> *x, const cpx<R> *roots, int lane) {
+__device__ __forceinline__ R stage_static(cpx<R> *x, const cpx<R> *roots, int lane) {
     constexpr int M = L / RAD;                                   // butterflies per line
     constexpr int CAPB = RAD == 16 ? 1 : (RAD == 8 ? 2 : 4);     // per lane (registers)
     constexpr int G0 = CAPB * 32 / M;
@@ -640,6 +642,7 @@ __device__ __forceinline__ void stage_static(cpx<R> *x, const cpx<R> *roots, int
     static_assert(MB <= CAPB, "stage does not fit the warp's registers");
     constexpr int STEP = L / (NS * RAD);
     const R inv = (R)1 / (R)L;
+    R energy = (R)0;
 #pragma unroll
     for (int l0 = 0; l0 < NL; l0 += G) {
         const int total = (NL - l0 < G ? NL - l0 : G) * M;
@@ -654,6 +657,10 @@ __device__ __forceinline__ void stage_static(cpx<R> *x, const cpx<R> *roots, int
                 const cpx<R> *xl = x + line * L;
 #pragma unroll
                 for (int k = 0; k < RAD; ++k) v[j][k] = xl[jj + k * M];
+                if (NS == 1) {
+#pragma unroll
+                    for (int k = 0; k < RAD; ++k) energy += cabs2(v[j][k]);
+                }
                 if (NS > 1) {
                     const int jm = jj % NS;
 #pragma unroll
@@ -679,28 +686,32 @@ __device__ __forceinline__ void stage_static(cpx<R> *x, const cpx<R> *roots, int
         }
         __syncwarp();
     }
+    return energy;
 }
 
+// Returns this lane's share of sum |x|^2 of the input samples.
 template <class R, int L, int NL>
-__device__ __forceinline__ void fft_static(cpx<R> *x, const cpx<R> *roots, int lane) {
+__device__ __forceinline__ R fft_static(cpx<R> *x, const cpx<R> *roots, int lane) {
     constexpr bool F = sizeof(R) == 4;
+    R e;
     if constexpr (L == 256 && F) {
-        stage_static<R, L, NL, 16, 1, false>(x, roots, lane);
+        e = stage_static<R, L, NL, 16, 1, false>(x, roots, lane);
         stage_static<R, L, NL, 16, 16, true>(x, roots, lane);
     } else if constexpr (L == 256) {
-        stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
+        e = stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
         stage_static<R, L, NL, 8, 8, false>(x, roots, lane);
         stage_static<R, L, NL, 4, 64, true>(x, roots, lane);
     } else if constexpr (L == 512) {
-        stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
+        e = stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
         stage_static<R, L, NL, 8, 8, false>(x, roots, lane);
         stage_static<R, L, NL, 8, 64, true>(x, roots, lane);
     } else if constexpr (L == 64) {
-        stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
+        e = stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
         stage_static<R, L, NL, 8, 8, true>(x, roots, lane);
     } else {
         static_assert(L == 64 || L == 256 || L == 512, "no static plan for this L");
     }
+    return e;
 }
 
 // ------------------------------------------------------------- bin map
