@@ -438,7 +438,8 @@ struct WarpLayout {
 
 __host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, int cs) {
     WarpLayout y;
-    const size_t spec_bytes = (size_t)(D + 1) * L * cs, sort_bytes = 1024 + (size_t)k_cap * 4;
+    const size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // room for padi()
+    const size_t sort_bytes = 1024 + (size_t)k_cap * 4;
     size_t o = 0;
     y.H = 2 * k_cap;
     y.spec = o;      o = align16(o + (spec_bytes > sort_bytes ? spec_bytes : sort_bytes));
@@ -494,6 +495,7 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
                                                            const int *__restrict__ sched_index,
                                                            int n_sched, OutPtrs out) {
     extern __shared__ __align__(16) unsigned char sm[];
+    constexpr bool PAD = LC != 0;  // padded spectra layout (see padi)
     Geo g = g_in;
     if (LC) g.L = LC;
     if (DC) {
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
             __syncwarp();
             my_energy = (LC == 0 && kn.noise_coef > 0) ? line_energy(spec, nl * L, lane, 32) : (R)0;
         } else {
-            my_energy = gather_lines(spec, cube, g, al, ta, lane, 32);
+            my_energy = gather_lines<R, PAD>(spec, cube, g, al, ta, lane, 32);
             if (it + 1 < kn.t_max) {
 #pragma unroll
                 for (int k = 0; k < MAXD; ++k) {
@@ -622,7 +624,7 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
                 }
 #pragma unroll
                 for (int i = 0; i < MAXD + 1; ++i)
-                    if (i < nl) spec[i * L + b] = spec[i * L + b] - P[i];
+                    if (i < nl) spec[padi<PAD>(i * L + b)] = spec[padi<PAD>(i * L + b)] - P[i];
             }
             __syncwarp();
         }
@@ -639,7 +641,7 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
         for (int c0 = 0; c0 < L; c0 += 32) {
             const int b = c0 + lane;
             R top = (R)0;
-            const bool ok = b < L && bin_is_candidate(spec, g, b, mag_tol, floor, &top);
+            const bool ok = b < L && bin_is_candidate<R, PAD>(spec, g, b, mag_tol, floor, &top);
             if (!ok) resid = max(resid, top);
             const unsigned msk = __ballot_sync(FULL, ok);
             if (ok) cand[n_cand + __popc(msk & lt_mask)] = (unsigned short)b;
@@ -652,7 +654,8 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
             int m[MAXD];
             cpx<R> a;
             int st = 0;
-            if (b >= 0) st = decode_candidate(spec, g, b, al, ta, roots, round_tol, verify_tol, m, &a);
+            if (b >= 0)
+                st = decode_candidate<R, PAD>(spec, g, b, al, ta, roots, round_tol, verify_tol, m, &a);
             const unsigned acc = __ballot_sync(FULL, st == 2);
             int key = 0, found = -1;
             if (st == 2) {
@@ -681,9 +684,10 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
                 slot_live[s] = keep;
                 const int u0 = phase_of(m, g, ta);  // driver.py:189-194
                 for (int i = 0; i < nl; ++i)
-                    spec[i * L + b] = spec[i * L + b] - a * roots[phase_step(u0, i, m, g)];
+                    spec[padi<PAD>(i * L + b)] =
+                        spec[padi<PAD>(i * L + b)] - a * roots[phase_step(u0, i, m, g)];
             }
-            if (b >= 0) resid = max(resid, bin_residual(spec, g, b));
+            if (b >= 0) resid = max(resid, bin_residual<R, PAD>(spec, g, b));
             n_slots += __popc(fresh);
             __syncwarp();
         }
@@ -1158,6 +1162,19 @@ int check_launch(const char *where) {
     return FPSSFT_OK;
 }
 
+// The warp kernel instance for a shape: compile-time specialisations for the
+// benchmark shapes, else the runtime-shape version.
+template <class R>
+const void *warp_kernel_for_t(const Geo &g) {
+    if (g.off32 && g.D == 2 && g.L == 256) return (const void *)recover_warp_kernel<R, 256, 2>;
+    if (g.off32 && g.D == 2 && g.L == 512) return (const void *)recover_warp_kernel<R, 512, 2>;
+    if (g.off32 && g.D == 3 && g.L == 64) return (const void *)recover_warp_kernel<R, 64, 3>;
+    return (const void *)recover_warp_kernel<R, 0, 0>;
+}
+const void *warp_kernel_for(const Geo &g, int precision) {
+    return precision == FPSSFT_F64 ? warp_kernel_for_t<double>(g) : warp_kernel_for_t<float>(g);
+}
+
 constexpr long long SMEM_PER_SM = 228 * 1024;    // B200 shared memory per SM
 constexpr long long SMEM_PER_CTA = 227 * 1024;   // opt-in limit per CTA
 constexpr long long SMEM_RESERVED = 1024;        // per-CTA system reservation
@@ -1171,6 +1188,18 @@ struct LaunchPlan {
 // enough ((D+1) L <= 2048), the packed key fits 31 bits and the per-warp state
 // fits; warps per CTA chosen to maximise resident instances per SM.  Else one
 // CTA per instance.  `g` receives the FFT plan of the chosen mode.
+// Registers per thread of the warp kernel chosen for (precision, L, D): the
+// compiled value when a device is present, else the launch-bounds cap.
+const void *warp_kernel_for(const Geo &g, int precision);
+
+int warp_kernel_regs(const Geo &g, int precision) {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, warp_kernel_for(g, precision)) == cudaSuccess && fa.numRegs > 0)
+        return fa.numRegs;
+    cudaGetLastError();  // no device: clear the error, assume the cap
+    return precision == FPSSFT_F64 ? 128 : 80;
+}
+
 int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) {
     const int cs = precision == FPSSFT_F64 ? 16 : 8;
     if (want != FPSSFT_MODE_CTA) {
@@ -1179,13 +1208,15 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
                   (g.L & (g.L - 1)) == 0 && plan_fft(&gw, g.nlines, precision, 32) > 0;
         if (ok) {
             const WarpLayout wl = make_warp_layout(g.D, g.L, kn.k_cap, cs);
+            const int regs = (warp_kernel_regs(gw, precision) + 7) / 8 * 8;
+            const long long reg_warps = 65536 / (regs * 32);
             int best_w = 0;
             long long best_warps = 0;
             for (int w : {8, 4, 2, 1}) {
                 const long long smem = (long long)wl.roots + w * (long long)wl.per_warp;
                 if (smem > SMEM_PER_CTA) continue;
-                const long long ctas =
-                    std::min<long long>({32, SMEM_PER_SM / (smem + SMEM_RESERVED), 64 / w});
+                const long long ctas = std::min<long long>(
+                    {32, SMEM_PER_SM / (smem + SMEM_RESERVED), 64 / w, reg_warps / w});
                 if (ctas * w > best_warps) {
                     best_warps = ctas * w;
                     best_w = w;
@@ -1226,11 +1257,9 @@ int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
     if (rc != FPSSFT_OK) return rc;
     cudaError_t e;
     if (lp.mode == FPSSFT_MODE_WARP) {
-        // compile-time specialisations for the benchmark shapes
-        auto kernel = recover_warp_kernel<R, 0, 0>;
-        if (g.off32 && g.D == 2 && g.L == 256) kernel = recover_warp_kernel<R, 256, 2>;
-        else if (g.off32 && g.D == 2 && g.L == 512) kernel = recover_warp_kernel<R, 512, 2>;
-        else if (g.off32 && g.D == 3 && g.L == 64) kernel = recover_warp_kernel<R, 64, 3>;
+        auto kernel = (void (*)(const float2 *, long long, long long, Geo, Knobs, const int *,
+                                const int *, int, OutPtrs))warp_kernel_for(
+            g, sizeof(R) == 8 ? FPSSFT_F64 : FPSSFT_F32);
         e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lp.smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recover_warp_kernel)");

@@ -48,6 +48,12 @@ __device__ __forceinline__ float cabs(cpx<float> a) { return sqrtf(a.re * a.re +
 template <class R>
 __device__ __forceinline__ R cabs2(cpx<R> a) { return a.re * a.re + a.im * a.im; }
 
+// Padded spectra layout of the compile-time warp kernels: one spare complex
+// after every 16, so the stride-16 writes of a radix-16 Stockham stage (and
+// the stride-L line accesses) spread over the shared-memory banks.
+template <bool PAD>
+__device__ __forceinline__ int padi(int e) { return PAD ? e + (e >> 4) : e; }
+
 // Synchronisation of the threads that own one instance: the whole CTA, or
 // one warp (team of 32 lanes).
 struct BlockTeam {
@@ -174,7 +180,7 @@ __device__ __forceinline__ void build_roots(cpx<R> *roots, int L) {
 // coordinate k, advanced by one with wrap, so each thread issues its D+1
 // loads from one base address.  Index math is fastmod, no division.
 // Returns this thread's share of sum |x|^2 over the gathered samples.
-template <class R>
+template <class R, bool PAD = false>
 __device__ __forceinline__ R gather_lines(cpx<R> *spec, const float2 *__restrict__ cube,
                                           const Geo &g, const int *al, const int *ta, int tid,
                                           int nth) {
@@ -197,12 +203,12 @@ __device__ __forceinline__ R gather_lines(cpx<R> *spec, const float2 *__restrict
 #pragma unroll
         for (int k = 0; k < MAXD; ++k)
             if (k < D) v[k + 1] = __ldcs(cube + base + delta[k]);
-        spec[l] = {(R)v[0].x, (R)v[0].y};
+        spec[padi<PAD>(l)] = {(R)v[0].x, (R)v[0].y};
         energy += (R)v[0].x * (R)v[0].x + (R)v[0].y * (R)v[0].y;
 #pragma unroll
         for (int k = 0; k < MAXD; ++k)
             if (k < D) {
-                spec[(k + 1) * L + l] = {(R)v[k + 1].x, (R)v[k + 1].y};
+                spec[padi<PAD>((k + 1) * L + l)] = {(R)v[k + 1].x, (R)v[k + 1].y};
                 energy += (R)v[k + 1].x * (R)v[k + 1].x + (R)v[k + 1].y * (R)v[k + 1].y;
             }
     }
@@ -244,12 +250,12 @@ __device__ __forceinline__ void gather_lines_async(cpx<float> *spec,
 #pragma unroll
             for (int k = 0; k < MAXD; ++k)
                 if (k < D) base += n[k] * g.stride32[k];
-            cp_async8(spec + l, cube + base);
+            cp_async8(spec + padi<true>(l), cube + base);
 #pragma unroll
             for (int k = 0; k < MAXD; ++k) {
                 if (k < D) {
                     const int d = (n[k] + 1 == g.N[k]) ? -n[k] * g.stride32[k] : g.stride32[k];
-                    cp_async8(spec + (k + 1) * LC + l, cube + (base + d));
+                    cp_async8(spec + padi<true>((k + 1) * LC + l), cube + (base + d));
                     n[k] += step[k];
                     if (n[k] >= g.N[k]) n[k] -= g.N[k];
                 }
@@ -654,9 +660,8 @@ __device__ __forceinline__ R stage_static(cpx<R> *x, const cpx<R> *roots, int la
             ob[j] = -1;
             if (q < total) {
                 const int line = l0 + q / M, jj = q % M;
-                const cpx<R> *xl = x + line * L;
 #pragma unroll
-                for (int k = 0; k < RAD; ++k) v[j][k] = xl[jj + k * M];
+                for (int k = 0; k < RAD; ++k) v[j][k] = x[padi<true>(line * L + jj + k * M)];
                 if (NS == 1) {
 #pragma unroll
                     for (int k = 0; k < RAD; ++k) energy += cabs2(v[j][k]);
@@ -680,7 +685,7 @@ __device__ __forceinline__ R stage_static(cpx<R> *x, const cpx<R> *roots, int la
                 for (int k = 0; k < RAD; ++k) {
                     cpx<R> o = v[j][k];
                     if (LAST) o = {o.re * inv, o.im * inv};  // L is a power of two: exact
-                    x[ob[j] + k * NS] = o;
+                    x[padi<true>(ob[j] + k * NS)] = o;
                 }
             }
         }
@@ -750,16 +755,16 @@ __device__ __forceinline__ int phase_step(int u0, int i, const int *m, const Geo
 // compares squared magnitudes (no square roots): top - low <= t top  <=>
 // low^2 >= (1 - t)^2 top^2 for t < 1.  `res` receives the bin's largest
 // |S_i|^2 (float) / |S_i| (double) for the termination test.
-template <class R>
+template <class R, bool PAD = false>
 __device__ __forceinline__ bool bin_is_candidate(const cpx<R> *spec, const Geo &g, int b,
                                                  R mag_tol, R floor, R *res) {
     if constexpr (sizeof(R) == 4) {
-        const R q0 = cabs2(spec[b]);
+        const R q0 = cabs2(spec[padi<PAD>(b)]);
         R top = q0, low = q0;
 #pragma unroll
         for (int i = 1; i < MAXD + 1; ++i) {
             if (i <= g.D) {
-                const R qi = cabs2(spec[i * g.L + b]);
+                const R qi = cabs2(spec[padi<PAD>(i * g.L + b)]);
                 top = max(top, qi);
                 low = min(low, qi);
             }
@@ -768,12 +773,12 @@ __device__ __forceinline__ bool bin_is_candidate(const cpx<R> *spec, const Geo &
         const R c = (R)1 - mag_tol;
         return q0 > floor * floor && (mag_tol >= (R)1 || low >= c * c * top);
     } else {
-        const R m0 = cabs(spec[b]);
+        const R m0 = cabs(spec[padi<PAD>(b)]);
         R top = m0, low = m0;
 #pragma unroll
         for (int i = 1; i < MAXD + 1; ++i) {
             if (i <= g.D) {
-                const R mi = cabs(spec[i * g.L + b]);
+                const R mi = cabs(spec[padi<PAD>(i * g.L + b)]);
                 top = max(top, mi);
                 low = min(low, mi);
             }
@@ -783,12 +788,16 @@ __device__ __forceinline__ bool bin_is_candidate(const cpx<R> *spec, const Geo &
     }
 }
 // Largest |S_i[b]|^2 (float) or |S_i[b]| (double) over the D+1 lines.
-template <class R>
+template <class R, bool PAD = false>
 __device__ __forceinline__ R bin_residual(const cpx<R> *spec, const Geo &g, int b) {
     R top = (R)0;
 #pragma unroll
-    for (int i = 0; i < MAXD + 1; ++i)
-        if (i <= g.D) top = max(top, sizeof(R) == 4 ? cabs2(spec[i * g.L + b]) : cabs(spec[i * g.L + b]));
+    for (int i = 0; i < MAXD + 1; ++i) {
+        if (i <= g.D) {
+            const cpx<R> v = spec[padi<PAD>(i * g.L + b)];
+            top = max(top, sizeof(R) == 4 ? cabs2(v) : cabs(v));
+        }
+    }
     return top;
 }
 
@@ -854,7 +863,7 @@ __device__ __forceinline__ int classify_bin(const cpx<R> *spec, const Geo &g, in
 }
 
 // As classify_bin for a bin already known to pass the magnitude test.
-template <class R>
+template <class R, bool PAD = false>
 __device__ __forceinline__ int decode_candidate(const cpx<R> *spec, const Geo &g, int b,
                                             const int *al, const int *ta, const cpx<R> *roots,
                                             R round_tol, R verify_tol,
@@ -863,7 +872,7 @@ __device__ __forceinline__ int decode_candidate(const cpx<R> *spec, const Geo &g
     cpx<R> s[MAXD + 1];
 #pragma unroll
     for (int i = 0; i < MAXD + 1; ++i)
-        if (i <= D) s[i] = spec[i * L + b];
+        if (i <= D) s[i] = spec[padi<PAD>(i * L + b)];
     const R mag0 = cabs(s[0]);
     const R two_pi = (R)6.283185307179586476925286766559;
     bool ok = true;
