@@ -808,6 +808,8 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
     }
 }
 
+#include "fpssft_team.cuh"
+
 // ------------------------------------------------------- per-function kernels
 template <class R>
 __global__ void __launch_bounds__(1024, 1) line_spectra_kernel(const float2 *__restrict__ cubes,
@@ -1175,6 +1177,33 @@ const void *warp_kernel_for(const Geo &g, int precision) {
     return precision == FPSSFT_F64 ? warp_kernel_for_t<double>(g) : warp_kernel_for_t<float>(g);
 }
 
+// The compile-time team kernel for a shape (one CTA of *nt threads per
+// instance), or nullptr if the shape has none.
+template <class R>
+const void *team_kernel_for_t(const Geo &g, int *nt) {
+    if (!g.off32 || g.D != 2) return nullptr;
+    if (g.L == 2048) {
+        *nt = 1024;
+        return (const void *)recover_team_kernel<R, 2048, 2, 1024>;
+    }
+    if (g.L == 512) {
+        *nt = 128;
+        return (const void *)recover_team_kernel<R, 512, 2, 128>;
+    }
+    return nullptr;
+}
+const void *team_kernel_for(const Geo &g, int precision, int *nt) {
+    return precision == FPSSFT_F64 ? team_kernel_for_t<double>(g, nt)
+                                   : team_kernel_for_t<float>(g, nt);
+}
+
+int kernel_regs(const void *fn, int fallback) {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess && fa.numRegs > 0) return fa.numRegs;
+    cudaGetLastError();  // no device: clear the error, assume the cap
+    return fallback;
+}
+
 constexpr long long SMEM_PER_SM = 228 * 1024;    // B200 shared memory per SM
 constexpr long long SMEM_PER_CTA = 227 * 1024;   // opt-in limit per CTA
 constexpr long long SMEM_RESERVED = 1024;        // per-CTA system reservation
@@ -1182,6 +1211,7 @@ constexpr long long SMEM_RESERVED = 1024;        // per-CTA system reservation
 struct LaunchPlan {
     int mode, threads, per_cta;
     size_t smem;
+    const void *kernel;  // nullptr: generic recover_kernel / recover_warp_kernel<R,0,0>
 };
 
 // Pick the kernel for a shape: warp-per-instance when the lines are short
@@ -1202,8 +1232,11 @@ int warp_kernel_regs(const Geo &g, int precision) {
 
 int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) {
     const int cs = precision == FPSSFT_F64 ? 16 : 8;
+    // candidate 1: warp per instance
+    long long warp_warps = 0;
+    LaunchPlan wp{};
+    Geo gw = g;
     if (want != FPSSFT_MODE_CTA) {
-        Geo gw = g;
         bool ok = g.key_bits_ <= 31 && kn.k_cap <= 32768 && (long long)g.nlines * g.L <= 2048 &&
                   (g.L & (g.L - 1)) == 0 && plan_fft(&gw, g.nlines, precision, 32) > 0;
         if (ok) {
@@ -1211,28 +1244,57 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
             const int regs = (warp_kernel_regs(gw, precision) + 7) / 8 * 8;
             const long long reg_warps = 65536 / (regs * 32);
             int best_w = 0;
-            long long best_warps = 0;
             for (int w : {8, 4, 2, 1}) {
                 const long long smem = (long long)wl.roots + w * (long long)wl.per_warp;
                 if (smem > SMEM_PER_CTA) continue;
                 const long long ctas = std::min<long long>(
                     {32, SMEM_PER_SM / (smem + SMEM_RESERVED), 64 / w, reg_warps / w});
-                if (ctas * w > best_warps) {
-                    best_warps = ctas * w;
+                if (ctas * w > warp_warps) {
+                    warp_warps = ctas * w;
                     best_w = w;
                 }
             }
-            if (best_w) {
-                g = gw;
-                lp->mode = FPSSFT_MODE_WARP;
-                lp->threads = 32 * best_w;
-                lp->per_cta = best_w;
-                lp->smem = wl.roots + (size_t)best_w * wl.per_warp;
-                return FPSSFT_OK;
-            }
+            if (best_w)
+                wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * best_w, best_w,
+                                wl.roots + (size_t)best_w * wl.per_warp,
+                                warp_kernel_for(gw, precision)};
         }
-        if (want == FPSSFT_MODE_WARP)
-            return fail(FPSSFT_EUNSUPPORTED, "shape/k_cap does not fit the warp-per-instance kernel");
+        if (want == FPSSFT_MODE_WARP) {
+            if (!warp_warps)
+                return fail(FPSSFT_EUNSUPPORTED,
+                            "shape/k_cap does not fit the warp-per-instance kernel");
+            g = gw;
+            *lp = wp;
+            return FPSSFT_OK;
+        }
+    }
+    // candidate 2: compile-time team kernel (one CTA per instance)
+    int tnt = 0;
+    const void *tk = (g.key_bits_ <= 31 && kn.k_cap <= 32768) ? team_kernel_for(g, precision, &tnt)
+                                                              : nullptr;
+    long long team_warps = 0;
+    LaunchPlan tp{};
+    if (tk) {
+        const TeamLayout tl = make_team_layout(g.D, g.L, kn.k_cap, cs);
+        if ((long long)tl.total <= SMEM_PER_CTA) {
+            const int regs = (kernel_regs(tk, tnt >= 1024 ? 64 : 128) + 7) / 8 * 8;
+            const long long ctas = std::min<long long>(
+                {32, SMEM_PER_SM / ((long long)tl.total + SMEM_RESERVED), 2048 / tnt,
+                 65536 / ((long long)regs * tnt)});
+            team_warps = ctas * tnt / 32;
+            tp = LaunchPlan{FPSSFT_MODE_CTA, tnt, 1, tl.total, tk};
+        }
+    }
+    // warp mode unless it keeps too few warps resident and the team kernel
+    // does clearly better
+    if (warp_warps && !(team_warps && warp_warps < 16 && team_warps * 2 > warp_warps * 3)) {
+        g = gw;
+        *lp = wp;
+        return FPSSFT_OK;
+    }
+    if (team_warps) {
+        *lp = tp;
+        return FPSSFT_OK;
     }
     const int nt = plan_fft(&g, g.nlines, precision, 0);
     if (nt < 0) return fail(FPSSFT_EUNSUPPORTED, "line length too large for one CTA");
@@ -1241,10 +1303,7 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
         return fail(FPSSFT_EUNSUPPORTED,
                     "shared memory for this (shape, k_cap, precision) is " +
                         std::to_string(lay.total) + " B, above the per-CTA limit; lower k_cap");
-    lp->mode = FPSSFT_MODE_CTA;
-    lp->threads = nt;
-    lp->per_cta = 1;
-    lp->smem = lay.total;
+    *lp = LaunchPlan{FPSSFT_MODE_CTA, nt, 1, lay.total, nullptr};
     return FPSSFT_OK;
 }
 
@@ -1256,10 +1315,21 @@ int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
     int rc = make_plan(g, kn, sizeof(R) == 8 ? FPSSFT_F64 : FPSSFT_F32, want_mode, &lp);
     if (rc != FPSSFT_OK) return rc;
     cudaError_t e;
+    if (lp.mode == FPSSFT_MODE_CTA && lp.kernel) {  // compile-time team kernel
+        auto kernel = (void (*)(const float2 *, long long, Geo, Knobs, const int *, const int *,
+                                int, OutPtrs))lp.kernel;
+        e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lp.smem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recover_team_kernel)");
+        if (batch == 0) return FPSSFT_OK;
+        kernel<<<(unsigned)batch, lp.threads, lp.smem, st>>>(
+            (const float2 *)cubes, (long long)batch_stride, g, kn, schedule, sched_index, n_sched,
+            o);
+        return check_launch("recover_team_kernel");
+    }
     if (lp.mode == FPSSFT_MODE_WARP) {
         auto kernel = (void (*)(const float2 *, long long, long long, Geo, Knobs, const int *,
-                                const int *, int, OutPtrs))warp_kernel_for(
-            g, sizeof(R) == 8 ? FPSSFT_F64 : FPSSFT_F32);
+                                const int *, int, OutPtrs))lp.kernel;
         e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lp.smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recover_warp_kernel)");

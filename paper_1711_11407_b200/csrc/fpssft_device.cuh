@@ -227,7 +227,7 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
-template <int LC = 0>
+template <int LC = 0, int NTC = 32>
 __device__ __forceinline__ void gather_lines_async(cpx<float> *spec,
                                                    const float2 *__restrict__ cube, const Geo &g,
                                                    const int *al, const int *ta, int tid,
@@ -240,12 +240,14 @@ __device__ __forceinline__ void gather_lines_async(cpx<float> *spec,
             n[k] = k < D ? (int)fastmod((unsigned)al[k] * (unsigned)tid + (unsigned)ta[k],
                                         g.magic[k], (unsigned)g.N[k])
                          : 0;
-            step[k] = k < D ? (int)fastmod((unsigned)al[k] * 32u, g.magic[k], (unsigned)g.N[k])
+            step[k] = k < D ? (int)fastmod((unsigned)al[k] * (unsigned)NTC, g.magic[k],
+                                           (unsigned)g.N[k])
                             : 0;
         }
 #pragma unroll 4
-        for (int j = 0; j < LC / 32; ++j) {
-            const int l = tid + 32 * j;
+        for (int j = 0; j < (LC + NTC - 1) / NTC; ++j) {
+            const int l = tid + NTC * j;
+            if (LC % NTC != 0 && l >= LC) break;
             int base = 0;
 #pragma unroll
             for (int k = 0; k < MAXD; ++k)
@@ -633,19 +635,25 @@ __device__ __forceinline__ void fft_lines_warp(cpx<R> *x, int nlines, const Geo 
     if (g.nstages == 0) __syncwarp();
 }
 
-// Compile-time FFT for the line lengths of the benchmark configs (warp
-// teams): every index, group and twiddle stride is a constant, so the stage
-// loops fully unroll.  Stage: radix RAD after NS points have been combined.
-// The first stage (NS == 1) also returns this lane's share of sum |x|^2 over
-// the raw samples it reads (each sample is read exactly once there).
-template <class R, int L, int NL, int RAD, int NS, bool LAST>
-__device__ __forceinline__ R stage_static(cpx<R> *x, const cpx<R> *roots, int lane) {
+// Compile-time FFT for the line lengths of the benchmark configs: every
+// index, group and twiddle stride is a constant, so the stage loops fully
+// unroll.  Team = one warp (NT = 32) or one CTA (NT = blockDim.x).  Stage:
+// radix RAD after NS points have been combined; the spectra use the padded
+// layout (padi).  The first stage (NS == 1) also returns this thread's share
+// of sum |x|^2 over the raw samples it reads (each is read exactly once).
+template <class R, int RAD>
+struct StageCap {  // butterflies per thread that fit the register budget
+    static constexpr int value = RAD == 16 ? 1 : (RAD == 8 ? 2 : 4);
+};
+
+template <class R, int L, int NL, int RAD, int NS, bool LAST, int NT, class Team>
+__device__ __forceinline__ R stage_static(cpx<R> *x, const cpx<R> *roots, int tid) {
     constexpr int M = L / RAD;                                   // butterflies per line
-    constexpr int CAPB = RAD == 16 ? 1 : (RAD == 8 ? 2 : 4);     // per lane (registers)
-    constexpr int G0 = CAPB * 32 / M;
+    constexpr int CAPB = StageCap<R, RAD>::value;
+    constexpr int G0 = CAPB * NT / M;
     constexpr int G = G0 < 1 ? 1 : (G0 > NL ? NL : G0);          // lines per group
-    constexpr int MB = (G * M + 31) / 32;
-    static_assert(MB <= CAPB, "stage does not fit the warp's registers");
+    constexpr int MB = (G * M + NT - 1) / NT;
+    static_assert(MB <= CAPB, "stage does not fit the team's registers");
     constexpr int STEP = L / (NS * RAD);
     const R inv = (R)1 / (R)L;
     R energy = (R)0;
@@ -656,7 +664,7 @@ __device__ __forceinline__ R stage_static(cpx<R> *x, const cpx<R> *roots, int la
         int ob[MB];
 #pragma unroll
         for (int j = 0; j < MB; ++j) {
-            const int q = lane + 32 * j;
+            const int q = tid + NT * j;
             ob[j] = -1;
             if (q < total) {
                 const int line = l0 + q / M, jj = q % M;
@@ -677,7 +685,7 @@ __device__ __forceinline__ R stage_static(cpx<R> *x, const cpx<R> *roots, int la
                 Bfly<R, RAD>::run(v[j], roots, L);
             }
         }
-        __syncwarp();
+        Team::sync();
 #pragma unroll
         for (int j = 0; j < MB; ++j) {
             if (ob[j] >= 0) {
@@ -689,32 +697,46 @@ __device__ __forceinline__ R stage_static(cpx<R> *x, const cpx<R> *roots, int la
                 }
             }
         }
-        __syncwarp();
+        Team::sync();
     }
     return energy;
 }
 
-// Returns this lane's share of sum |x|^2 of the input samples.
-template <class R, int L, int NL>
-__device__ __forceinline__ R fft_static(cpx<R> *x, const cpx<R> *roots, int lane) {
+template <int L>
+struct HasStaticPlan {
+    static constexpr bool value = L == 64 || L == 256 || L == 512 || L == 2048;
+};
+
+// Returns this thread's share of sum |x|^2 of the input samples.
+template <class R, int L, int NL, int NT = 32, class Team = WarpTeam>
+__device__ __forceinline__ R fft_static(cpx<R> *x, const cpx<R> *roots, int tid) {
     constexpr bool F = sizeof(R) == 4;
     R e;
     if constexpr (L == 256 && F) {
-        e = stage_static<R, L, NL, 16, 1, false>(x, roots, lane);
-        stage_static<R, L, NL, 16, 16, true>(x, roots, lane);
+        e = stage_static<R, L, NL, 16, 1, false, NT, Team>(x, roots, tid);
+        stage_static<R, L, NL, 16, 16, true, NT, Team>(x, roots, tid);
     } else if constexpr (L == 256) {
-        e = stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
-        stage_static<R, L, NL, 8, 8, false>(x, roots, lane);
-        stage_static<R, L, NL, 4, 64, true>(x, roots, lane);
+        e = stage_static<R, L, NL, 8, 1, false, NT, Team>(x, roots, tid);
+        stage_static<R, L, NL, 8, 8, false, NT, Team>(x, roots, tid);
+        stage_static<R, L, NL, 4, 64, true, NT, Team>(x, roots, tid);
     } else if constexpr (L == 512) {
-        e = stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
-        stage_static<R, L, NL, 8, 8, false>(x, roots, lane);
-        stage_static<R, L, NL, 8, 64, true>(x, roots, lane);
+        e = stage_static<R, L, NL, 8, 1, false, NT, Team>(x, roots, tid);
+        stage_static<R, L, NL, 8, 8, false, NT, Team>(x, roots, tid);
+        stage_static<R, L, NL, 8, 64, true, NT, Team>(x, roots, tid);
     } else if constexpr (L == 64) {
-        e = stage_static<R, L, NL, 8, 1, false>(x, roots, lane);
-        stage_static<R, L, NL, 8, 8, true>(x, roots, lane);
+        e = stage_static<R, L, NL, 8, 1, false, NT, Team>(x, roots, tid);
+        stage_static<R, L, NL, 8, 8, true, NT, Team>(x, roots, tid);
+    } else if constexpr (L == 2048 && F) {
+        e = stage_static<R, L, NL, 16, 1, false, NT, Team>(x, roots, tid);
+        stage_static<R, L, NL, 16, 16, false, NT, Team>(x, roots, tid);
+        stage_static<R, L, NL, 8, 256, true, NT, Team>(x, roots, tid);
+    } else if constexpr (L == 2048) {
+        e = stage_static<R, L, NL, 8, 1, false, NT, Team>(x, roots, tid);
+        stage_static<R, L, NL, 8, 8, false, NT, Team>(x, roots, tid);
+        stage_static<R, L, NL, 8, 64, false, NT, Team>(x, roots, tid);
+        stage_static<R, L, NL, 4, 512, true, NT, Team>(x, roots, tid);
     } else {
-        static_assert(L == 64 || L == 256 || L == 512, "no static plan for this L");
+        static_assert(HasStaticPlan<L>::value, "no static plan for this L");
     }
     return e;
 }

@@ -1,0 +1,408 @@
+// CTA-per-instance kernel with a compile-time shape (team of NT threads).
+//
+// The same loop as recover_warp_kernel for lines too long for one warp
+// (config 4: L = 2048) or instances whose on-chip state is too large to keep
+// many warps resident (config 5: L = 512, k_cap = 1024): NT threads own one
+// instance and synchronise with block barriers.  Per iteration:
+//   cp.async gather -> compile-time FFT (padded layout) -> projection of the
+//   recovered set (counting sort by bin, 16-bit scratch) -> magnitude test on
+//   every bin with block-scan compaction of candidates -> dense decode of the
+//   candidates -> merge in candidate (= ascending bin) order -> residual and
+//   amp_sum reductions -> termination.
+// Included by fpssft.cu after the warp kernel (shares its helpers).
+#pragma once
+// (included inside namespace fpssft)
+
+struct TeamLayout {
+    size_t spec, roots, slot_amp, slot_key, hash, slot_live;
+    size_t bin_start, bin_fill, seg, slot_bin, slot_u0;  // projection scratch (union A)
+    size_t cand, cand_key, cand_amp, cand_st;            // classifier scratch (union B)
+    size_t red, total;
+    int H;
+};
+
+__host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, int cs) {
+    TeamLayout y;
+    const size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // padi() layout
+    const size_t sort_bytes = 1024 + (size_t)k_cap * 4;
+    size_t o = 0;
+    y.H = 2 * k_cap;
+    y.spec = o;      o = align16(o + (spec_bytes > sort_bytes ? spec_bytes : sort_bytes));
+    y.roots = o;     o = align16(o + (size_t)L * cs);
+    y.slot_amp = o;  o = align16(o + (size_t)k_cap * cs);
+    y.slot_key = o;  o = align16(o + (size_t)k_cap * 4);
+    y.hash = o;      o = align16(o + (size_t)y.H * 2);
+    y.slot_live = o; o = align16(o + (size_t)k_cap);
+    const size_t u = o;
+    y.bin_start = u; size_t a = align16(u + (size_t)(L + 1) * 2);
+    y.bin_fill = a;  a = align16(a + (size_t)L * 4);
+    y.seg = a;       a = align16(a + (size_t)k_cap * 2);
+    y.slot_bin = a;  a = align16(a + (size_t)k_cap * 2);
+    y.slot_u0 = a;   a = align16(a + (size_t)k_cap * 2);
+    y.cand = u;      size_t b = align16(u + (size_t)L * 2);
+    y.cand_key = b;  b = align16(b + (size_t)L * 4);
+    y.cand_amp = b;  b = align16(b + (size_t)L * cs);
+    y.cand_st = b;   b = align16(b + (size_t)L);
+    o = a > b ? a : b;
+    y.red = o;       o = align16(o + 64 * 8);
+    y.total = o;
+    return y;
+}
+
+constexpr unsigned short U16_NONE = 0xFFFF;
+
+template <class R, int LC, int DC, int NT>
+__global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_team_kernel(const float2 *__restrict__ cubes,
+                                                             long long batch_stride, Geo g_in,
+                                                             Knobs kn,
+                                                             const int *__restrict__ schedule,
+                                                             const int *__restrict__ sched_index,
+                                                             int n_sched, OutPtrs out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    constexpr bool PAD = true;
+    Geo g = g_in;
+    g.L = LC;
+    g.D = DC;
+    g.nlines = DC + 1;
+    constexpr int L = LC, D = DC, nl = DC + 1;
+    const TeamLayout lay = make_team_layout(D, L, kn.k_cap, (int)sizeof(cpx<R>));
+    cpx<R> *spec = (cpx<R> *)(sm + lay.spec);
+    cpx<R> *roots = (cpx<R> *)(sm + lay.roots);
+    cpx<R> *slot_amp = (cpx<R> *)(sm + lay.slot_amp);
+    int *slot_key = (int *)(sm + lay.slot_key);
+    unsigned short *hash = (unsigned short *)(sm + lay.hash);
+    unsigned char *slot_live = sm + lay.slot_live;
+    unsigned short *bin_start = (unsigned short *)(sm + lay.bin_start);
+    unsigned short *bin_fill = (unsigned short *)(sm + lay.bin_fill);
+    unsigned short *seg = (unsigned short *)(sm + lay.seg);
+    unsigned short *slot_bin = (unsigned short *)(sm + lay.slot_bin);
+    unsigned short *slot_u0 = (unsigned short *)(sm + lay.slot_u0);
+    unsigned short *cand = (unsigned short *)(sm + lay.cand);
+    int *cand_key = (int *)(sm + lay.cand_key);
+    cpx<R> *cand_amp = (cpx<R> *)(sm + lay.cand_amp);
+    unsigned char *cand_st = sm + lay.cand_st;
+    int *ired = (int *)(sm + lay.red);
+    R *rred = (R *)(sm + lay.red + 256);
+
+    const int tid = threadIdx.x, H = lay.H;
+    const long long inst = blockIdx.x;
+    const float2 *cube = cubes + inst * batch_stride;
+    int sidx = sched_index ? sched_index[inst] : 0;
+    const bool sched_ok = sidx >= 0 && sidx < n_sched;
+    if (!sched_ok) sidx = 0;
+    const int *sched = schedule + (long long)sidx * kn.t_max * 2 * D;
+    const R mag_tol = (R)kn.mag_tol, round_tol = (R)kn.round_tol, verify_tol = (R)kn.verify_tol;
+    const R prune = (R)kn.amp_prune_tol;
+
+    build_roots(roots, L);
+    for (int h = tid; h < H; h += NT) hash[h] = U16_NONE;
+    __syncthreads();
+
+    int n_slots = 0, stall = 0, it_run = 0;
+    int term = sched_ok ? FPSSFT_TERM_MAX_ITERATIONS : -1;
+    R amp_sum = (R)0;
+    int nal[MAXD], nta[MAXD];
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+        nal[k] = k < D ? sched[k] : 0;
+        nta[k] = k < D ? sched[D + k] : 0;
+    }
+
+    for (int it = 0; it < kn.t_max && term != -1; ++it) {
+        int al[MAXD], ta[MAXD];
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) {
+            al[k] = nal[k];
+            ta[k] = nta[k];
+        }
+        if (!line_params_ok(g, al, ta)) {
+            term = -1;
+            break;
+        }
+        it_run = it + 1;
+
+        // (1) gather + (2) DFT                                 driver.py:146-154
+        if constexpr (sizeof(R) == 4) {
+            gather_lines_async<LC, NT>(spec, cube, g, al, ta, tid, NT);
+        } else {
+            gather_lines<R, PAD>(spec, cube, g, al, ta, tid, NT);
+        }
+        if (it + 1 < kn.t_max) {
+#pragma unroll
+            for (int k = 0; k < MAXD; ++k) {
+                nal[k] = k < D ? sched[(long long)(it + 1) * 2 * D + k] : 0;
+                nta[k] = k < D ? sched[(long long)(it + 1) * 2 * D + D + k] : 0;
+            }
+        }
+        if constexpr (sizeof(R) == 4) cp_async_wait_all();
+        __syncthreads();
+        const R my_energy = fft_static<R, LC, nl, NT, BlockTeam>(spec, roots, tid);
+        R noise_floor = (R)0;
+        if (sizeof(R) == 4 && kn.noise_coef > 0)
+            noise_floor = (R)kn.noise_coef * sqrt(block_sum(my_energy, rred));
+
+        // (3) construction-subtraction: counting sort of the live slots by
+        //     bin, per-bin sums in slot order (deterministic, no float atomics)
+        if (n_slots > 0) {
+            int *fill = (int *)bin_fill;
+            for (int b = tid; b < L; b += NT) fill[b] = 0;
+            __syncthreads();
+            for (int s = tid; s < n_slots; s += NT) {
+                unsigned short bb = U16_NONE;
+                if (slot_live[s]) {
+                    int m[MAXD];
+                    unpack_key(slot_key[s], g, m);
+                    const int b = bin_of(m, g, al);
+                    bb = (unsigned short)b;
+                    slot_u0[s] = (unsigned short)phase_of(m, g, ta);
+                    atomicAdd(&fill[b], 1);
+                }
+                slot_bin[s] = bb;
+            }
+            __syncthreads();
+            int carry = 0;
+#pragma unroll 1
+            for (int j0 = 0; j0 < L; j0 += NT) {
+                const int b = j0 + tid;
+                const int c = b < L ? fill[b] : 0;
+                int tot;
+                const int pre = block_exscan(c, ired, &tot);
+                if (b < L) {
+                    bin_start[b] = (unsigned short)(carry + pre);
+                    fill[b] = 0;
+                }
+                carry += tot;
+            }
+            if (tid == 0) bin_start[L] = (unsigned short)carry;
+            __syncthreads();
+            for (int s = tid; s < n_slots; s += NT) {
+                const unsigned short bb = slot_bin[s];
+                if (bb != U16_NONE) seg[bin_start[bb] + atomicAdd(&fill[bb], 1)] = (unsigned short)s;
+            }
+            __syncthreads();
+            for (int b = tid; b < L; b += NT) {
+                const int st = bin_start[b], en = bin_start[b + 1];
+                if (en == st) continue;
+                for (int i = st + 1; i < en; ++i) {  // short segments: insertion sort
+                    const unsigned short v = seg[i];
+                    int j = i - 1;
+                    while (j >= st && seg[j] > v) {
+                        seg[j + 1] = seg[j];
+                        --j;
+                    }
+                    seg[j + 1] = v;
+                }
+                cpx<R> P[MAXD + 1];
+#pragma unroll
+                for (int i = 0; i < MAXD + 1; ++i) P[i] = {(R)0, (R)0};
+                for (int p = st; p < en; ++p) {
+                    const int s = seg[p];
+                    int m[MAXD];
+                    unpack_key(slot_key[s], g, m);
+                    const cpx<R> as = slot_amp[s];
+                    const int u0 = slot_u0[s];
+#pragma unroll
+                    for (int i = 0; i < MAXD + 1; ++i)
+                        if (i < nl) P[i] = P[i] + as * roots[phase_step(u0, i, m, g)];
+                }
+#pragma unroll
+                for (int i = 0; i < MAXD + 1; ++i)
+                    if (i < nl) spec[padi<PAD>(i * L + b)] = spec[padi<PAD>(i * L + b)] - P[i];
+            }
+            __syncthreads();
+        }
+
+        // (4) magnitude test on every bin, candidates compacted in ascending
+        //     order; the residual of non-candidate bins is folded in
+        const R floor =
+            max(max((R)kn.energy_floor_abs, (R)kn.energy_floor * amp_sum), noise_floor);
+        R resid = (R)0;
+        int n_cand = 0;
+#pragma unroll 1
+        for (int j0 = 0; j0 < L; j0 += NT) {
+            const int b = j0 + tid;
+            R top = (R)0;
+            const bool ok = b < L && bin_is_candidate<R, PAD>(spec, g, b, mag_tol, floor, &top);
+            if (!ok) resid = max(resid, top);
+            int tot;
+            const int pre = block_exscan(ok ? 1 : 0, ired, &tot);
+            if (ok) cand[n_cand + pre] = (unsigned short)b;
+            n_cand += tot;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < n_cand; idx += NT) {
+            int m[MAXD];
+            cpx<R> a;
+            const int st = decode_candidate<R, PAD>(spec, g, cand[idx], al, ta, roots, round_tol,
+                                                    verify_tol, m, &a);
+            cand_st[idx] = (unsigned char)st;
+            if (st == 2) {
+                cand_key[idx] = pack_key(m, g);
+                cand_amp[idx] = a;
+            }
+        }
+        __syncthreads();
+
+        // (5) merge-by-sum in ascending bin order (driver.py:103-108)
+        int n_acc = 0;
+        bool overflow = false;
+#pragma unroll 1
+        for (int c0 = 0; c0 < n_cand; c0 += NT) {
+            const int idx = c0 + tid;
+            const int st = idx < n_cand ? cand_st[idx] : 0;
+            int found = -1, key = 0;
+            if (st == 2) {
+                key = cand_key[idx];
+                found = hash16_find(hash, slot_key, H, key);
+            }
+            const int fresh = st == 2 && found < 0;
+            int tot;  // low 16 bits: new slots, high: accepted
+            const int pre = block_exscan(fresh | ((st == 2) << 16), ired, &tot);
+            const int tot_new = tot & 0xFFFF;
+            if (n_slots + tot_new > kn.k_cap) {
+                overflow = true;
+                break;
+            }
+            if (st == 2) {
+                const cpx<R> a = cand_amp[idx];
+                cpx<R> v = a;
+                int s;
+                if (fresh) {
+                    s = n_slots + (pre & 0xFFFF);
+                    slot_key[s] = key;
+                    hash16_insert(hash, H, key, s);
+                } else {
+                    s = found;
+                    v = slot_amp[s] + a;  // a pruned slot holds 0: entries.get(f, 0) + a
+                }
+                const bool keep = !(cabs(v) <= prune);
+                slot_amp[s] = keep ? v : cpx<R>{(R)0, (R)0};
+                slot_live[s] = keep;
+                int m[MAXD];
+                unpack_key(key, g, m);
+                const int b = cand[idx];
+                const int u0 = phase_of(m, g, ta);  // driver.py:189-194
+#pragma unroll
+                for (int i = 0; i < MAXD + 1; ++i)
+                    if (i < nl)
+                        spec[padi<PAD>(i * L + b)] =
+                            spec[padi<PAD>(i * L + b)] - a * roots[phase_step(u0, i, m, g)];
+            }
+            n_slots += tot_new;
+            n_acc += tot >> 16;
+            __syncthreads();  // inserts visible to the next round's lookups
+        }
+        if (overflow) {
+            term = FPSSFT_TERM_K_CAP_OVERFLOW;
+            if (tid == 0 && out.iter_stats) {
+                int *st = out.iter_stats + (inst * kn.t_max + it) * 3;
+                st[0] = n_cand;
+                st[1] = 0;
+                st[2] = n_cand;
+            }
+            break;
+        }
+        for (int idx = tid; idx < n_cand; idx += NT)
+            resid = max(resid, bin_residual<R, PAD>(spec, g, cand[idx]));
+
+        // (6) amp_sum and (7) termination                   driver.py:108,196-204
+        R my = (R)0;
+        for (int s = tid; s < n_slots; s += NT)
+            if (slot_live[s]) my += cabs(slot_amp[s]);
+        amp_sum = block_sum(my, rred);
+        const R worst = block_max(resid, rred);  // |S|^2 (float) or |S| (double)
+        stall = n_acc > 0 ? 0 : stall + 1;
+        const R clean = max((R)kn.energy_floor_abs, (R)kn.residual_stop * amp_sum);
+        const bool is_clean = sizeof(R) == 8 ? worst <= clean : worst <= clean * clean;
+        if (tid == 0 && out.iter_stats) {
+            int *st = out.iter_stats + (inst * kn.t_max + it) * 3;
+            st[0] = n_cand;
+            st[1] = n_acc;
+            st[2] = n_cand - n_acc;
+        }
+        __syncthreads();
+        if (is_clean) {
+            term = FPSSFT_TERM_RESIDUAL_CLEAN;
+            break;
+        }
+        if (stall >= kn.stall_limit) {
+            term = FPSSFT_TERM_STALL;
+            break;
+        }
+    }
+
+    // ---- RecoveryReport: counting sort of the live keys (top 8 bits), then
+    //      insertion sort inside the buckets
+    __syncthreads();
+    int *hist = (int *)spec;
+    int *sslot = hist + 256;
+    const int kb = g.key_bits_;
+    const int shift = kb > 8 ? kb - 8 : 0;
+    for (int i = tid; i < 256; i += NT) hist[i] = 0;
+    __syncthreads();
+    int my_live = 0;
+    for (int s = tid; s < n_slots; s += NT)
+        if (slot_live[s]) {
+            ++my_live;
+            atomicAdd(&hist[slot_key[s] >> shift], 1);
+        }
+    const int count = block_sum(my_live, ired);
+    if (tid < 32) {  // exclusive scan of the 256 buckets by warp 0
+        const int lane = tid;
+        int c[8], run = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            c[i] = hist[lane * 8 + i];
+            run += c[i];
+        }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int start = incl - run;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            hist[lane * 8 + i] = start;
+            start += c[i];
+        }
+    }
+    __syncthreads();
+    for (int s = tid; s < n_slots; s += NT)
+        if (slot_live[s]) sslot[atomicAdd(&hist[slot_key[s] >> shift], 1)] = s;
+    __syncthreads();
+    for (int bkt = tid; bkt < 256; bkt += NT) {
+        const int en = hist[bkt], st = bkt ? hist[bkt - 1] : 0;
+        for (int i = st + 1; i < en; ++i) {
+            const int v = sslot[i], kv = slot_key[v];
+            int j = i - 1;
+            while (j >= st && slot_key[sslot[j]] > kv) {
+                sslot[j + 1] = sslot[j];
+                --j;
+            }
+            sslot[j + 1] = v;
+        }
+    }
+    __syncthreads();
+    for (int r = tid; r < count; r += NT) {
+        const int s = sslot[r];
+        int m[MAXD];
+        unpack_key(slot_key[s], g, m);
+        int *fo = out.freqs + (inst * kn.k_cap + r) * D;
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k)
+            if (k < D) fo[k] = m[k];
+        double *ao = out.amps + (inst * kn.k_cap + r) * 2;
+        ao[0] = (double)slot_amp[s].re;
+        ao[1] = (double)slot_amp[s].im;
+    }
+    if (tid == 0) {
+        out.count[inst] = count;
+        out.iterations[inst] = it_run;
+        out.samples_used[inst] = (long long)it_run * nl * L;
+        out.terminated_by[inst] = term;
+    }
+}
+

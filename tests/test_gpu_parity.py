@@ -177,8 +177,8 @@ def _batch(w: W.Workload, count: int):
 
 @pytest.mark.parametrize("cfg_id,count,prec,mode", [
     (2, 48, "fp32", "warp"), (2, 16, "fp32", "cta"), (2, 16, "fp64", "warp"), (1, 1, "fp32", "auto"),
-    (4, 2, "fp32", "auto"), (3, 8, "fp32", "warp"), (3, 4, "fp32", "cta"), (5, 6, "fp32", "warp"),
-    (5, 2, "fp32", "cta"), (3, 2, "fp64", "auto"), (5, 2, "fp64", "auto")])
+    (4, 2, "fp32", "auto"), (3, 8, "fp32", "warp"), (3, 8, "fp32", "cta"), (5, 6, "fp32", "warp"),
+    (5, 8, "fp32", "cta"), (3, 2, "fp64", "auto"), (5, 2, "fp64", "auto")])
 def test_config_batches_match_oracle(cfg_id, count, prec, mode):
     w = W.CONFIGS[cfg_id]
     inst, cubes = _batch(w, count)
