@@ -140,6 +140,19 @@ int fpssft_project_onto_bins(const int32_t *freqs, const double *amps, const int
                              const int32_t *alpha_tau, int32_t per_instance, double *out,
                              int32_t precision, void *stream);
 
+/*
+ * Dense re-synthesis of recovered spectra on the full grid (config 5's
+ * "inverse-synthesise each image"): for every instance b
+ *   cube_b[n] = sum_{i < counts[b]} amps[b,i] * exp(+2 pi j sum_k n_k freqs[b,i,k] / N_k)
+ * -- the dense equivalent of SyntheticSource.sample_many (core.py:176-217),
+ * exact integer-phase roots.  freqs [B, k_cap, D] int32, amps [B, k_cap, 2]
+ * double (the fpssft_run_batch outputs), cubes: complex64 row-major,
+ * cube_b = cubes + b*batch_stride (elements).
+ */
+int fpssft_synthesize(const int32_t *freqs, const double *amps, const int32_t *counts,
+                      int64_t batch, int32_t k_cap, const fpssft_shape *shape, void *cubes,
+                      int64_t batch_stride, int32_t precision, void *stream);
+
 /* Dynamic shared memory one fpssft_run_batch CTA needs (0 if unsupported). */
 size_t fpssft_smem_bytes(const fpssft_shape *shape, const fpssft_params *params);
 

@@ -10,7 +10,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfpssft.so")
+LIB_PATH = os.environ.get("FPSSFT_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libfpssft.so")  # FPSSFT_LIB: A/B builds
 MAX_DIMS = 4
 
 F32, F64 = 0, 1
@@ -19,7 +20,7 @@ MODES = {"auto": MODE_AUTO, "cta": MODE_CTA, "warp": MODE_WARP}
 TERM_NAMES = {0: "residual_clean", 1: "stall", 2: "max_iterations", 3: "k_cap_overflow",
               -1: "invalid_schedule"}
 
-EXPORTS = ("fpssft_run_batch", "fpssft_line_spectra", "fpssft_dft_forward",
+EXPORTS = ("fpssft_run_batch", "fpssft_line_spectra", "fpssft_dft_forward", "fpssft_synthesize",
            "fpssft_decode_spectra", "fpssft_project_onto_bins", "fpssft_smem_bytes",
            "fpssft_block_threads", "fpssft_plan", "fpssft_launches_per_batch",
            "fpssft_set_l2_fetch_granularity", "fpssft_get_l2_fetch_granularity", "fpssft_last_error",
@@ -72,6 +73,7 @@ def lib() -> C.CDLL:
                                             C.c_double, P, P, P, P, P]
         h.fpssft_project_onto_bins.argtypes = [P, P, P, I64, I32, C.POINTER(Shape), P, I32, P,
                                                I32, P]
+        h.fpssft_synthesize.argtypes = [P, P, P, I64, I32, C.POINTER(Shape), P, I64, I32, P]
         h.fpssft_smem_bytes.argtypes = [C.POINTER(Shape), C.POINTER(Params)]
         h.fpssft_smem_bytes.restype = C.c_size_t
         h.fpssft_block_threads.argtypes = [C.POINTER(Shape), I32]

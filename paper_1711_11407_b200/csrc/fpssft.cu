@@ -21,6 +21,10 @@
 #include "../../include/fpssft.h"
 #include "fpssft_device.cuh"
 
+#ifndef FPSSFT_WARP_MINB
+#define FPSSFT_WARP_MINB 2  // CTAs of 256 threads per SM the warp kernel's registers allow
+#endif
+
 namespace fpssft {
 
 // ------------------------------------------------------------ smem layout
@@ -488,7 +492,7 @@ __device__ __forceinline__ void hash16_insert(unsigned short *hash, int H, int k
 // LC / DC: compile-time line length and dimensionality (0 = runtime), so the
 // benchmark shapes get fully unrolled gathers, FFTs and bin loops.
 template <class R, int LC, int DC>
-__global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__restrict__ cubes,
+__global__ void __launch_bounds__(256, FPSSFT_WARP_MINB) recover_warp_kernel(const float2 *__restrict__ cubes,
                                                            long long batch, long long batch_stride,
                                                            Geo g_in, Knobs kn,
                                                            const int *__restrict__ schedule,
@@ -810,6 +814,125 @@ __global__ void __launch_bounds__(256, 2) recover_warp_kernel(const float2 *__re
 
 #include "fpssft_team.cuh"
 
+// ------------------------------------------------------------ re-synthesis
+// x(n) = sum_i a_i exp(+2 pi j sum_k n_k m_ik / N_k) on the full grid of
+// every instance (config 5's "inverse-synthesise each image"; the dense
+// equivalent of SyntheticSource.sample_many, core.py:176-217, with the same
+// exact integer-phase root table).  One CTA per instance; the grid is
+// produced RC rows (last dimension = row) at a time:
+//   V[r][m_last] = sum over entries with that m_last (in entry order) of
+//                  a * root_L[sum_{k<D-1} c_k n_k m_k mod L]   (sparse part)
+//   row = inverse FFT of V[r] along the last dimension        (dense part)
+// and each finished row is written once, coalesced: the kernel is bound by
+// the HBM write of the grid.
+template <class R>
+__global__ void __launch_bounds__(256) synth_kernel(const int *__restrict__ freqs,
+                                                    const double *__restrict__ amps,
+                                                    const int *__restrict__ counts, int k_cap,
+                                                    Geo gc, Geo gr, int rc, float2 *out,
+                                                    long long out_stride) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int D = gc.D, L = gc.L, NL = gr.L;  // NL = N_{D-1} (row length)
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const long long inst = blockIdx.x;
+    const int n = min(counts[inst], k_cap);
+    long long rows = 1;  // product of all but the last extent
+    for (int k = 0; k < D - 1; ++k) rows *= gc.N[k];
+    size_t o = 0;
+    cpx<R> *V = (cpx<R> *)(sm + o);          o = align16(o + (size_t)rc * NL * sizeof(cpx<R>));
+    cpx<R> *rootsL = (cpx<R> *)(sm + o);     o = align16(o + (size_t)L * sizeof(cpx<R>));
+    cpx<R> *rootsN = (cpx<R> *)(sm + o);     o = align16(o + (size_t)NL * sizeof(cpx<R>));
+    cpx<R> *eamp = (cpx<R> *)(sm + o);       o = align16(o + (size_t)k_cap * sizeof(cpx<R>));
+    int *ekey = (int *)(sm + o);             o = align16(o + (size_t)k_cap * 4 * MAXD);
+    int *col_start = (int *)(sm + o);        o = align16(o + (size_t)(NL + 1) * 4);
+    int *col_fill = (int *)(sm + o);         o = align16(o + (size_t)NL * 4);
+    int *order = (int *)(sm + o);            o = align16(o + (size_t)k_cap * 4);
+    int *ired = (int *)(sm + o);
+
+    build_roots(rootsL, L);
+    build_roots(rootsN, NL);
+    for (int c = tid; c < NL; c += NT) col_fill[c] = 0;
+    __syncthreads();
+    for (int e = tid; e < n; e += NT) {
+        const long long src = inst * k_cap + e;
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) ekey[e * MAXD + k] = k < D ? freqs[src * D + k] : 0;
+        eamp[e] = {(R)amps[src * 2], (R)amps[src * 2 + 1]};
+        atomicAdd(&col_fill[freqs[src * D + D - 1]], 1);
+    }
+    __syncthreads();
+    int carry = 0;
+    for (int c0 = 0; c0 < NL; c0 += NT) {  // columns -> entry ranges
+        const int c = c0 + tid;
+        int tot;
+        const int pre = block_exscan(c < NL ? col_fill[c] : 0, ired, &tot);
+        if (c < NL) {
+            col_start[c] = carry + pre;
+            col_fill[c] = 0;
+        }
+        carry += tot;
+    }
+    if (tid == 0) col_start[NL] = carry;
+    __syncthreads();
+    for (int e = tid; e < n; e += NT) {
+        const int c = ekey[e * MAXD + D - 1];
+        order[col_start[c] + atomicAdd(&col_fill[c], 1)] = e;
+    }
+    __syncthreads();
+    for (int c = tid; c < NL; c += NT) {  // entry order inside a column: deterministic sums
+        const int st = col_start[c], en = col_start[c + 1];
+        for (int i = st + 1; i < en; ++i) {
+            const int v = order[i];
+            int j = i - 1;
+            while (j >= st && order[j] > v) {
+                order[j + 1] = order[j];
+                --j;
+            }
+            order[j + 1] = v;
+        }
+    }
+    __syncthreads();
+
+    float2 *img = out + inst * out_stride;
+    const R scale = (R)NL;
+    for (long long r0 = 0; r0 < rows; r0 += rc) {
+        const int nr = (int)min((long long)rc, rows - r0);
+        // sparse part: conj(V) so that the forward FFT below yields the
+        // inverse transform: IFFT(v) = conj(FFT(conj(v))) * NL
+        for (int r = 0; r < nr; ++r) {
+            // w_k = c_k n_k mod L for this row (uniform across the block)
+            long long row = r0 + r;
+            int w[MAXD] = {0, 0, 0, 0};
+            for (int k = D - 2; k >= 0; --k) {
+                const int nk = (int)(row % gc.N[k]);
+                row /= gc.N[k];
+                w[k] = (int)((long long)gc.cof[k] * nk % L);
+            }
+            for (int c = tid; c < NL; c += NT) {
+                cpx<R> acc = {(R)0, (R)0};
+                for (int p = col_start[c]; p < col_start[c + 1]; ++p) {
+                    const int e = order[p];
+                    int u = 0;  // each term < L * N_k; the host guards D L max N < 2^31
+#pragma unroll
+                    for (int k = 0; k < MAXD - 1; ++k)
+                        if (k < D - 1) u += w[k] * ekey[e * MAXD + k];
+                    acc = acc + eamp[e] * rootsL[u % L];
+                }
+                V[r * NL + c] = {acc.re, -acc.im};
+            }
+        }
+        __syncthreads();
+        fft_lines<R, BlockTeam>(V, nr, gr, rootsN, tid, NT);
+        for (int q = tid; q < nr * NL; q += NT) {
+            const cpx<R> x = V[q];
+            img[(r0 + q / NL) * NL + q % NL] = make_float2((float)(x.re * scale),
+                                                          (float)(-x.im * scale));
+        }
+        __syncthreads();
+    }
+}
+
+
 // ------------------------------------------------------- per-function kernels
 template <class R>
 __global__ void __launch_bounds__(1024, 1) line_spectra_kernel(const float2 *__restrict__ cubes,
@@ -1093,6 +1216,7 @@ int plan_fft(Geo *g, int nlines, int precision, int team) {
         const long long m = rad[i] ? L / rad[i] : L;  // butterflies per line
         long long G = team ? std::max(1LL, std::min<long long>(nlines, cap(rad[i]) * nt / m))
                            : nlines;
+        G = std::min<long long>(G, 255);  // 8-bit field
         long long mb = (G * m + nt - 1) / nt;
         if (mb > cap(rad[i])) return -1;
         mb = mb <= 1 ? 1 : (mb <= 2 ? 2 : 4);
@@ -1420,6 +1544,54 @@ int fpssft_run_batch(const void *cubes, int64_t batch, int64_t batch_stride,
                                    sched_index, n_sched, o, st);
     return run_batch_t<float>(cubes, batch, batch_stride, g, kn, params->mode, schedule,
                               sched_index, n_sched, o, st);
+}
+
+int fpssft_synthesize(const int32_t *freqs, const double *amps, const int32_t *counts,
+                      int64_t batch, int32_t k_cap, const fpssft_shape *shape, void *cubes,
+                      int64_t batch_stride, int32_t precision, void *stream) {
+    Geo gc, gr;
+    int rc;
+    if ((rc = make_geo(shape, &gc)) != FPSSFT_OK) return rc;
+    if (batch < 0 || batch > INT_MAX) return fail(FPSSFT_EINVAL, "bad batch");
+    if (k_cap < 1) return fail(FPSSFT_EINVAL, "k_cap must be >= 1");
+    for (int k = 0; k < gc.D; ++k)
+        if (shape->strides[k] != (k == gc.D - 1 ? 1 : shape->strides[k + 1] * shape->dims[k + 1]))
+            return fail(FPSSFT_EINVAL, "synthesize writes row-major contiguous cubes");
+    if (batch == 0) return FPSSFT_OK;
+    if (!freqs || !amps || !counts || !cubes) return fail(FPSSFT_EINVAL, "NULL buffer");
+    fpssft_shape row;
+    std::memset(&row, 0, sizeof(row));
+    row.ndim = 1;
+    row.dims[0] = shape->dims[gc.D - 1];
+    row.strides[0] = 1;
+    if ((rc = make_geo(&row, &gr)) != FPSSFT_OK) return rc;
+    const int NT = 256, NL = gr.L;
+    const int cs = precision == FPSSFT_F64 ? 16 : 8;
+    int rcnt = std::max(1, std::min(16, 65536 / (NL * cs)));  // rows per chunk
+    while (rcnt > 1 && plan_fft(&gr, rcnt, precision, NT) < 0) rcnt /= 2;
+    if (plan_fft(&gr, rcnt, precision, NT) < 0)
+        return fail(FPSSFT_EUNSUPPORTED, "row length too large for the synthesis kernel");
+    size_t sm = align16((size_t)rcnt * NL * cs) + align16((size_t)gc.L * cs) +
+                align16((size_t)NL * cs) + align16((size_t)k_cap * cs) +
+                align16((size_t)k_cap * 4 * MAXD) + align16((size_t)(NL + 1) * 4) +
+                align16((size_t)NL * 4) + align16((size_t)k_cap * 4) + 64 * 8;
+    if ((long long)sm > SMEM_PER_CTA) return fail(FPSSFT_EUNSUPPORTED, "k_cap/row too large");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    if (precision == FPSSFT_F64) {
+        e = cudaFuncSetAttribute(synth_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(synth_kernel)");
+        synth_kernel<double><<<(unsigned)batch, NT, sm, st>>>(freqs, amps, counts, k_cap, gc, gr,
+                                                             rcnt, (float2 *)cubes, batch_stride);
+    } else {
+        e = cudaFuncSetAttribute(synth_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(synth_kernel)");
+        synth_kernel<float><<<(unsigned)batch, NT, sm, st>>>(freqs, amps, counts, k_cap, gc, gr,
+                                                            rcnt, (float2 *)cubes, batch_stride);
+    }
+    return check_launch("synth_kernel");
 }
 
 int fpssft_plan(const fpssft_shape *shape, const fpssft_params *params, int32_t *mode,

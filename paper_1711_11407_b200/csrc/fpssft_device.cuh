@@ -19,6 +19,9 @@
 namespace fpssft {
 
 constexpr int MAXD = 4;
+#ifndef FPSSFT_R16_256
+#define FPSSFT_R16_256 1  // 256-point lines: radix 16x16 (1) or 8x8x4 (0)
+#endif
 constexpr int MAXSTAGES = 16;
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -76,7 +79,7 @@ struct Geo {
     int nstages;                    // FFT plan, 16 bits per stage s in plan[s/4] >> 16(s%4):
     unsigned long long plan[4];     //   bits 0-4 radix {2,3,4,5,7,8,16} (0 = direct O(L^2)),
                                     //   bits 5-7 butterflies per thread {1,2,4},
-                                    //   bits 8-10 lines transformed together (1..D+1)
+                                    //   bits 8-15 lines transformed together (1..255)
     int threads;                    // threads per instance the plan was made for
     int key_shift[MAXD];            // packed frequency key: m_k << key_shift[k]
     int key_mask[MAXD];             //   (lexicographic order = key order)
@@ -591,7 +594,7 @@ __device__ __forceinline__ void fft_lines(cpx<R> *x, int nlines, const Geo &g,
     int Ns = 1;
     for (int s = 0; s < g.nstages; ++s) {
         const int code = stage_code(g, s);
-        const int r = code & 31, mb = (code >> 5) & 7, G = (code >> 8) & 7;
+        const int r = code & 31, mb = (code >> 5) & 7, G = max(1, (code >> 8) & 255);
         const bool last = (s == g.nstages - 1);
         switch (r) {
             case 16: fft_stage_mb<R, 16, Team>(x, nlines, G, g.L, Ns, mb, roots, last, tid, nth); break;
@@ -624,7 +627,7 @@ __device__ __forceinline__ void fft_lines_warp(cpx<R> *x, int nlines, const Geo 
     int Ns = 1;
     for (int s = 0; s < g.nstages; ++s) {
         const int code = stage_code(g, s);
-        const int r = code & 31, G = (code >> 8) & 7;
+        const int r = code & 31, G = max(1, (code >> 8) & 255);
         const bool last = (s == g.nstages - 1);
         if (F && r == 16) fft_stage<R, 16, 1, WarpTeam>(x, nlines, G, g.L, Ns, roots, last, lane, 32);
         else if (r == 8) fft_stage<R, 8, F ? 2 : 1, WarpTeam>(x, nlines, G, g.L, Ns, roots, last, lane, 32);
@@ -712,7 +715,7 @@ template <class R, int L, int NL, int NT = 32, class Team = WarpTeam>
 __device__ __forceinline__ R fft_static(cpx<R> *x, const cpx<R> *roots, int tid) {
     constexpr bool F = sizeof(R) == 4;
     R e;
-    if constexpr (L == 256 && F) {
+    if constexpr (L == 256 && F && FPSSFT_R16_256) {
         e = stage_static<R, L, NL, 16, 1, false, NT, Team>(x, roots, tid);
         stage_static<R, L, NL, 16, 16, true, NT, Team>(x, roots, tid);
     } else if constexpr (L == 256) {

@@ -139,3 +139,28 @@ def project_onto_bins(freqs, amps, alpha, tau, shape: CubeShape, *, precision: s
                                              N.ptr(out), _precision_code(precision),
                                              N.stream_ptr(dev)))
     return out[0]
+
+
+def synthesize(result_or_freqs, amps=None, counts=None, *, shape: CubeShape | None = None,
+               precision: str = "fp32", out=None):
+    """Dense complex64 grid of every instance's recovered spectrum
+    (x(n) = sum_i a_i exp(+2 pi j sum_k n_k m_ik / N_k), the dense form of
+    SyntheticSource.sample_many, core.py:176-217).  Accepts a ``BatchResult``
+    or device tensors (freqs [B,k,D] int32, amps [B,k] complex128, counts [B])."""
+    import torch
+
+    if amps is None:
+        res = result_or_freqs
+        freqs, amps, counts, shape = res.freqs, res.amps, res.count, res.shape
+    else:
+        freqs = result_or_freqs
+    B, k_cap = int(freqs.shape[0]), int(freqs.shape[1])
+    dev = freqs.device
+    if out is None:
+        out = torch.empty((B, *shape.dims), dtype=torch.complex64, device=dev)
+    N.check(N.lib().fpssft_synthesize(N.ptr(freqs.contiguous()), N.ptr(amps.contiguous()),
+                                      N.ptr(counts.contiguous()), B, k_cap,
+                                      C_ref(N.make_shape(shape.dims)), N.ptr(out),
+                                      int(out.stride(0)) if B else 0,
+                                      _precision_code(precision), N.stream_ptr(dev)))
+    return out

@@ -353,3 +353,49 @@ def test_lazy_source_is_materialised():
                     P.FpsSftConfig(max_iterations=12, seed=5, **G.PROFILES["P32"]))
     order = np.lexsort(f.T[::-1])
     np.testing.assert_array_equal(rep.recovered.freq_array, f[order])
+
+
+# ------------------------------------------------------------ re-synthesis
+@pytest.mark.parametrize("dims,k", [((512, 512), 500), ((12, 18), 9), ((4, 6, 5), 7), ((32,), 5),
+                                    ((64, 64, 64), 200), ((256, 256), 100), ((10, 15), 150)])
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_synthesize_matches_dense_evaluation(dims, k, prec, rng):
+    """a15: dense re-synthesis vs the float64 evaluation of the same spectra
+    (SyntheticSource.sample_many semantics, core.py:176-217)."""
+    B = 3
+    k = min(k, int(np.prod(dims)))
+    kc = 1 << (k - 1).bit_length()
+    fr = np.zeros((B, kc, len(dims)), np.int32)
+    am = np.zeros((B, kc), np.complex128)
+    cnt = np.zeros(B, np.int32)
+    want = []
+    for b in range(B):
+        n = k - b  # ragged counts
+        flat = rng.choice(int(np.prod(dims)), size=n, replace=False)
+        f = np.stack(np.unravel_index(flat, dims), axis=-1)
+        a = rng.rayleigh(1.0, n) * np.exp(2j * np.pi * rng.random(n))
+        fr[b, :n], am[b, :n], cnt[b] = f, a, n
+        want.append(W.synthesize_np(dims, f, a))
+    got = ops.synthesize(torch.as_tensor(fr).to(DEV), torch.as_tensor(am).to(DEV),
+                         torch.as_tensor(cnt).to(DEV), shape=P.CubeShape(dims),
+                         precision=prec).cpu().numpy()
+    for b in range(B):
+        scale = np.abs(am[b]).sum()
+        # the grid is written as complex64 in both modes (rounding ~6e-8 |x|)
+        tol = (2e-6 if prec == "fp32" else 1.2e-7) * scale
+        assert np.abs(got[b] - want[b]).max() <= tol
+
+
+def test_cfg5_recover_then_resynthesise():
+    """Config 5 end to end on a few frames: recover, re-synthesise, compare
+    with the oracle's re-synthesis of its own recovered spectrum."""
+    w = W.CONFIGS[5]
+    inst, cubes = _batch(w, 3)
+    cfg = P.FpsSftConfig(seed=5, **G.PROFILES["PN"])
+    res = P.fps_sft_batch(cubes, cfg, k_cap=1024, precision="fp64")
+    img = ops.synthesize(res).cpu().numpy()
+    prof = O.Profile(**G.PROFILES["PN"])
+    for b, (_, _, cube) in enumerate(inst):
+        ref = O.recover(cube, w.dims, prof, seed=5)
+        want = O.synthesize(w.dims, ref.freqs, ref.amps)
+        assert np.abs(img[b] - want).max() <= 2e-6 * np.abs(ref.amps).sum()
