@@ -825,6 +825,120 @@ __global__ void __launch_bounds__(256, FPSSFT_WARP_MINB) recover_warp_kernel(con
 //   row = inverse FFT of V[r] along the last dimension        (dense part)
 // and each finished row is written once, coalesced: the kernel is bound by
 // the HBM write of the grid.
+// Compile-time variant for 2-D grids with NL-point rows (config 5: 512 x 512):
+// RC rows per chunk, compile-time padded FFT (fft_static), NT threads.
+template <class R, int NL, int RC, int NT>
+__global__ void __launch_bounds__(NT) synth_static_kernel(const int *__restrict__ freqs,
+                                                          const double *__restrict__ amps,
+                                                          const int *__restrict__ counts,
+                                                          int k_cap, Geo gc, float2 *out,
+                                                          long long out_stride) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int L = gc.L, N0 = gc.N[0], c0 = gc.cof[0];
+    const int tid = threadIdx.x;
+    const long long inst = blockIdx.x;
+    const int n = min(counts[inst], k_cap);
+    constexpr int VROW = NL + NL / 16 + 1;  // padded row stride (padi layout)
+    size_t o = 0;
+    cpx<R> *V = (cpx<R> *)(sm + o);       o = align16(o + (size_t)RC * VROW * sizeof(cpx<R>));
+    cpx<R> *rootsL = (cpx<R> *)(sm + o);  o = align16(o + (size_t)L * sizeof(cpx<R>));
+    cpx<R> *rootsN = (cpx<R> *)(sm + o);  o = align16(o + (size_t)NL * sizeof(cpx<R>));
+    cpx<R> *eamp = (cpx<R> *)(sm + o);    o = align16(o + (size_t)k_cap * sizeof(cpx<R>));
+    int *em0 = (int *)(sm + o);           o = align16(o + (size_t)k_cap * 4);
+    int *col_start = (int *)(sm + o);     o = align16(o + (size_t)(NL + 1) * 4);
+    int *col_fill = (int *)(sm + o);      o = align16(o + (size_t)NL * 4);
+    int *order = (int *)(sm + o);         o = align16(o + (size_t)k_cap * 4);
+    int *active = (int *)(sm + o);        o = align16(o + (size_t)NL * 4);
+    int *ired = (int *)(sm + o);
+
+    build_roots(rootsL, L);
+    build_roots(rootsN, NL);
+    for (int c = tid; c < NL; c += NT) col_fill[c] = 0;
+    __syncthreads();
+    for (int e = tid; e < n; e += NT) {
+        const long long src = inst * k_cap + e;
+        em0[e] = freqs[src * 2];
+        eamp[e] = {(R)amps[src * 2], (R)amps[src * 2 + 1]};
+        atomicAdd(&col_fill[freqs[src * 2 + 1]], 1);
+    }
+    __syncthreads();
+    // column -> entry ranges, and the list of non-empty columns (ascending)
+    int carry = 0, n_active = 0;
+    for (int j0 = 0; j0 < NL; j0 += NT) {
+        const int c = j0 + tid;
+        const int cnt = c < NL ? col_fill[c] : 0;
+        int tot;
+        const int pre = block_exscan(cnt | ((cnt > 0) << 16), ired, &tot);
+        if (c < NL) {
+            col_start[c] = carry + (pre & 0xFFFF);
+            col_fill[c] = 0;
+            if (cnt) active[n_active + (pre >> 16)] = c;
+        }
+        carry += tot & 0xFFFF;
+        n_active += tot >> 16;
+    }
+    if (tid == 0) col_start[NL] = carry;
+    __syncthreads();
+    for (int e = tid; e < n; e += NT) {
+        const int c = freqs[(inst * k_cap + e) * 2 + 1];
+        order[col_start[c] + atomicAdd(&col_fill[c], 1)] = e;
+    }
+    __syncthreads();
+    for (int c = tid; c < NL; c += NT) {  // entry order inside a column: deterministic sums
+        const int st = col_start[c], en = col_start[c + 1];
+        for (int i = st + 1; i < en; ++i) {
+            const int v = order[i];
+            int j = i - 1;
+            while (j >= st && order[j] > v) {
+                order[j + 1] = order[j];
+                --j;
+            }
+            order[j + 1] = v;
+        }
+    }
+    __syncthreads();
+
+    float2 *img = out + inst * out_stride;
+    const R scale = (R)NL;
+    const unsigned long long magicL = ~0ULL / (unsigned)L + 1ULL;
+    for (int r0 = 0; r0 < N0; r0 += RC) {
+        for (int q = tid; q < RC * VROW; q += NT) V[q] = {(R)0, (R)0};
+        __syncthreads();
+        // sparse part: one thread per non-empty column, all RC rows of the
+        // chunk, entries in order; phase c0 n0 m0 mod L advanced by c0 m0 per row
+        for (int a = tid; a < n_active; a += NT) {
+            const int c = active[a];
+            cpx<R> acc[RC];
+#pragma unroll
+            for (int r = 0; r < RC; ++r) acc[r] = {(R)0, (R)0};
+            for (int p = col_start[c]; p < col_start[c + 1]; ++p) {
+                const int e = order[p];
+                const unsigned m0 = (unsigned)em0[e];
+                const cpx<R> am = eamp[e];
+                const unsigned step = fastmod((unsigned)c0 * m0, magicL, (unsigned)L);
+                unsigned u = fastmod((unsigned)c0 * (unsigned)r0 % (unsigned)L * m0, magicL,
+                                     (unsigned)L);
+#pragma unroll
+                for (int r = 0; r < RC; ++r) {
+                    acc[r] = acc[r] + am * rootsL[u];
+                    u += step;
+                    if (u >= (unsigned)L) u -= (unsigned)L;
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < RC; ++r) V[padi<true>(r * NL + c)] = {acc[r].re, -acc[r].im};
+        }
+        __syncthreads();
+        fft_static<R, NL, RC, NT, BlockTeam>(V, rootsN, tid);
+#pragma unroll 4
+        for (int q = tid; q < RC * NL; q += NT) {
+            const cpx<R> x = V[padi<true>(q)];
+            img[(long long)r0 * NL + q] = make_float2((float)(x.re * scale), (float)(-x.im * scale));
+        }
+        __syncthreads();
+    }
+}
+
 template <class R>
 __global__ void __launch_bounds__(256) synth_kernel(const int *__restrict__ freqs,
                                                     const double *__restrict__ amps,
@@ -1567,6 +1681,33 @@ int fpssft_synthesize(const int32_t *freqs, const double *amps, const int32_t *c
     if ((rc = make_geo(&row, &gr)) != FPSSFT_OK) return rc;
     const int NT = 256, NL = gr.L;
     const int cs = precision == FPSSFT_F64 ? 16 : 8;
+    if (gc.D == 2 && NL == 512 && gc.N[0] % 16 == 0 &&
+        (long long)gc.L * gc.N[0] < (1LL << 32)) {
+        constexpr int RC = 16;  // compile-time variant: config 5's 512 x 512 images
+        const size_t sm2 = align16((size_t)RC * (512 + 512 / 16 + 1) * cs) +  // V (padded)
+                           align16((size_t)gc.L * cs) + align16((size_t)512 * cs) +
+                           align16((size_t)k_cap * cs) + align16((size_t)k_cap * 4) +
+                           align16((size_t)513 * 4) + align16((size_t)512 * 4) +
+                           align16((size_t)k_cap * 4) + align16((size_t)512 * 4) + 64 * 8;
+        if ((long long)sm2 <= SMEM_PER_CTA) {
+            cudaStream_t st = (cudaStream_t)stream;
+            cudaError_t e;
+            if (precision == FPSSFT_F64) {
+                auto k = synth_static_kernel<double, 512, RC, 256>;
+                e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+                if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(synth)");
+                k<<<(unsigned)batch, 256, sm2, st>>>(freqs, amps, counts, k_cap, gc,
+                                                     (float2 *)cubes, batch_stride);
+            } else {
+                auto k = synth_static_kernel<float, 512, RC, 256>;
+                e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+                if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(synth)");
+                k<<<(unsigned)batch, 256, sm2, st>>>(freqs, amps, counts, k_cap, gc,
+                                                     (float2 *)cubes, batch_stride);
+            }
+            return check_launch("synth_static_kernel");
+        }
+    }
     int rcnt = std::max(1, std::min(16, 65536 / (NL * cs)));  // rows per chunk
     while (rcnt > 1 && plan_fft(&gr, rcnt, precision, NT) < 0) rcnt /= 2;
     if (plan_fft(&gr, rcnt, precision, NT) < 0)
