@@ -77,23 +77,27 @@ _SAMPLE = None  # (cubes, dims, profile kwargs, seed) inherited by forked worker
 def _oracle_chunk(idx):
     from oracle import fps_oracle as O
 
-    cubes, dims, prof, seed = _SAMPLE
+    cubes, dims, prof, seed, synth = _SAMPLE
     p = O.Profile(**prof)
     t0 = time.perf_counter()
     its = 0
     for i in idx:
-        its += O.recover(cubes[i], dims, p, seed=seed).iterations_run
+        rep = O.recover(cubes[i], dims, p, seed=seed)
+        its += rep.iterations_run
+        if synth:  # config 5 also re-synthesises the image (numpy ifftn of the spectrum)
+            O.synthesize(dims, rep.freqs, rep.amps)
     return time.perf_counter() - t0, its
 
 
-def cpu_oracle_throughput(cubes: np.ndarray, dims, prof: dict, seed: int, workers: int):
+def cpu_oracle_throughput(cubes: np.ndarray, dims, prof: dict, seed: int, workers: int,
+                          synth: bool = False):
     """instances/s of the CPU oracle port over ``cubes`` on ``workers``
     processes (the reference's own ProcessPoolExecutor parallelism,
     oracle.py:275-277): instances / max worker busy time."""
     import multiprocessing as mp
 
     global _SAMPLE
-    _SAMPLE = (cubes, tuple(dims), prof, seed)
+    _SAMPLE = (cubes, tuple(dims), prof, seed, synth)
     n = len(cubes)
     parts = [list(range(i, n, workers)) for i in range(workers)]
     parts = [p for p in parts if p]
@@ -137,13 +141,15 @@ def run_reference(args, w):
         cpu_oracle_throughput(cubes[:cores], w.dims, prof, args.config, cores)
     times, its = [], []
     for _ in range(args.steps):
-        rate, wall, mean_it = cpu_oracle_throughput(cubes, w.dims, prof, args.config, cores)
+        rate, wall, mean_it = cpu_oracle_throughput(cubes, w.dims, prof, args.config, cores,
+                                                    synth=args.config == 5)
         times.append(count / rate)
         its.append(mean_it)
     total = sum(times)
     value = count * args.steps / total
     sample = (f"{count} of the {w.batch} instances of {w.name} (instances 0..{count - 1}), "
-              f"numpy float64 oracle port, {cores} worker processes")
+              f"numpy float64 oracle port, {cores} worker processes"
+              + (", recovery + numpy re-synthesis" if args.config == 5 else ""))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
@@ -414,7 +420,7 @@ def main():
         n = int(max(cores, min(B, args.cpu_seconds / max(per, 1e-4))))
         sample = cubes[:n].cpu().numpy()
         rate, wall, mean_it = cpu_oracle_throughput(sample, w.dims, P.PROFILES[w.profile],
-                                                    args.config, cores)
+                                                    args.config, cores, synth=synth)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"instances 0..{n - 1} of this run's {w.name} batch (same complex64 "
                          f"cubes), numpy float64 oracle port, {cores} processes, "
