@@ -216,6 +216,20 @@ def main():
             sched.append((a, t))
         ops[f"sched{qi}"] = np.asarray(sched, np.int64)
         op_meta["schedule"].append(dict(key=f"sched{qi}", dims=list(dims), seed=seed, T=T))
+    # sweep generator pins: run_sweep's trial seeds (oracle.py:215-227) and
+    # generate() spectra for uniform and clustered placements (oracle.py:88-139)
+    from fps_sft.oracle import GeneratorSpec, _trial_seeds, generate
+    op_meta["sweep"] = []
+    ops["trial_seeds"] = np.asarray(_trial_seeds(505, 8), dtype=np.uint64)
+    for gi, (dims, k, placement, csize, seed) in enumerate(
+            [((256, 256), 1280, "uniform", None, 11), ((32, 32), 9, "clustered", 9, 12),
+             ((64, 48), 50, "clustered", 25, 13), ((16, 12), 16, "uniform", None, 14)]):
+        truth, _ = generate(GeneratorSpec(shape=CubeShape(dims), k=k, placement=placement,
+                                          cluster_size=csize, seed=seed))
+        ops[f"gen{gi}/freqs"] = truth.freq_array
+        ops[f"gen{gi}/amps"] = truth.amp_array
+        op_meta["sweep"].append(dict(key=f"gen{gi}", dims=list(dims), k=k, placement=placement,
+                                     cluster_size=csize, seed=seed))
     np.savez_compressed(os.path.join(HERE, "ops.npz"), **ops)
     meta["ops"] = op_meta
     with open(os.path.join(HERE, "golden.json"), "w") as fh:

@@ -399,3 +399,26 @@ def test_cfg5_recover_then_resynthesise():
         ref = O.recover(cube, w.dims, prof, seed=5)
         want = O.synthesize(w.dims, ref.freqs, ref.amps)
         assert np.abs(img[b] - want).max() <= 2e-6 * np.abs(ref.amps).sum()
+
+
+# ------------------------------------------------------- Monte Carlo sweeps
+def test_sweep_small_shapes_recover():  # cf. pkg/tests/test_driver.py:57-69
+    from paper_1711_11407_b200 import sweep as S
+    row, per = S.run_cell(P.CubeShape((16, 12)), 16, "uniform", 100, 7,
+                          P.FpsSftConfig(max_iterations=30, stall_limit=10, **G.PROFILES["P32"]))
+    assert row.p_success >= 0.99
+    np.testing.assert_array_equal(per["samples_used"], per["iterations"] * 3 * 48)
+
+
+@pytest.mark.slow
+def test_sweep_paper_anchors_c5_c6():
+    """pkg/tests/test_acceptance.py:182-219 on the GPU: p(K=5 N0) >= 0.90 and
+    p(K=6 N0) <= 0.05 on 256x256 with T_max=85; mean samples for K=N0 in [4%, 8%]."""
+    from paper_1711_11407_b200 import sweep as S
+    cfg = P.FpsSftConfig(max_iterations=85, stall_limit=12, **G.PROFILES["P32"])
+    rows = S.run_sweep([(256, 256)], [1280, 1536], ["uniform"], 100, 505, cfg)
+    p = {r.k: r.p_success for r in rows}
+    assert p[1280] >= 0.90 and p[1536] <= 0.05, p
+    row = S.run_sweep([(256, 256)], [256], ["uniform"], 100, 606, cfg)[0]
+    assert row.p_success >= 0.99
+    assert 0.04 <= row.mean_percent_samples <= 0.08, row

@@ -144,7 +144,7 @@ def test_smem_budget_fits_configs():
         assert 0 < need <= 227 * 1024, (dims, need)
 
 
-@pytest.mark.parametrize("dims,k_cap,mode", [((256, 256), 256, "warp"), ((512, 512), 1024, "warp"),
+@pytest.mark.parametrize("dims,k_cap,mode", [((256, 256), 256, "warp"), ((512, 512), 1024, "cta"),
                                            ((64, 64, 64), 512, "warp"), ((1024, 2048), 2048, "cta"),
                                            ((12, 18), 64, "cta")])
 def test_launch_plan_picks_kernel(dims, k_cap, mode):
@@ -154,3 +154,17 @@ def test_launch_plan_picks_kernel(dims, k_cap, mode):
     assert 0 < plan["smem_bytes"] <= 227 * 1024
     if mode == "warp":
         assert plan["threads_per_cta"] == 32 * plan["instances_per_cta"]
+
+
+def test_sweep_seeds_and_generator_match_reference():  # oracle.py:88-139, 215-227
+    from paper_1711_11407_b200 import sweep as S
+    ops = G.npz("ops.npz")
+    got = np.asarray(S.trial_seeds(505, 8), dtype=np.uint64)
+    np.testing.assert_array_equal(got, ops["trial_seeds"])
+    for e in OPS["sweep"]:
+        kind = "clustered" if e["placement"] == "clustered" else "uniform"
+        f, a = S.generate_spectrum(P.CubeShape(e["dims"]), e["k"], e["seed"], kind,
+                                   e["cluster_size"])
+        order = np.lexsort(f.T[::-1])
+        np.testing.assert_array_equal(f[order], ops[f"{e['key']}/freqs"])
+        np.testing.assert_array_equal(a[order], ops[f"{e['key']}/amps"])
