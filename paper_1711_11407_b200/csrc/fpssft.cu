@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <cstdio>
 #include <cstring>
@@ -813,6 +814,7 @@ __global__ void __launch_bounds__(256, FPSSFT_WARP_MINB) recover_warp_kernel(con
 }
 
 #include "fpssft_team.cuh"
+#include "fpssft_warp_il.cuh"
 
 // ------------------------------------------------------------ re-synthesis
 // x(n) = sum_i a_i exp(+2 pi j sum_k n_k m_ik / N_k) on the full grid of
@@ -1415,6 +1417,28 @@ const void *warp_kernel_for(const Geo &g, int precision) {
     return precision == FPSSFT_F64 ? warp_kernel_for_t<double>(g) : warp_kernel_for_t<float>(g);
 }
 
+// Instances per warp of the interleaved warp kernel; off (1) by default:
+// measured on config 2/3 it loses to one instance per warp (half the warps
+// resident, 0.33 vs 0.225 ms) -- the loop is bound by per-warp dependency
+// latency, not by gather/compute phase alignment.  FPSSFT_IL=2|3 enables it.
+int il_instances_per_warp() {
+    const char *e = std::getenv("FPSSFT_IL");
+    const int v = e ? std::atoi(e) : 1;
+    return v < 1 ? 1 : (v > 3 ? 3 : v);
+}
+const void *il_kernel_for(const Geo &g, int precision, int ni) {
+    if (precision != FPSSFT_F32 || !g.off32) return nullptr;
+#define FPSSFT_IL_CASE(L_, D_)                                                             \
+    if (g.L == L_ && g.D == D_)                                                            \
+        return ni == 2 ? (const void *)recover_warp_il_kernel<float, L_, D_, 2>             \
+                       : (const void *)recover_warp_il_kernel<float, L_, D_, 3>;
+    FPSSFT_IL_CASE(256, 2)
+    FPSSFT_IL_CASE(512, 2)
+    FPSSFT_IL_CASE(64, 3)
+#undef FPSSFT_IL_CASE
+    return nullptr;
+}
+
 // The compile-time team kernel for a shape (one CTA of *nt threads per
 // instance), or nullptr if the shape has none.
 template <class R>
@@ -1496,6 +1520,27 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
                 wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * best_w, best_w,
                                 wl.roots + (size_t)best_w * wl.per_warp,
                                 warp_kernel_for(gw, precision)};
+            // interleaved variant (NI instances per warp, float32, compile-time
+            // shapes): same resident instances with the gathers pipelined
+            const int ni = il_instances_per_warp();
+            const void *ik = ni > 1 ? il_kernel_for(gw, precision, ni) : nullptr;
+            if (best_w && ik) {
+                long long best_inst = 0;
+                int bw = 0;
+                for (int w : {4, 2, 1}) {
+                    const long long smem = (long long)wl.roots + (long long)w * ni * wl.per_warp;
+                    if (smem > SMEM_PER_CTA) continue;
+                    const long long ctas = std::min<long long>(
+                        {32, SMEM_PER_SM / (smem + SMEM_RESERVED), 64 / w, reg_warps / w});
+                    if (ctas * w * ni > best_inst) {
+                        best_inst = ctas * w * ni;
+                        bw = w;
+                    }
+                }
+                if (bw && best_inst >= warp_warps)
+                    wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * bw, bw * ni,
+                                    wl.roots + (size_t)bw * ni * wl.per_warp, ik};
+            }
         }
         if (want == FPSSFT_MODE_WARP) {
             if (!warp_warps)
