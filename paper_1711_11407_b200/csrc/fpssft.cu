@@ -1445,6 +1445,7 @@ template <class R>
 const void *team_kernel_for_t(const Geo &g, int *nt) {
     if (!g.off32 || g.D != 2) return nullptr;
     if (g.L == 2048) {
+        if (*nt == 512) return (const void *)recover_team_kernel<R, 2048, 2, 512>;
         *nt = 1024;
         return (const void *)recover_team_kernel<R, 2048, 2, 1024>;
     }
@@ -1551,21 +1552,31 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
             return FPSSFT_OK;
         }
     }
-    // candidate 2: compile-time team kernel (one CTA per instance)
-    int tnt = 0;
-    const void *tk = (g.key_bits_ <= 31 && kn.k_cap <= 32768) ? team_kernel_for(g, precision, &tnt)
-                                                              : nullptr;
-    long long team_warps = 0;
+    // candidate 2: compile-time team kernel (one CTA per instance); among
+    // its CTA sizes take the one with the most resident instances; on a tie
+    // the smaller CTA (more registers per thread: measured faster on config
+    // 4, 0.588 vs 0.618 ms)
+    long long team_warps = 0, team_inst = 0;
     LaunchPlan tp{};
-    if (tk) {
+    if (g.key_bits_ <= 31 && kn.k_cap <= 32768) {
         const TeamLayout tl = make_team_layout(g.D, g.L, kn.k_cap, cs);
-        if ((long long)tl.total <= SMEM_PER_CTA) {
+        const char *env = std::getenv("FPSSFT_TEAM_NT");
+        for (int want_nt : {512, 0}) {
+            if (env && std::atoi(env) != (want_nt ? want_nt : 1024)) continue;
+            int tnt = want_nt;
+            const void *tk = team_kernel_for(g, precision, &tnt);
+            if (!tk || (want_nt && tnt != want_nt) || (long long)tl.total > SMEM_PER_CTA) continue;
             const int regs = (kernel_regs(tk, tnt >= 1024 ? 64 : 128) + 7) / 8 * 8;
             const long long ctas = std::min<long long>(
                 {32, SMEM_PER_SM / ((long long)tl.total + SMEM_RESERVED), 2048 / tnt,
                  65536 / ((long long)regs * tnt)});
-            team_warps = ctas * tnt / 32;
-            tp = LaunchPlan{FPSSFT_MODE_CTA, tnt, 1, tl.total, tk};
+            if (ctas < 1) continue;
+            const long long warps = ctas * tnt / 32;
+            if (ctas > team_inst) {
+                team_inst = ctas;
+                team_warps = warps;
+                tp = LaunchPlan{FPSSFT_MODE_CTA, tnt, 1, tl.total, tk};
+            }
         }
     }
     // warp mode unless it keeps too few warps resident and the team kernel

@@ -16,7 +16,7 @@
 struct TeamLayout {
     size_t spec, roots, slot_amp, slot_key, hash, slot_live;
     size_t bin_start, bin_fill, seg, slot_bin, slot_u0;  // projection scratch (union A)
-    size_t cand, cand_key, cand_amp, cand_st;            // classifier scratch (union B)
+    size_t cand;                                         // classifier scratch (union B)
     size_t red, total;
     int H;
 };
@@ -40,9 +40,6 @@ __host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, 
     y.slot_bin = a;  a = align16(a + (size_t)k_cap * 2);
     y.slot_u0 = a;   a = align16(a + (size_t)k_cap * 2);
     y.cand = u;      size_t b = align16(u + (size_t)L * 2);
-    y.cand_key = b;  b = align16(b + (size_t)L * 4);
-    y.cand_amp = b;  b = align16(b + (size_t)L * cs);
-    y.cand_st = b;   b = align16(b + (size_t)L);
     o = a > b ? a : b;
     y.red = o;       o = align16(o + 64 * 8);
     y.total = o;
@@ -78,9 +75,6 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
     unsigned short *slot_bin = (unsigned short *)(sm + lay.slot_bin);
     unsigned short *slot_u0 = (unsigned short *)(sm + lay.slot_u0);
     unsigned short *cand = (unsigned short *)(sm + lay.cand);
-    int *cand_key = (int *)(sm + lay.cand_key);
-    cpx<R> *cand_amp = (cpx<R> *)(sm + lay.cand_amp);
-    unsigned char *cand_st = sm + lay.cand_st;
     int *ired = (int *)(sm + lay.red);
     R *rred = (R *)(sm + lay.red + 256);
 
@@ -230,29 +224,23 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
             n_cand += tot;
         }
         __syncthreads();
-        for (int idx = tid; idx < n_cand; idx += NT) {
-            int m[MAXD];
-            cpx<R> a;
-            const int st = decode_candidate<R, PAD>(spec, g, cand[idx], al, ta, roots, round_tol,
-                                                    verify_tol, m, &a);
-            cand_st[idx] = (unsigned char)st;
-            if (st == 2) {
-                cand_key[idx] = pack_key(m, g);
-                cand_amp[idx] = a;
-            }
-        }
-        __syncthreads();
 
-        // (5) merge-by-sum in ascending bin order (driver.py:103-108)
+        // (5) decode + merge-by-sum, NT candidates per round in ascending bin
+        //     order (driver.py:103-108); decode results stay in registers
         int n_acc = 0;
         bool overflow = false;
 #pragma unroll 1
         for (int c0 = 0; c0 < n_cand; c0 += NT) {
             const int idx = c0 + tid;
-            const int st = idx < n_cand ? cand_st[idx] : 0;
+            const int b = idx < n_cand ? cand[idx] : -1;
+            int m[MAXD];
+            cpx<R> a;
+            int st = 0;
+            if (b >= 0)
+                st = decode_candidate<R, PAD>(spec, g, b, al, ta, roots, round_tol, verify_tol, m, &a);
             int found = -1, key = 0;
             if (st == 2) {
-                key = cand_key[idx];
+                key = pack_key(m, g);
                 found = hash16_find(hash, slot_key, H, key);
             }
             const int fresh = st == 2 && found < 0;
@@ -264,7 +252,6 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
                 break;
             }
             if (st == 2) {
-                const cpx<R> a = cand_amp[idx];
                 cpx<R> v = a;
                 int s;
                 if (fresh) {
@@ -278,9 +265,6 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
                 const bool keep = !(cabs(v) <= prune);
                 slot_amp[s] = keep ? v : cpx<R>{(R)0, (R)0};
                 slot_live[s] = keep;
-                int m[MAXD];
-                unpack_key(key, g, m);
-                const int b = cand[idx];
                 const int u0 = phase_of(m, g, ta);  // driver.py:189-194
 #pragma unroll
                 for (int i = 0; i < MAXD + 1; ++i)
@@ -288,6 +272,7 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
                         spec[padi<PAD>(i * L + b)] =
                             spec[padi<PAD>(i * L + b)] - a * roots[phase_step(u0, i, m, g)];
             }
+            if (b >= 0) resid = max(resid, bin_residual<R, PAD>(spec, g, b));
             n_slots += tot_new;
             n_acc += tot >> 16;
             __syncthreads();  // inserts visible to the next round's lookups
@@ -302,8 +287,6 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
             }
             break;
         }
-        for (int idx = tid; idx < n_cand; idx += NT)
-            resid = max(resid, bin_residual<R, PAD>(spec, g, cand[idx]));
 
         // (6) amp_sum and (7) termination                   driver.py:108,196-204
         R my = (R)0;
