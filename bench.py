@@ -60,6 +60,49 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _probe_rate():
+    """Random-line fetch rate of this GPU measured by tools/gather_probe.cu
+    (variant 0: plain 8-byte loads, 2^28-element array, all SMs)."""
+    import re
+
+    try:
+        for line in open(os.path.join(ROOT, "profiles", "r01_gather_probe.txt")):
+            m = re.search(r"2\^28 x8B\s+ctas\s+1184\s+variant 0:.*?([0-9.]+) Gsamples/s", line)
+            if m:
+                return float(m.group(1)) * 1e9
+    except OSError:
+        pass
+    return None
+
+
+def _lines_per_launch(shape, schedule, iterations, sched_index=None):
+    """Distinct 128-byte lines the gathers of one launch touch: per
+    iteration, the (D+1) L sample offsets of the lines (row-major complex64
+    cube, 16 samples per line), counted once per instance that runs it."""
+    dims = np.asarray(shape.dims, np.int64)
+    strides = np.cumprod(np.concatenate([[1], dims[::-1][:-1]]))[::-1]
+    L = shape.line_len
+    l = np.arange(L, dtype=np.int64)[:, None]
+    iters = np.asarray(iterations)
+    sidx = np.zeros(len(iters), np.int64) if sched_index is None else np.asarray(sched_index)
+    total = 0
+    for s in np.unique(sidx):
+        its = iters[sidx == s]
+        per_t = []
+        for t in range(int(its.max())):
+            al, ta = schedule[s, t, 0].astype(np.int64), schedule[s, t, 1].astype(np.int64)
+            offs = []
+            for i in range(shape.ndim + 1):
+                tau = ta.copy()
+                if i:
+                    tau[i - 1] = (tau[i - 1] + 1) % dims[i - 1]
+                offs.append((((l * al + tau) % dims) * strides).sum(1))
+            per_t.append(len(np.unique(np.concatenate(offs) // 16)))
+        per_t = np.asarray(per_t)
+        total += int(sum(per_t[:n].sum() for n in its))
+    return total
+
+
 def _traffic(workload_name):
     """DRAM bytes per launch from the committed ncu capture, if any."""
     try:
@@ -355,6 +398,14 @@ def main():
                 "kernel": "recover (" + runner.plan["mode"] + " per instance)",
                 "kernel_ms": rec_ms,
                 "note": "achieved = sum(samples_used)*8 B gathered per launch / mean launch time"}
+    probe = _probe_rate()
+    lines = _lines_per_launch(shape, runner.schedule_host, iters)
+    roofline["gather"] = {
+        "lines_per_launch": lines, "achieved_lines_per_s": lines / (rec_ms / 1e3),
+        "peak_lines_per_s": probe,
+        "frac": (lines / (rec_ms / 1e3) / probe) if probe else None,
+        "note": "random 128-byte line fetches: the measured bound of an isolated-8-byte "
+                "gather (tools/gather_probe.cu, profiles/r01_gather_probe.txt)"}
     if synth:
         s_ms = sum(synth_ms) / args.steps
         wbytes = cubes.numel() * cubes.element_size()

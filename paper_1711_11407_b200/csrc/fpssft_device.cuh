@@ -317,65 +317,6 @@ __device__ __forceinline__ void gather_lines_async(cpx<float> *spec,
             if (k < D) cp_async8(spec + (k + 1) * L + l, cube + base + delta[k]);
     }
 }
-// Register-staged variant: samples read with non-L1-allocating loads
-// (ld.global.nc.L1::no_allocate), CH rows of every line in flight per thread,
-// then stored to shared memory.  An L1-allocating fill (cp.async.ca) pulls
-// whole 128-byte lines through L2 for one 8-byte sample; this path moves
-// only the 32-byte sectors that hold samples.
-__device__ __forceinline__ float2 ld_stream(const float2 *p) {
-    float2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];"
-                 : "=f"(v.x), "=f"(v.y)
-                 : "l"(p));
-    return v;
-}
-template <class R, int CH>
-__device__ __forceinline__ R gather_lines_reg(cpx<R> *spec, const float2 *__restrict__ cube,
-                                              const Geo &g, const int *al, const int *ta, int tid,
-                                              int nth) {
-    const int L = g.L, D = g.D;
-    R energy = (R)0;
-    for (int l0 = tid; l0 < L; l0 += CH * nth) {
-        float2 v[CH][MAXD + 1];
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-            const int l = l0 + c * nth;
-            if (l < L) {
-                long long base = 0;
-                long long delta[MAXD];
-#pragma unroll
-                for (int k = 0; k < MAXD; ++k) {
-                    if (k < D) {
-                        unsigned n = fastmod((unsigned)al[k] * (unsigned)l + (unsigned)ta[k],
-                                             g.magic[k], (unsigned)g.N[k]);
-                        base += (long long)n * g.stride[k];
-                        delta[k] = (n + 1 == (unsigned)g.N[k]) ? -(long long)n * g.stride[k]
-                                                                : g.stride[k];
-                    }
-                }
-                v[c][0] = ld_stream(cube + base);
-#pragma unroll
-                for (int k = 0; k < MAXD; ++k)
-                    if (k < D) v[c][k + 1] = ld_stream(cube + base + delta[k]);
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-            const int l = l0 + c * nth;
-            if (l < L) {
-#pragma unroll
-                for (int k = 0; k < MAXD + 1; ++k) {
-                    if (k <= D) {
-                        spec[k * L + l] = {(R)v[c][k].x, (R)v[c][k].y};
-                        energy += (R)v[c][k].x * (R)v[c][k].x + (R)v[c][k].y * (R)v[c][k].y;
-                    }
-                }
-            }
-        }
-    }
-    return energy;
-}
-
 template <class R>
 __device__ __forceinline__ R line_energy(const cpx<R> *spec, int n, int tid, int nth) {
     R e = (R)0;

@@ -322,10 +322,12 @@ def fps_sft_batch(cubes, config: FpsSftConfig = FpsSftConfig(), *, schedule=None
     return runner.run(cubes)
 
 
-def materialize(source) -> tuple[CubeShape, "np.ndarray | object"]:
+def materialize(source, device=None) -> tuple[CubeShape, "np.ndarray | object"]:
     """The dense complex64 cube behind a sample source: a ``DenseSource``'s
-    own array, otherwise ``sample_many`` over the whole grid (host side,
-    evaluated once; e.g. the reference's lazy ``SyntheticSource``)."""
+    own array; for a lazy sinusoid mixture that exposes its spectrum (the
+    reference's ``SyntheticSource.spectrum``, core.py:176-217) the grid is
+    synthesised on the device (``fpssft_synthesize``, SURVEY §8(f) row 4);
+    otherwise ``sample_many`` over the whole grid on the host."""
     shape = source.shape()
     if not isinstance(shape, CubeShape):
         shape = CubeShape(shape.dims)
@@ -334,6 +336,24 @@ def materialize(source) -> tuple[CubeShape, "np.ndarray | object"]:
     data = getattr(source, "_data", None)  # the reference's DenseSource
     if isinstance(data, np.ndarray) and data.shape == shape.dims:
         return shape, data.astype(np.complex64)
+    spec = getattr(source, "spectrum", None)
+    if spec is not None and hasattr(spec, "freq_array") and hasattr(spec, "amp_array"):
+        import torch
+
+        from .ops import synthesize
+
+        f = np.asarray(spec.freq_array, np.int32).reshape(-1, shape.ndim)
+        a = np.asarray(spec.amp_array, np.complex128)
+        k = max(1, len(a))
+        kc = 1 << (k - 1).bit_length()
+        fr = np.zeros((1, kc, shape.ndim), np.int32)
+        am = np.zeros((1, kc), np.complex128)
+        fr[0, :len(a)], am[0, :len(a)] = f, a
+        dev = torch.device(device if device is not None else "cuda")
+        cube = synthesize(torch.as_tensor(fr, device=dev), torch.as_tensor(am, device=dev),
+                          torch.as_tensor(np.asarray([len(a)], np.int32), device=dev),
+                          shape=shape, precision="fp64")
+        return shape, cube[0]
     if shape.n_total > (1 << 24):
         raise ValueError(f"refusing to materialise a lazy source of {shape.n_total} samples")
     grid = np.indices(shape.dims).reshape(shape.ndim, -1).T
@@ -351,7 +371,7 @@ def fps_sft(source: SignalSource, config: FpsSftConfig = FpsSftConfig(), *,
     """
     import torch
 
-    shape, cube = materialize(source)
+    shape, cube = materialize(source, device)
     dev = torch.device(device if device is not None else "cuda")
     if isinstance(cube, torch.Tensor):
         t = cube.to(device=dev, dtype=torch.complex64)
