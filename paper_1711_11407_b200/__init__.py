@@ -11,16 +11,17 @@ from .core import (CubeShape, DenseSource, FreqIndex, SignalSource, Sinusoid, Sp
 from .driver import (PROFILES, BatchResult, BatchRunner, FpsSftConfig, IterationStats,
                      RecoveryReport, default_max_iterations, fps_sft, fps_sft_batch, materialize,
                      max_k_cap)
+from .baseline import baseline_sft
 from .schedule import (bins_of_frequencies, is_valid_slope, sample_slope, schedule_from_seed,
                        valid_slopes)
 
 __version__ = "0.1.0"
 
-ALGORITHMS = {"fps-b200": fps_sft}
+ALGORITHMS = {"fps-b200": fps_sft, "baseline-b200": baseline_sft}
 
 __all__ = ["ALGORITHMS", "BatchResult", "BatchRunner", "CubeShape", "DenseSource",
            "FpsSftConfig", "FreqIndex", "IterationStats", "PROFILES", "RecoveryReport",
-           "SignalSource", "Sinusoid", "SparseSpectrum", "bins_of_frequencies",
+           "SignalSource", "Sinusoid", "SparseSpectrum", "baseline_sft", "bins_of_frequencies",
            "default_max_iterations", "fps_sft", "fps_sft_batch", "is_valid_slope",
            "make_dense_source", "materialize", "max_k_cap", "sample_slope",
            "schedule_from_seed", "spectra_match", "valid_slopes"]

@@ -131,6 +131,35 @@ def main():
         meta["runs"].append(entry)
         print(f"{n:28s} it={rep.iterations_run:3d} k={rep.recovered.k:4d} {rep.terminated_by}",
               flush=True)
+    # baseline_sft (driver.py:219-314), the row/column comparison algorithm
+    from fps_sft.driver import baseline_sft
+    meta["baseline"] = []
+    for name, recipe, cfg in (
+            ("bl_single", dict(kind="spectrum", dims=[8, 8], freqs=[[2, 3]], amps_re=[1.5],
+                               amps_im=[-0.5]), dict(max_iterations=10)),
+            ("bl_deadlock", dict(kind="spectrum", dims=[8, 8], freqs=[[2, 2], [2, 5], [5, 2], [5, 5]], amps_re=[1.0] * 4,
+                                 amps_im=[0.0] * 4), dict(max_iterations=30)),
+            ("bl_uniform32", dict(kind="reference_generate", dims=[32, 32], k=8, seed=5),
+             dict(max_iterations=30)),
+            ("bl_uniform64", dict(kind="reference_generate", dims=[64, 64], k=40, seed=9),
+             dict(max_iterations=40)),
+            ("bl_uniform256", dict(kind="reference_generate", dims=[256, 256], k=128, seed=3),
+             dict(max_iterations=60))):
+        cube = cube_from_recipe(recipe)
+        dims = tuple(recipe["dims"])
+        rep = baseline_sft(make_dense_source(cube, CubeShape(dims)),
+                           FpsSftConfig(**cfg, **PROFILES["P32"]))
+        arrays[f"{name}/freqs"] = rep.recovered.freq_array.reshape(-1, 2)
+        arrays[f"{name}/amps"] = rep.recovered.amp_array
+        arrays[f"{name}/log_counts"] = np.asarray([(s.candidates, s.accepted, s.rejected)
+                                                   for s in rep.iteration_log], np.int64)
+        if cube.size <= INLINE_MAX:
+            arrays[f"{name}/cube"] = cube
+        meta["baseline"].append(dict(name=name, recipe=recipe, cfg=cfg, profile="P32",
+                                     sha256=sha(cube), iterations_run=rep.iterations_run,
+                                     samples_used=rep.samples_used,
+                                     terminated_by=rep.terminated_by))
+        print(f"{name:28s} it={rep.iterations_run:3d} k={rep.recovered.k:4d} {rep.terminated_by}")
     np.savez_compressed(os.path.join(HERE, "runs.npz"), **arrays)
 
     # ---------------- per-function pins ----------------

@@ -463,3 +463,33 @@ def test_lazy_spectrum_source_synthesised_on_device():
     order = np.lexsort(f.T[::-1])
     np.testing.assert_array_equal(rep.recovered.freq_array, f[order])
     assert np.all(np.abs(rep.recovered.amp_array - a[order]) <= 1e-4 * np.abs(a[order]))
+
+
+# ------------------------------------------------------------- baseline_sft
+BASE = G.meta().get("baseline", [])
+
+
+@pytest.mark.parametrize("entry", BASE, ids=lambda e: e["name"])
+def test_baseline_sft_matches_reference(entry):  # driver.py:219-314
+    a = G.npz("runs.npz")
+    n = entry["name"]
+    cube = a[f"{n}/cube"] if f"{n}/cube" in a else G.cube_from_recipe(entry["recipe"])
+    assert G.sha(cube) == entry["sha256"]
+    shape = P.CubeShape(cube.shape)
+    cfg = P.FpsSftConfig(**entry["cfg"], **G.PROFILES[entry["profile"]])
+    rep = P.baseline_sft(P.make_dense_source(cube, shape), cfg)
+    assert rep.terminated_by == entry["terminated_by"]
+    assert rep.iterations_run == entry["iterations_run"]
+    assert rep.samples_used == entry["samples_used"]
+    np.testing.assert_array_equal(rep.recovered.freq_array.reshape(-1, 2), a[f"{n}/freqs"])
+    want = a[f"{n}/amps"]
+    assert np.all(np.abs(rep.recovered.amp_array - want) <= 1e-4 * np.abs(want))
+    assert [(s.candidates, s.accepted, s.rejected) for s in rep.iteration_log] == \
+        [tuple(int(v) for v in c) for c in a[f"{n}/log_counts"]]
+
+
+def test_baseline_sft_rejects_bad_shapes():  # pkg/tests/test_driver.py:170-183
+    for dims in ((8, 12), (6, 6), (4, 4, 4)):
+        cube = np.zeros(dims, np.complex64)
+        with pytest.raises(ValueError):
+            P.baseline_sft(P.make_dense_source(cube, P.CubeShape(dims)))
