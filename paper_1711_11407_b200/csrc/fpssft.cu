@@ -22,6 +22,9 @@
 #include "../../include/fpssft.h"
 #include "fpssft_device.cuh"
 
+#ifndef FPSSFT_PREFETCH_FROM
+#define FPSSFT_PREFETCH_FROM 4  // L2-prefetch iteration t+1 from iteration t >= this on
+#endif
 #ifndef FPSSFT_WARP_MINB
 #define FPSSFT_WARP_MINB 2  // CTAs of 256 threads per SM the warp kernel's registers allow
 #endif
@@ -573,6 +576,13 @@ __global__ void __launch_bounds__(256, FPSSFT_WARP_MINB) recover_warp_kernel(con
                     nal[k] = k < D ? sched[(long long)(it + 1) * 2 * D + k] : 0;
                     nta[k] = k < D ? sched[(long long)(it + 1) * 2 * D + D + k] : 0;
                 }
+                // long-running instances (noisy configs: tens of iterations)
+                // L2-prefetch the next iteration's lines; short ones do not --
+                // on config 2 (~3 iterations) the extra random DRAM fetches of
+                // a last-iteration prefetch cost more than the latency saved
+                if (LC != 0 && it >= FPSSFT_PREFETCH_FROM && g.off32 &&
+                    line_params_ok(g, nal, nta))
+                    prefetch_lines_l2<LC>(cube, g, nal, nta, lane);
             }
             cp_async_wait_all();
             __syncwarp();

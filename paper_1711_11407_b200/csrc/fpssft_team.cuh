@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
                 nal[k] = k < D ? sched[(long long)(it + 1) * 2 * D + k] : 0;
                 nta[k] = k < D ? sched[(long long)(it + 1) * 2 * D + D + k] : 0;
             }
+            // (no L2 prefetch here: measured slower on config 5, 42.3 vs 38.2 ms)
         }
         if constexpr (sizeof(R) == 4) cp_async_wait_all();
         __syncthreads();
