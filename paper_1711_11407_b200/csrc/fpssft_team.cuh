@@ -12,6 +12,9 @@
 // Included by fpssft.cu after the warp kernel (shares its helpers).
 #pragma once
 // (included inside namespace fpssft)
+#ifndef FPSSFT_TEAM_PROJ
+#define FPSSFT_TEAM_PROJ 1  // projection: 1 = warp match_any + ordered apply, 0 = counting sort
+#endif
 
 struct TeamLayout {
     size_t spec, roots, slot_amp, slot_key, hash, slot_live;
@@ -136,7 +139,63 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
         if (sizeof(R) == 4 && kn.noise_coef > 0)
             noise_floor = (R)kn.noise_coef * sqrt(block_sum(my_energy, rred));
 
-        // (3) construction-subtraction: counting sort of the live slots by
+        // (3) construction-subtraction
+#if FPSSFT_TEAM_PROJ == 1
+        //     NT slots per round, 32 per warp; slots sharing a bin inside a
+        //     warp are summed by their lowest lane (match_any), and the warps
+        //     apply their partial sums one after another -- a fixed order, so
+        //     the result is deterministic without a sort
+        if (n_slots > 0) {
+            constexpr int NW = NT / 32;
+            const int warp = tid >> 5, lane = tid & 31;
+            int *scr_u = (int *)(sm + lay.bin_start) + warp * 32 * (MAXD + 1);
+            cpx<R> *scr_amp = (cpx<R> *)((int *)(sm + lay.bin_start) + NW * 32 * (MAXD + 1)) +
+                              warp * 32;
+#pragma unroll 1
+            for (int c0 = 0; c0 < n_slots; c0 += NT) {
+                const int s = c0 + tid;
+                const bool valid = s < n_slots && slot_live[s];
+                int b = -1 - lane;
+                if (valid) {
+                    int m[MAXD];
+                    unpack_key(slot_key[s], g, m);
+                    b = bin_of(m, g, al);
+                    const int u0 = phase_of(m, g, ta);
+#pragma unroll
+                    for (int i = 0; i < MAXD + 1; ++i)
+                        if (i < nl) scr_u[i * 32 + lane] = phase_step(u0, i, m, g);
+                    scr_amp[lane] = slot_amp[s];
+                }
+                __syncwarp();
+                const unsigned grp = __match_any_sync(FULL, b);
+                const bool leader = valid && lane == __ffs(grp) - 1;
+                cpx<R> P[MAXD + 1];
+#pragma unroll
+                for (int i = 0; i < MAXD + 1; ++i) P[i] = {(R)0, (R)0};
+                if (leader) {
+                    for (unsigned rest = grp; rest; rest &= rest - 1) {
+                        const int j = __ffs(rest) - 1;
+                        const cpx<R> aj = scr_amp[j];
+#pragma unroll
+                        for (int i = 0; i < MAXD + 1; ++i)
+                            if (i < nl) P[i] = P[i] + aj * roots[scr_u[i * 32 + j]];
+                    }
+                }
+                const int nw_live = min(NW, (n_slots - c0 + 31) / 32);
+                for (int w2 = 0; w2 < nw_live; ++w2) {
+                    if (w2) __syncthreads();
+                    if (warp == w2 && leader) {
+#pragma unroll
+                        for (int i = 0; i < MAXD + 1; ++i)
+                            if (i < nl)
+                                spec[padi<PAD>(i * L + b)] = spec[padi<PAD>(i * L + b)] - P[i];
+                    }
+                }
+                __syncthreads();
+            }
+        }
+#else
+        //     counting sort of the live slots by
         //     bin, per-bin sums in slot order (deterministic, no float atomics)
         if (n_slots > 0) {
             int *fill = (int *)bin_fill;
@@ -207,22 +266,31 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
             __syncthreads();
         }
 
+#endif
+
         // (4) magnitude test on every bin, candidates compacted in ascending
         //     order; the residual of non-candidate bins is folded in
         const R floor =
             max(max((R)kn.energy_floor_abs, (R)kn.energy_floor * amp_sum), noise_floor);
         R resid = (R)0;
         int n_cand = 0;
-#pragma unroll 1
-        for (int j0 = 0; j0 < L; j0 += NT) {
-            const int b = j0 + tid;
-            R top = (R)0;
-            const bool ok = b < L && bin_is_candidate<R, PAD>(spec, g, b, mag_tol, floor, &top);
-            if (!ok) resid = max(resid, top);
-            int tot;
-            const int pre = block_exscan(ok ? 1 : 0, ired, &tot);
-            if (ok) cand[n_cand + pre] = (unsigned short)b;
-            n_cand += tot;
+        {
+            // thread t tests the BPT consecutive bins [t BPT, (t+1) BPT): one
+            // block scan of the per-thread counts keeps ascending order
+            constexpr int BPT = (LC + NT - 1) / NT;
+            unsigned okm = 0;
+#pragma unroll
+            for (int j = 0; j < BPT; ++j) {
+                const int b = tid * BPT + j;
+                R top = (R)0;
+                const bool ok = b < L && bin_is_candidate<R, PAD>(spec, g, b, mag_tol, floor, &top);
+                if (!ok) resid = max(resid, top);
+                okm |= (unsigned)ok << j;
+            }
+            int pos = block_exscan(__popc(okm), ired, &n_cand);
+#pragma unroll
+            for (int j = 0; j < BPT; ++j)
+                if (okm >> j & 1) cand[pos++] = (unsigned short)(tid * BPT + j);
         }
         __syncthreads();
 
