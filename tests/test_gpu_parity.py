@@ -493,3 +493,25 @@ def test_baseline_sft_rejects_bad_shapes():  # pkg/tests/test_driver.py:170-183
         cube = np.zeros(dims, np.complex64)
         with pytest.raises(ValueError):
             P.baseline_sft(P.make_dense_source(cube, P.CubeShape(dims)))
+
+
+@pytest.mark.parametrize("dims,k", [((1, 8), 3), ((8, 1), 3), ((11, 13), 6), ((3, 4, 5, 6), 9),
+                                    ((7,), 2), ((2, 2), 2), ((5, 5, 5), 8), ((9, 12), 10)])
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_unusual_shapes_match_oracle(dims, k, prec, rng):
+    """Degenerate (N_k = 1), prime, 4-D and tiny shapes through the generic
+    kernels, against the oracle on the same cube and schedule."""
+    f, a = W.reference_generate(dims, k, 17)
+    cube = W.synthesize_np(dims, f, a).astype(np.complex64)
+    prof = dict(G.PROFILES["P32"])
+    cfg = P.FpsSftConfig(max_iterations=12, stall_limit=6, seed=5, **prof)
+    rep = P.fps_sft(P.make_dense_source(cube, P.CubeShape(dims)), cfg, precision=prec)
+    ref = O.recover(cube, dims, O.Profile(max_iterations=12, stall_limit=6, **prof), seed=5)
+    if prec == "fp32" and len(ref.amps) and np.abs(ref.amps).min() < 1e-5 * np.abs(ref.amps).sum():
+        pytest.skip("reference recovered complex64-rounding-level entries")
+    exp = dict(freqs=ref.freqs, amps=ref.amps, terminated_by=ref.terminated_by,
+               iterations_run=ref.iterations_run, samples_used=ref.samples_used,
+               log_alpha=[x[0] for x in ref.log], log_tau=[x[1] for x in ref.log],
+               log_counts=[x[2:] for x in ref.log])
+    _check_report(rep, exp, 1e-9 if prec == "fp64" else 1e-4,
+                  amp_atol_rel=1e-13 if prec == "fp64" else 0.0)
