@@ -1569,13 +1569,14 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
     long long team_warps = 0, team_inst = 0;
     LaunchPlan tp{};
     if (g.key_bits_ <= 31 && kn.k_cap <= 32768) {
-        const TeamLayout tl = make_team_layout(g.D, g.L, kn.k_cap, cs);
         const char *env = std::getenv("FPSSFT_TEAM_NT");
         for (int want_nt : {512, 0}) {
             if (env && std::atoi(env) != (want_nt ? want_nt : 1024)) continue;
             int tnt = want_nt;
             const void *tk = team_kernel_for(g, precision, &tnt);
-            if (!tk || (want_nt && tnt != want_nt) || (long long)tl.total > SMEM_PER_CTA) continue;
+            if (!tk || (want_nt && tnt != want_nt)) continue;
+            const TeamLayout tl = make_team_layout(g.D, g.L, kn.k_cap, cs, tnt);
+            if ((long long)tl.total > SMEM_PER_CTA) continue;
             const int regs = (kernel_regs(tk, tnt >= 1024 ? 64 : 128) + 7) / 8 * 8;
             const long long ctas = std::min<long long>(
                 {32, SMEM_PER_SM / ((long long)tl.total + SMEM_RESERVED), 2048 / tnt,
@@ -1616,7 +1617,8 @@ int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
                 const Knobs &kn, int want_mode, const int32_t *schedule,
                 const int32_t *sched_index, int32_t n_sched, const OutPtrs &o, cudaStream_t st) {
     LaunchPlan lp;
-    int rc = make_plan(g, kn, sizeof(R) == 8 ? FPSSFT_F64 : FPSSFT_F32, want_mode, &lp);
+    const int prec = sizeof(R) == 8 ? FPSSFT_F64 : FPSSFT_F32;
+    int rc = make_plan(g, kn, prec, want_mode, &lp);
     if (rc != FPSSFT_OK) return rc;
     cudaError_t e;
     if (lp.mode == FPSSFT_MODE_CTA && lp.kernel) {  // compile-time team kernel

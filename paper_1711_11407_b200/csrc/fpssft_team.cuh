@@ -24,7 +24,7 @@ struct TeamLayout {
     int H;
 };
 
-__host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, int cs) {
+__host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, int cs, int nt) {
     TeamLayout y;
     const size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // padi() layout
     const size_t sort_bytes = 1024 + (size_t)k_cap * 4;
@@ -43,7 +43,10 @@ __host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, 
     y.slot_bin = a;  a = align16(a + (size_t)k_cap * 2);
     y.slot_u0 = a;   a = align16(a + (size_t)k_cap * 2);
     y.cand = u;      size_t b = align16(u + (size_t)L * 2);
+    // the match_any projection's per-warp scratch also lives in this union
+    const size_t c = align16(u + (size_t)(nt / 32) * 32 * ((MAXD + 1) * 4 + cs));
     o = a > b ? a : b;
+    o = o > c ? o : c;
     y.red = o;       o = align16(o + 64 * 8);
     y.total = o;
     return y;
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
     g.D = DC;
     g.nlines = DC + 1;
     constexpr int L = LC, D = DC, nl = DC + 1;
-    const TeamLayout lay = make_team_layout(D, L, kn.k_cap, (int)sizeof(cpx<R>));
+    const TeamLayout lay = make_team_layout(D, L, kn.k_cap, (int)sizeof(cpx<R>), NT);
     cpx<R> *spec = (cpx<R> *)(sm + lay.spec);
     cpx<R> *roots = (cpx<R> *)(sm + lay.roots);
     cpx<R> *slot_amp = (cpx<R> *)(sm + lay.slot_amp);

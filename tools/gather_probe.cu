@@ -4,6 +4,7 @@
 // run under ncu for dram__bytes_read.sum / lts__t_sectors_srcunit_tex_op_read.sum.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cuda_runtime.h>
 
 template <int V>
@@ -102,6 +103,36 @@ int main(int argc, char **argv) {
                         c.logn, blocks, V, ms, loads / ms / 1e6);                         \
     }
             RUN(0) RUN(2) RUN(3) RUN(4)
+        }
+    }
+    // zero-copy: the same random 8-byte gathers from pinned, mapped host memory
+    {
+        float2 *h = nullptr, *hd = nullptr;
+        if (cudaHostAlloc(&h, n * sizeof(float2), cudaHostAllocMapped) == cudaSuccess &&
+            cudaHostGetDevicePointer(&hd, h, 0) == cudaSuccess) {
+            memset(h, 0, n * sizeof(float2));
+            const unsigned long long mask = n - 1;
+            for (int sms : {148, 74}) {
+                const int blocks = sms * 8;
+                const double loads = (double)blocks * threads * per;
+                for (int rep = 0; rep < 2; ++rep) {
+#define RUNH(V)                                                                            \
+    {                                                                                      \
+        cudaEventRecord(e0);                                                               \
+        probe<V><<<blocks, threads>>>(hd, mask, per, o, 29 + rep);                         \
+        cudaEventRecord(e1);                                                               \
+        cudaEventSynchronize(e1);                                                          \
+        float ms;                                                                          \
+        cudaEventElapsedTime(&ms, e0, e1);                                                 \
+        if (rep) printf("HOST-MAPPED 2^28 x8B  ctas %4d  variant %d: %.3f ms  %.3f Gsamples/s\n", \
+                        blocks, V, ms, loads / ms / 1e6);                                  \
+    }
+                    RUNH(0) RUNH(3)
+                }
+            }
+            cudaFreeHost(h);
+        } else {
+            printf("no mapped host memory\n");
         }
     }
     cudaError_t e = cudaDeviceSynchronize();
