@@ -515,3 +515,18 @@ def test_unusual_shapes_match_oracle(dims, k, prec, rng):
                log_counts=[x[2:] for x in ref.log])
     _check_report(rep, exp, 1e-9 if prec == "fp64" else 1e-4,
                   amp_atol_rel=1e-13 if prec == "fp64" else 0.0)
+
+
+@pytest.mark.parametrize("dims,k_cap", [((1024, 2048), 64), ((512, 512), 16), ((256, 256), 8),
+                                        ((64, 64, 64), 16)])
+def test_tiny_k_cap_overflows_cleanly(dims, k_cap):
+    """Every kernel family with a recovered-set capacity far below K: the
+    overflow is reported per instance and nothing faults."""
+    f, a = W.reference_generate(dims, 4 * k_cap, 3)
+    cube = torch.as_tensor(W.synthesize_np(dims, f, a).astype(np.complex64))[None].to(DEV)
+    cfg = P.FpsSftConfig(max_iterations=6, **G.PROFILES["P32"])
+    for mode in ("auto", "cta"):
+        res = P.fps_sft_batch(cube, cfg, k_cap=k_cap, mode=mode)
+        torch.cuda.synchronize()
+        assert res.terminated_by.item() == 3
+        assert 0 <= res.count.item() <= k_cap
