@@ -25,8 +25,14 @@
 #ifndef FPSSFT_PREFETCH_FROM
 #define FPSSFT_PREFETCH_FROM 4  // L2-prefetch iteration t+1 from iteration t >= this on
 #endif
+#ifndef FPSSFT_TEAM_GATHER_NC
+#define FPSSFT_TEAM_GATHER_NC FPSSFT_GATHER_NC
+#endif
+#ifndef FPSSFT_WARP_NT
+#define FPSSFT_WARP_NT 256  // largest CTA of the warp kernel (FPSSFT_WARP_NT / 32 instances)
+#endif
 #ifndef FPSSFT_WARP_MINB
-#define FPSSFT_WARP_MINB 2  // CTAs of 256 threads per SM the warp kernel's registers allow
+#define FPSSFT_WARP_MINB 2  // CTAs of FPSSFT_WARP_NT threads per SM its registers must allow
 #endif
 
 namespace fpssft {
@@ -496,7 +502,7 @@ __device__ __forceinline__ void hash16_insert(unsigned short *hash, int H, int k
 // LC / DC: compile-time line length and dimensionality (0 = runtime), so the
 // benchmark shapes get fully unrolled gathers, FFTs and bin loops.
 template <class R, int LC, int DC>
-__global__ void __launch_bounds__(256, FPSSFT_WARP_MINB) recover_warp_kernel(const float2 *__restrict__ cubes,
+__global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp_kernel(const float2 *__restrict__ cubes,
                                                            long long batch, long long batch_stride,
                                                            Geo g_in, Knobs kn,
                                                            const int *__restrict__ schedule,
@@ -569,7 +575,14 @@ __global__ void __launch_bounds__(256, FPSSFT_WARP_MINB) recover_warp_kernel(con
         // (1) gather + (2) DFT of the D+1 lines           driver.py:146-154
         R my_energy;
         if constexpr (sizeof(R) == 4) {
-            gather_lines_async<LC>(spec, cube, g, al, ta, lane, 32);
+            bool reg_gather = false;
+            // register gather for short lines (config 3: 1.2% faster), cp.async
+            // for L >= 256 (config 2: 1% faster) -- measured, profiles/README.md
+            if constexpr (FPSSFT_GATHER_NC && LC != 0 && LC < 256 && DC != 0) {
+                reg_gather = g.off32;
+                if (reg_gather) gather_lines_nc<LC, DC>(spec, cube, g, al, ta, lane);
+            }
+            if (!reg_gather) gather_lines_async<LC>(spec, cube, g, al, ta, lane, 32);
             if (it + 1 < kn.t_max) {
 #pragma unroll
                 for (int k = 0; k < MAXD; ++k) {
@@ -1518,6 +1531,7 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
             const long long reg_warps = 65536 / (regs * 32);
             int best_w = 0;
             for (int w : {8, 4, 2, 1}) {
+                if (32 * w > FPSSFT_WARP_NT) continue;
                 const long long smem = (long long)wl.roots + w * (long long)wl.per_warp;
                 if (smem > SMEM_PER_CTA) continue;
                 const long long ctas = std::min<long long>(

@@ -327,6 +327,69 @@ __device__ __forceinline__ void gather_lines_async(cpx<float> *spec,
             if (k < D) cp_async8(spec + (k + 1) * L + l, cube + base + delta[k]);
     }
 }
+// Register gather for compile-time shapes (LC, DC, NTC threads): batches of
+// up to 24 samples per thread are all in flight before the first shared
+// store.  ld.global.nc.L1::no_allocate keeps the random lines out of L1 --
+// cp.async.ca stages every sample through an L1 line, and with most of the
+// SM's 256 KB carved out as shared memory those in-flight lines back up the
+// load pipe.
+#ifndef FPSSFT_GATHER_NC
+#define FPSSFT_GATHER_NC 1
+#endif
+__device__ __forceinline__ float2 ld_nc8(const float2 *p) {
+    float2 v;
+#if FPSSFT_GATHER_L2_64B
+    asm("ld.global.nc.L1::no_allocate.L2::64B.v2.f32 {%0, %1}, [%2];"
+        : "=f"(v.x), "=f"(v.y) : "l"(p));
+#else
+    asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+#endif
+    return v;
+}
+template <int LC, int DC, int NTC = 32>
+__device__ __forceinline__ void gather_lines_nc(cpx<float> *spec, const float2 *__restrict__ cube,
+                                                const Geo &g, const int *al, const int *ta,
+                                                int tid) {
+    constexpr int NL = DC + 1, J = (LC + NTC - 1) / NTC;
+    constexpr int JB = 24 / NL < J ? 24 / NL : J;
+    int n[DC], step[DC];
+#pragma unroll
+    for (int k = 0; k < DC; ++k) {
+        n[k] = (int)fastmod((unsigned)al[k] * (unsigned)tid + (unsigned)ta[k], g.magic[k],
+                            (unsigned)g.N[k]);
+        step[k] = (int)fastmod((unsigned)al[k] * (unsigned)NTC, g.magic[k], (unsigned)g.N[k]);
+    }
+#pragma unroll
+    for (int j0 = 0; j0 < J; j0 += JB) {
+        float2 v[JB][NL];
+#pragma unroll
+        for (int jj = 0; jj < JB; ++jj) {
+            const int l = tid + NTC * (j0 + jj);
+            if (j0 + jj < J && (LC % NTC == 0 || l < LC)) {
+                int base = 0;
+#pragma unroll
+                for (int k = 0; k < DC; ++k) base += n[k] * g.stride32[k];
+                v[jj][0] = ld_nc8(cube + base);
+#pragma unroll
+                for (int k = 0; k < DC; ++k) {
+                    // tau + e_k: the next index along axis k, wrapping
+                    const int d = (n[k] + 1 == g.N[k]) ? -n[k] * g.stride32[k] : g.stride32[k];
+                    v[jj][k + 1] = ld_nc8(cube + (base + d));
+                    n[k] += step[k];
+                    if (n[k] >= g.N[k]) n[k] -= g.N[k];
+                }
+            }
+        }
+#pragma unroll
+        for (int jj = 0; jj < JB; ++jj) {
+            const int l = tid + NTC * (j0 + jj);
+            if (j0 + jj < J && (LC % NTC == 0 || l < LC)) {
+#pragma unroll
+                for (int i = 0; i < NL; ++i) spec[padi<true>(i * LC + l)] = {v[jj][i].x, v[jj][i].y};
+            }
+        }
+    }
+}
 // L2 prefetch of a future iteration's line samples (compile-time line
 // length, one warp): the same addresses as gather_lines_async, no data moved
 // on chip.

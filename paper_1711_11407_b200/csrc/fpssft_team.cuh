@@ -123,7 +123,12 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
 
         // (1) gather + (2) DFT                                 driver.py:146-154
         if constexpr (sizeof(R) == 4) {
-            gather_lines_async<LC, NT>(spec, cube, g, al, ta, tid, NT);
+            bool reg_gather = false;
+            if constexpr (FPSSFT_TEAM_GATHER_NC && DC != 0) {
+                reg_gather = g.off32;
+                if (reg_gather) gather_lines_nc<LC, DC, NT>(spec, cube, g, al, ta, tid);
+            }
+            if (!reg_gather) gather_lines_async<LC, NT>(spec, cube, g, al, ta, tid, NT);
         } else {
             gather_lines<R, PAD>(spec, cube, g, al, ta, tid, NT);
         }
