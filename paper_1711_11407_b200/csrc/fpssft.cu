@@ -452,7 +452,9 @@ struct WarpLayout {
 
 __host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, int cs) {
     WarpLayout y;
-    const size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // room for padi()
+    size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // room for padi()
+    if (warp_stage16(D, L, cs) && spec_bytes < (size_t)(D + 1) * L * 16)
+        spec_bytes = (size_t)(D + 1) * L * 16;  // 16-byte staging slots (gather_lines_cg16)
     const size_t sort_bytes = 1024 + (size_t)k_cap * 4;
     size_t o = 0;
     y.H = 2 * k_cap;
@@ -574,6 +576,8 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
 
         // (1) gather + (2) DFT of the D+1 lines           driver.py:146-154
         R my_energy;
+        bool staged = false;
+        unsigned par = 0, dup = 0;
         if constexpr (sizeof(R) == 4) {
             bool reg_gather = false;
             // register gather for short lines (config 3: 1.2% faster), cp.async
@@ -582,7 +586,12 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
                 reg_gather = g.off32;
                 if (reg_gather) gather_lines_nc<LC, DC>(spec, cube, g, al, ta, lane);
             }
-            if (!reg_gather) gather_lines_async<LC>(spec, cube, g, al, ta, lane, 32);
+            if constexpr (warp_stage16(DC, LC, 8)) {
+                staged = g.off32;
+                if (staged)
+                    par = gather_lines_cg16<LC, DC>((float4 *)spec, cube, g, al, ta, lane, &dup);
+            }
+            if (!reg_gather && !staged) gather_lines_async<LC>(spec, cube, g, al, ta, lane, 32);
             if (it + 1 < kn.t_max) {
 #pragma unroll
                 for (int k = 0; k < MAXD; ++k) {
@@ -599,6 +608,12 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             }
             cp_async_wait_all();
             __syncwarp();
+            if constexpr (warp_stage16(DC, LC, 8)) {
+                if (staged) {
+                    compact_stage16<LC, DC + 1>(spec, par, dup, lane);
+                    __syncwarp();
+                }
+            }
             my_energy = (LC == 0 && kn.noise_coef > 0) ? line_energy(spec, nl * L, lane, 32) : (R)0;
         } else {
             my_energy = gather_lines<R, PAD>(spec, cube, g, al, ta, lane, 32);
@@ -1530,8 +1545,10 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
             const int regs = (warp_kernel_regs(gw, precision) + 7) / 8 * 8;
             const long long reg_warps = 65536 / (regs * 32);
             int best_w = 0;
-            for (int w : {8, 4, 2, 1}) {
+            const char *wenv = std::getenv("FPSSFT_WARP_W");  // occupancy experiments
+            for (int w : {8, 7, 6, 5, 4, 3, 2, 1}) {
                 if (32 * w > FPSSFT_WARP_NT) continue;
+                if (wenv ? std::atoi(wenv) != w : (w & (w - 1)) != 0) continue;
                 const long long smem = (long long)wl.roots + w * (long long)wl.per_warp;
                 if (smem > SMEM_PER_CTA) continue;
                 const long long ctas = std::min<long long>(
@@ -1626,6 +1643,27 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
     return FPSSFT_OK;
 }
 
+// Shared-memory carveout for a launch: only as much of the SM's unified
+// L1/shared memory as the CTAs that will actually be co-resident need, the
+// rest stays L1.  The line gathers are random 8-byte reads whose in-flight
+// misses live in L1: config 3 (128 CTAs, one per SM) runs 1.30 ms with the
+// driver's default 228 KB carveout (28 KB of L1) and 1.07 ms with 132 KB.
+void set_carveout(const void *kernel, long long grid, int threads, size_t smem) {
+    int dev = 0, sms = 0, occ = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess ||
+        sms <= 0 || occ <= 0) {
+        cudaGetLastError();
+        return;
+    }
+    const long long per_sm = std::min<long long>(occ, (grid + sms - 1) / sms);
+    const long long need = per_sm * ((long long)smem + SMEM_RESERVED);
+    const int pct = (int)std::min<long long>(100, (need * 100 + SMEM_PER_SM - 1) / SMEM_PER_SM);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaGetLastError();  // a hint: never an error
+}
+
 template <class R>
 int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
                 const Knobs &kn, int want_mode, const int32_t *schedule,
@@ -1642,6 +1680,7 @@ int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
                                  (int)lp.smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recover_team_kernel)");
         if (batch == 0) return FPSSFT_OK;
+        set_carveout((const void *)kernel, batch, lp.threads, lp.smem);
         kernel<<<(unsigned)batch, lp.threads, lp.smem, st>>>(
             (const float2 *)cubes, (long long)batch_stride, g, kn, schedule, sched_index, n_sched,
             o);
@@ -1655,6 +1694,7 @@ int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recover_warp_kernel)");
         if (batch == 0) return FPSSFT_OK;
         const long long grid = (batch + lp.per_cta - 1) / lp.per_cta;
+        set_carveout((const void *)kernel, grid, lp.threads, lp.smem);
         kernel<<<(unsigned)grid, lp.threads, lp.smem, st>>>(
             (const float2 *)cubes, (long long)batch, (long long)batch_stride, g, kn, schedule,
             sched_index, n_sched, o);
@@ -1664,6 +1704,7 @@ int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
                              (int)lp.smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recover_kernel)");
     if (batch == 0) return FPSSFT_OK;
+    set_carveout((const void *)recover_kernel<R>, batch, lp.threads, lp.smem);
     recover_kernel<R><<<(unsigned)batch, lp.threads, lp.smem, st>>>(
         (const float2 *)cubes, (long long)batch_stride, g, kn, schedule, sched_index, n_sched, o);
     return check_launch("recover_kernel");

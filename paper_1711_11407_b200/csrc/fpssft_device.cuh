@@ -390,6 +390,101 @@ __device__ __forceinline__ void gather_lines_nc(cpx<float> *spec, const float2 *
         }
     }
 }
+// 16-byte gather that bypasses L1 (compile-time shapes, one warp): each
+// sample is fetched as the aligned 16-byte chunk holding it with
+// cp.async.cg into a 16-byte staging slot; bit t of the returned mask says
+// which half is the sample (t = line * LC/32 + j for l = lane + 32 j).  The
+// cp.async.ca 8-byte form stages every in-flight sample in an L1 line, and L1
+// is what the shared-memory carveout leaves (92 KB at config 2's 162 KB of
+// shared memory per SM), which caps the misses in flight.
+#ifndef FPSSFT_GATHER_CG
+#define FPSSFT_GATHER_CG 1
+#endif
+__host__ __device__ constexpr bool warp_stage16(int D, int L, int cs) {
+    return FPSSFT_GATHER_CG && cs == 8 && L == 256 && D == 2;
+}
+__device__ __forceinline__ void cp_async16_cg(void *smem_dst, const void *gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ unsigned stage16(float4 *dst, const float2 *src, int bit) {
+    const unsigned long long a = (unsigned long long)src;
+    cp_async16_cg(dst, (const void *)(a & ~15ull));
+    return (unsigned)((a >> 3) & 1ull) << bit;
+}
+template <int LC, int DC>
+__device__ __forceinline__ unsigned gather_lines_cg16(float4 *stage, const float2 *__restrict__ cube,
+                                                      const Geo &g, const int *al, const int *ta,
+                                                      int lane, unsigned *dup) {
+    constexpr int J = LC / 32;
+    static_assert(LC % 32 == 0 && (DC + 1) * J <= 32, "one mask bit per staged sample");
+    int n[DC], step[DC];
+#pragma unroll
+    for (int k = 0; k < DC; ++k) {
+        n[k] = (int)fastmod((unsigned)al[k] * (unsigned)lane + (unsigned)ta[k], g.magic[k],
+                            (unsigned)g.N[k]);
+        step[k] = (int)fastmod((unsigned)al[k] * 32u, g.magic[k], (unsigned)g.N[k]);
+    }
+    unsigned par = 0, dp = 0;
+    const bool unit_last = g.stride32[DC - 1] == 1;
+#pragma unroll 4
+    for (int j = 0; j < J; ++j) {
+        const int l = lane + 32 * j;
+        int base = 0;
+#pragma unroll
+        for (int k = 0; k < DC; ++k) base += n[k] * g.stride32[k];
+        const unsigned p0 = stage16(stage + l, cube + base, j);
+        par |= p0;
+#pragma unroll
+        for (int k = 0; k < DC; ++k) {
+            const bool wrap = n[k] + 1 == g.N[k];
+            const int d = wrap ? -n[k] * g.stride32[k] : g.stride32[k];
+            if (k == DC - 1 && unit_last && !wrap && p0 == 0u) {
+                // tau + e_last is the upper half of tau's own chunk
+                dp |= 1u << j;
+            } else {
+                par |= stage16(stage + (k + 1) * LC + l, cube + (base + d), (k + 1) * J + j);
+            }
+            n[k] += step[k];
+            if (n[k] >= g.N[k]) n[k] -= g.N[k];
+        }
+    }
+    *dup = dp;
+    return par;
+}
+// Staging slots -> padded spectra, in place (the spectra start at the
+// staging base): flat sample f = 32 t + lane goes from 16-byte slot f to
+// complex padi(f) (byte ~8.5 f), i.e. into slots < 0.54 f that every lane has
+// already read, so one warp barrier per batch between its reads and writes.
+// Samples of the last-axis line that shared tau's chunk (bit j of dup) are
+// carried in registers from the line-0 step: same lane, same j.
+template <int LC, int NL>
+__device__ __forceinline__ void compact_stage16(cpx<float> *spec, unsigned par, unsigned dup,
+                                                int lane) {
+    constexpr int J = LC / 32, T = NL * J, B = J;
+    const float4 *stage = (const float4 *)spec;
+    float2 hold[J];
+#pragma unroll
+    for (int t0 = 0; t0 < T; t0 += B) {
+        float2 v[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const int t = t0 + b, i = t / J, j = t % J;
+            if (i == NL - 1 && ((dup >> j) & 1u)) {
+                v[b] = hold[j];
+            } else {
+                const float4 q = stage[32 * t + lane];
+                const bool hi = (par >> t) & 1u;
+                v[b] = hi ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
+                if (i == 0) hold[j] = make_float2(q.z, q.w);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int b = 0; b < B; ++b) spec[padi<true>(32 * (t0 + b) + lane)] = {v[b].x, v[b].y};
+    }
+}
 // L2 prefetch of a future iteration's line samples (compile-time line
 // length, one warp): the same addresses as gather_lines_async, no data moved
 // on chip.
