@@ -453,7 +453,7 @@ struct WarpLayout {
 __host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, int cs) {
     WarpLayout y;
     size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // room for padi()
-    if (warp_stage16(D, L, cs) && spec_bytes < (size_t)(D + 1) * L * 16)
+    if (stage16_ok(D, L, cs, 32) && spec_bytes < (size_t)(D + 1) * L * 16)
         spec_bytes = (size_t)(D + 1) * L * 16;  // 16-byte staging slots (gather_lines_cg16)
     const size_t sort_bytes = 1024 + (size_t)k_cap * 4;
     size_t o = 0;
@@ -582,12 +582,13 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             bool reg_gather = false;
             // register gather for short lines (config 3: 1.2% faster), cp.async
             // for L >= 256 (config 2: 1% faster) -- measured, profiles/README.md
-            if constexpr (FPSSFT_GATHER_NC && LC != 0 && LC < 256 && DC != 0) {
+            if constexpr (FPSSFT_GATHER_NC && LC != 0 && LC < 256 && DC != 0 &&
+                          !stage16_ok(DC, LC, 8, 32)) {
                 reg_gather = g.off32;
                 if (reg_gather) gather_lines_nc<LC, DC>(spec, cube, g, al, ta, lane);
             }
-            if constexpr (warp_stage16(DC, LC, 8)) {
-                staged = g.off32;
+            if constexpr (LC != 0 && stage16_ok(DC, LC, 8, 32)) {
+                staged = g.off32 && !reg_gather;
                 if (staged)
                     par = gather_lines_cg16<LC, DC>((float4 *)spec, cube, g, al, ta, lane, &dup);
             }
@@ -608,9 +609,9 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             }
             cp_async_wait_all();
             __syncwarp();
-            if constexpr (warp_stage16(DC, LC, 8)) {
+            if constexpr (LC != 0 && stage16_ok(DC, LC, 8, 32)) {
                 if (staged) {
-                    compact_stage16<LC, DC + 1>(spec, par, dup, lane);
+                    compact_stage16<LC, DC + 1, 32, WarpTeam>(spec, par, dup, lane);
                     __syncwarp();
                 }
             }

@@ -400,8 +400,18 @@ __device__ __forceinline__ void gather_lines_nc(cpx<float> *spec, const float2 *
 #ifndef FPSSFT_GATHER_CG
 #define FPSSFT_GATHER_CG 1
 #endif
-__host__ __device__ constexpr bool warp_stage16(int D, int L, int cs) {
-    return FPSSFT_GATHER_CG && cs == 8 && L == 256 && D == 2;
+// Staging applies to float spectra with compile-time shapes whose NL x J
+// samples per thread fit one 32-bit mask (J = L / nt samples per line).
+#ifndef FPSSFT_STAGE16_TEAM
+#define FPSSFT_STAGE16_TEAM 1
+#endif
+#ifndef FPSSFT_STAGE16_W64
+#define FPSSFT_STAGE16_W64 1
+#endif
+__host__ __device__ constexpr bool stage16_ok(int D, int L, int cs, int nt) {
+    return FPSSFT_GATHER_CG && cs == 8 && D >= 2 && L % nt == 0 && (D + 1) * (L / nt) <= 32 &&
+           (nt == 32 ? ((L == 256 && D == 2) || (FPSSFT_STAGE16_W64 && L == 64 && D == 3))
+                      : FPSSFT_STAGE16_TEAM != 0);
 }
 __device__ __forceinline__ void cp_async16_cg(void *smem_dst, const void *gsrc) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -413,24 +423,28 @@ __device__ __forceinline__ unsigned stage16(float4 *dst, const float2 *src, int 
     cp_async16_cg(dst, (const void *)(a & ~15ull));
     return (unsigned)((a >> 3) & 1ull) << bit;
 }
-template <int LC, int DC>
+// Thread tid stages l = tid + NTC j of every line into slot line * LC + l;
+// returns the half-select mask (bit line * J + j) and in *dup the samples of
+// the last-axis line (unit stride, no wrap) that sit in the upper half of
+// tau's own chunk and so need no request of their own.
+template <int LC, int DC, int NTC = 32>
 __device__ __forceinline__ unsigned gather_lines_cg16(float4 *stage, const float2 *__restrict__ cube,
                                                       const Geo &g, const int *al, const int *ta,
-                                                      int lane, unsigned *dup) {
-    constexpr int J = LC / 32;
-    static_assert(LC % 32 == 0 && (DC + 1) * J <= 32, "one mask bit per staged sample");
+                                                      int tid, unsigned *dup) {
+    constexpr int J = LC / NTC;
+    static_assert(LC % NTC == 0 && (DC + 1) * J <= 32, "one mask bit per staged sample");
     int n[DC], step[DC];
 #pragma unroll
     for (int k = 0; k < DC; ++k) {
-        n[k] = (int)fastmod((unsigned)al[k] * (unsigned)lane + (unsigned)ta[k], g.magic[k],
+        n[k] = (int)fastmod((unsigned)al[k] * (unsigned)tid + (unsigned)ta[k], g.magic[k],
                             (unsigned)g.N[k]);
-        step[k] = (int)fastmod((unsigned)al[k] * 32u, g.magic[k], (unsigned)g.N[k]);
+        step[k] = (int)fastmod((unsigned)al[k] * (unsigned)NTC, g.magic[k], (unsigned)g.N[k]);
     }
     unsigned par = 0, dp = 0;
     const bool unit_last = g.stride32[DC - 1] == 1;
 #pragma unroll 4
     for (int j = 0; j < J; ++j) {
-        const int l = lane + 32 * j;
+        const int l = tid + NTC * j;
         int base = 0;
 #pragma unroll
         for (int k = 0; k < DC; ++k) base += n[k] * g.stride32[k];
@@ -440,12 +454,10 @@ __device__ __forceinline__ unsigned gather_lines_cg16(float4 *stage, const float
         for (int k = 0; k < DC; ++k) {
             const bool wrap = n[k] + 1 == g.N[k];
             const int d = wrap ? -n[k] * g.stride32[k] : g.stride32[k];
-            if (k == DC - 1 && unit_last && !wrap && p0 == 0u) {
-                // tau + e_last is the upper half of tau's own chunk
-                dp |= 1u << j;
-            } else {
+            if (k == DC - 1 && unit_last && !wrap && p0 == 0u)
+                dp |= 1u << j;  // tau + e_last: the upper half of tau's chunk
+            else
                 par |= stage16(stage + (k + 1) * LC + l, cube + (base + d), (k + 1) * J + j);
-            }
             n[k] += step[k];
             if (n[k] >= g.N[k]) n[k] -= g.N[k];
         }
@@ -454,35 +466,34 @@ __device__ __forceinline__ unsigned gather_lines_cg16(float4 *stage, const float
     return par;
 }
 // Staging slots -> padded spectra, in place (the spectra start at the
-// staging base): flat sample f = 32 t + lane goes from 16-byte slot f to
-// complex padi(f) (byte ~8.5 f), i.e. into slots < 0.54 f that every lane has
-// already read, so one warp barrier per batch between its reads and writes.
-// Samples of the last-axis line that shared tau's chunk (bit j of dup) are
-// carried in registers from the line-0 step: same lane, same j.
-template <int LC, int NL>
+// staging base), one line per batch.  Sample f = NTC t + tid moves from
+// 16-byte slot f (staged by this same thread) to complex padi(f), byte
+// ~8.5 f: inside slots < 0.54 f, all read by the end of f's batch -- so one
+// team barrier per batch, between its reads and its writes.  Last-axis
+// samples flagged in dup are carried in registers from the line-0 batch.
+template <int LC, int NL, int NTC, class Team>
 __device__ __forceinline__ void compact_stage16(cpx<float> *spec, unsigned par, unsigned dup,
-                                                int lane) {
-    constexpr int J = LC / 32, T = NL * J, B = J;
+                                                int tid) {
+    constexpr int J = LC / NTC;
     const float4 *stage = (const float4 *)spec;
     float2 hold[J];
 #pragma unroll
-    for (int t0 = 0; t0 < T; t0 += B) {
-        float2 v[B];
+    for (int i = 0; i < NL; ++i) {
+        float2 v[J];
 #pragma unroll
-        for (int b = 0; b < B; ++b) {
-            const int t = t0 + b, i = t / J, j = t % J;
+        for (int j = 0; j < J; ++j) {
+            const int t = i * J + j;
             if (i == NL - 1 && ((dup >> j) & 1u)) {
-                v[b] = hold[j];
+                v[j] = hold[j];
             } else {
-                const float4 q = stage[32 * t + lane];
-                const bool hi = (par >> t) & 1u;
-                v[b] = hi ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
+                const float4 q = stage[NTC * t + tid];
+                v[j] = ((par >> t) & 1u) ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
                 if (i == 0) hold[j] = make_float2(q.z, q.w);
             }
         }
-        __syncwarp();
+        Team::sync();
 #pragma unroll
-        for (int b = 0; b < B; ++b) spec[padi<true>(32 * (t0 + b) + lane)] = {v[b].x, v[b].y};
+        for (int j = 0; j < J; ++j) spec[padi<true>(NTC * (i * J + j) + tid)] = {v[j].x, v[j].y};
     }
 }
 // L2 prefetch of a future iteration's line samples (compile-time line

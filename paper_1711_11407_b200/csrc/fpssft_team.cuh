@@ -26,7 +26,9 @@ struct TeamLayout {
 
 __host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, int cs, int nt) {
     TeamLayout y;
-    const size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // padi() layout
+    size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // padi() layout
+    if (stage16_ok(D, L, cs, nt) && spec_bytes < (size_t)(D + 1) * L * 16)
+        spec_bytes = (size_t)(D + 1) * L * 16;  // 16-byte staging slots (gather_lines_cg16)
     const size_t sort_bytes = 1024 + (size_t)k_cap * 4;
     size_t o = 0;
     y.H = 2 * k_cap;
@@ -122,13 +124,19 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
         it_run = it + 1;
 
         // (1) gather + (2) DFT                                 driver.py:146-154
+        bool staged = false;
+        unsigned par = 0, dup = 0;
         if constexpr (sizeof(R) == 4) {
             bool reg_gather = false;
-            if constexpr (FPSSFT_TEAM_GATHER_NC && DC != 0) {
+            if constexpr (stage16_ok(DC, LC, 8, NT)) {
+                staged = g.off32;
+                if (staged)
+                    par = gather_lines_cg16<LC, DC, NT>((float4 *)spec, cube, g, al, ta, tid, &dup);
+            } else if constexpr (FPSSFT_TEAM_GATHER_NC && DC != 0) {
                 reg_gather = g.off32;
                 if (reg_gather) gather_lines_nc<LC, DC, NT>(spec, cube, g, al, ta, tid);
             }
-            if (!reg_gather) gather_lines_async<LC, NT>(spec, cube, g, al, ta, tid, NT);
+            if (!reg_gather && !staged) gather_lines_async<LC, NT>(spec, cube, g, al, ta, tid, NT);
         } else {
             gather_lines<R, PAD>(spec, cube, g, al, ta, tid, NT);
         }
@@ -141,6 +149,9 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
             // (no L2 prefetch here: measured slower on config 5, 42.3 vs 38.2 ms)
         }
         if constexpr (sizeof(R) == 4) cp_async_wait_all();
+        if constexpr (stage16_ok(DC, LC, (int)sizeof(cpx<R>), NT)) {
+            if (staged) compact_stage16<LC, nl, NT, BlockTeam>((cpx<float> *)spec, par, dup, tid);
+        }
         __syncthreads();
         const R my_energy = fft_static<R, LC, nl, NT, BlockTeam>(spec, roots, tid);
         R noise_floor = (R)0;
