@@ -1549,7 +1549,7 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
             const char *wenv = std::getenv("FPSSFT_WARP_W");  // occupancy experiments
             for (int w : {8, 7, 6, 5, 4, 3, 2, 1}) {
                 if (32 * w > FPSSFT_WARP_NT) continue;
-                if (wenv ? std::atoi(wenv) != w : (w & (w - 1)) != 0) continue;
+                if (wenv && std::atoi(wenv) != w) continue;
                 const long long smem = (long long)wl.roots + w * (long long)wl.per_warp;
                 if (smem > SMEM_PER_CTA) continue;
                 const long long ctas = std::min<long long>(
