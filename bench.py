@@ -61,13 +61,14 @@ def _peaks():
 
 
 def _probe_rate():
-    """Random-line fetch rate of this GPU measured by tools/gather_probe.cu
-    (variant 0: plain 8-byte loads, 2^28-element array, all SMs)."""
+    """Random 64-byte-segment fetch rate of this GPU measured by
+    tools/gather_probe.cu (variant 2: 8-byte loads with the .L2::64B fetch
+    size, 2^28-element array, all SMs)."""
     import re
 
     try:
         for line in open(os.path.join(ROOT, "profiles", "r01_gather_probe.txt")):
-            m = re.search(r"2\^28 x8B\s+ctas\s+1184\s+variant 0:.*?([0-9.]+) Gsamples/s", line)
+            m = re.search(r"2\^28 x8B\s+ctas\s+1184\s+variant 2:.*?([0-9.]+) Gsamples/s", line)
             if m:
                 return float(m.group(1)) * 1e9
     except OSError:
@@ -75,10 +76,12 @@ def _probe_rate():
     return None
 
 
-def _lines_per_launch(shape, schedule, iterations, sched_index=None):
-    """Distinct 128-byte lines the gathers of one launch touch: per
-    iteration, the (D+1) L sample offsets of the lines (row-major complex64
-    cube, 16 samples per line), counted once per instance that runs it."""
+def _segments_per_launch(shape, schedule, iterations, sched_index=None, seg=8):
+    """Distinct 64-byte DRAM segments (seg = 8 complex64 samples) the gathers
+    of one launch touch: per iteration, the (D+1) L sample offsets of the
+    lines (row-major cube), counted once per instance that runs it.  With the
+    .L2::64B fetch size a miss moves one such segment (config 2: 6.7 M
+    segments, 427 MB of DRAM reads under ncu)."""
     dims = np.asarray(shape.dims, np.int64)
     strides = np.cumprod(np.concatenate([[1], dims[::-1][:-1]]))[::-1]
     L = shape.line_len
@@ -97,7 +100,7 @@ def _lines_per_launch(shape, schedule, iterations, sched_index=None):
                 if i:
                     tau[i - 1] = (tau[i - 1] + 1) % dims[i - 1]
                 offs.append((((l * al + tau) % dims) * strides).sum(1))
-            per_t.append(len(np.unique(np.concatenate(offs) // 16)))
+            per_t.append(len(np.unique(np.concatenate(offs) // seg)))
         per_t = np.asarray(per_t)
         total += int(sum(per_t[:n].sum() for n in its))
     return total
@@ -399,13 +402,14 @@ def main():
                 "kernel_ms": rec_ms,
                 "note": "achieved = sum(samples_used)*8 B gathered per launch / mean launch time"}
     probe = _probe_rate()
-    lines = _lines_per_launch(shape, runner.schedule_host, iters)
+    segs = _segments_per_launch(shape, runner.schedule_host, iters)
     roofline["gather"] = {
-        "lines_per_launch": lines, "achieved_lines_per_s": lines / (rec_ms / 1e3),
-        "peak_lines_per_s": probe,
-        "frac": (lines / (rec_ms / 1e3) / probe) if probe else None,
-        "note": "random 128-byte line fetches: the measured bound of an isolated-8-byte "
-                "gather (tools/gather_probe.cu, profiles/r01_gather_probe.txt)"}
+        "segments_per_launch": segs, "achieved_segments_per_s": segs / (rec_ms / 1e3),
+        "peak_segments_per_s": probe,
+        "frac": (segs / (rec_ms / 1e3) / probe) if probe else None,
+        "note": "distinct random 64-byte DRAM segments the line gathers touch vs the measured "
+                "random-fetch rate of this B200 (tools/gather_probe.cu variant 2, "
+                "profiles/r01_gather_probe.txt): the bound of a scattered-sample gather"}
     if synth:
         s_ms = sum(synth_ms) / args.steps
         wbytes = cubes.numel() * cubes.element_size()
