@@ -104,6 +104,20 @@ int fpssft_line_spectra(const void *cubes, int64_t batch, int64_t batch_stride,
                         int32_t per_instance, void *spectra, int32_t precision, void *stream);
 
 /*
+ * Line samples only, into global memory (extract_line for the D+1 offsets,
+ * lines.py:36-64 + core.py:236-238) -- the first half of
+ * fpssft_line_spectra for lines too long to transform in one CTA's shared
+ * memory (the imaging shape 512 x 576, L = 4608, in float64), followed by
+ * fpssft_dft_forward.  cubes: complex64 (cube_precision FPSSFT_F32) or
+ * complex128 (FPSSFT_F64) row-major with shape->strides; lines: [B, D+1, L]
+ * complex of `precision`.  B <= 65535.
+ */
+int fpssft_gather_lines(const void *cubes, int32_t cube_precision, int64_t batch,
+                        int64_t batch_stride, const fpssft_shape *shape,
+                        const int32_t *alpha_tau, int32_t per_instance, void *lines,
+                        int32_t precision, void *stream);
+
+/*
  * Batched 1/L-normalised forward DFT (transform.py:17-22, dft_forward).
  * lines/out: [B, L] complex64 (F32) or complex128 (F64); may alias.
  */

@@ -101,7 +101,11 @@ class SparseSpectrum:
         """Build from device output already validated, sorted and unique."""
         self = cls.__new__(cls)
         self.shape = shape
-        self.entries = {tuple(int(v) for v in f): complex(a) for f, a in zip(freqs, amps)}
+        freqs = np.asarray(freqs, np.int64).reshape(-1, shape.ndim)
+        amps = np.asarray(amps, np.complex128).reshape(-1)
+        self.entries = dict(zip(map(tuple, freqs.tolist()), amps.tolist()))
+        self.__dict__["freq_array"] = freqs  # cached_property values, already at hand
+        self.__dict__["amp_array"] = amps
         return self
 
     @classmethod

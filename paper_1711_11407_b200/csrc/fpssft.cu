@@ -1129,15 +1129,18 @@ __global__ void __launch_bounds__(1024, 1) dft_kernel(const cpx<R> *__restrict__
     for (int l = threadIdx.x; l < g.L; l += blockDim.x) out[off + l] = x[l];
 }
 
-template <class R>
+// GLOBAL: the spectra stay in global memory (lines too long for shared
+// memory, e.g. the 512 x 576 imaging shape, L = 4608, in float64); only the
+// root table is staged.
+template <class R, bool GLOBAL = false>
 __global__ void __launch_bounds__(1024, 1) decode_kernel(const cpx<R> *__restrict__ spectra, Geo g,
                                                       const int *__restrict__ alpha_tau,
                                                       int per_instance, Knobs kn, double floor,
                                                       int *status, int *freqs, double *amps,
                                                       int *n_candidates) {
     extern __shared__ __align__(16) unsigned char sm[];
-    cpx<R> *spec = (cpx<R> *)sm;
-    cpx<R> *roots = spec + (size_t)g.nlines * g.L;
+    cpx<R> *spec = GLOBAL ? nullptr : (cpx<R> *)sm;
+    cpx<R> *roots = GLOBAL ? (cpx<R> *)sm : spec + (size_t)g.nlines * g.L;
     int *ired = (int *)(roots + g.L);
     const int inst = blockIdx.x, D = g.D, L = g.L;
     const int *at = alpha_tau + (per_instance ? (long long)inst * 2 * D : 0);
@@ -1151,10 +1154,12 @@ __global__ void __launch_bounds__(1024, 1) decode_kernel(const cpx<R> *__restric
     const cpx<R> *src = spectra + (long long)inst * g.nlines * L;
     R my_e = (R)0;
     for (int e = threadIdx.x; e < g.nlines * L; e += blockDim.x) {
-        spec[e] = src[e];
-        my_e += spec[e].re * spec[e].re + spec[e].im * spec[e].im;
+        const cpx<R> v = src[e];
+        if (!GLOBAL) spec[e] = v;
+        my_e += v.re * v.re + v.im * v.im;
     }
     __syncthreads();
+    const cpx<R> *sp = GLOBAL ? src : spec;
     R fl = (R)floor;
     if (sizeof(R) == 4 && kn.noise_coef > 0)  // sum |x|^2 = L sum |S|^2 (Parseval)
         fl = max(fl, (R)kn.noise_coef * sqrt((R)L * block_sum(my_e, (R *)(ired + 32))));
@@ -1162,7 +1167,7 @@ __global__ void __launch_bounds__(1024, 1) decode_kernel(const cpx<R> *__restric
     for (int b = threadIdx.x; b < L; b += blockDim.x) {
         int m[MAXD] = {0, 0, 0, 0};
         cpx<R> a = {(R)0, (R)0};
-        const int st = classify_bin(spec, g, b, al, ta, roots, (R)kn.mag_tol, (R)kn.round_tol,
+        const int st = classify_bin(sp, g, b, al, ta, roots, (R)kn.mag_tol, (R)kn.round_tol,
                                     (R)kn.verify_tol, fl, m, &a);
         my += st > 0;
         const long long o = (long long)inst * L + b;
@@ -1214,6 +1219,8 @@ __global__ void __launch_bounds__(1024, 1) project_kernel(const int *__restrict_
         out[((long long)inst * L + b) * 2 + 1] = (double)spec[b].im;
     }
 }
+
+#include "fpssft_large.cuh"
 
 // ================================================================== host
 namespace {
@@ -1908,6 +1915,43 @@ int fpssft_line_spectra(const void *cubes, int64_t batch, int64_t batch_stride,
     return check_launch("line_spectra_kernel");
 }
 
+int fpssft_gather_lines(const void *cubes, int32_t cube_precision, int64_t batch,
+                        int64_t batch_stride, const fpssft_shape *shape, const int32_t *alpha_tau,
+                        int32_t per_instance, void *lines, int32_t precision, void *stream) {
+    Geo g;
+    int rc;
+    if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
+    if (batch < 0 || batch > 65535) return fail(FPSSFT_EINVAL, "bad batch (0..65535)");
+    if (batch == 0) return FPSSFT_OK;
+    if (!cubes || !alpha_tau || !lines) return fail(FPSSFT_EINVAL, "NULL buffer");
+    if (cube_precision != FPSSFT_F32 && cube_precision != FPSSFT_F64)
+        return fail(FPSSFT_EINVAL, "cube_precision must be FPSSFT_F32 or FPSSFT_F64");
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long n = (long long)g.nlines * g.L;
+    const dim3 grid((unsigned)std::min<long long>((n + 255) / 256, 4096), (unsigned)batch);
+    const bool c128 = cube_precision == FPSSFT_F64;
+    if (precision == FPSSFT_F64) {
+        if (c128)
+            gather_lines_kernel<double2, double><<<grid, 256, 0, st>>>(
+                (const double2 *)cubes, batch_stride, g, alpha_tau, per_instance,
+                (cpx<double> *)lines);
+        else
+            gather_lines_kernel<float2, double><<<grid, 256, 0, st>>>(
+                (const float2 *)cubes, batch_stride, g, alpha_tau, per_instance,
+                (cpx<double> *)lines);
+    } else {
+        if (c128)
+            gather_lines_kernel<double2, float><<<grid, 256, 0, st>>>(
+                (const double2 *)cubes, batch_stride, g, alpha_tau, per_instance,
+                (cpx<float> *)lines);
+        else
+            gather_lines_kernel<float2, float><<<grid, 256, 0, st>>>(
+                (const float2 *)cubes, batch_stride, g, alpha_tau, per_instance,
+                (cpx<float> *)lines);
+    }
+    return check_launch("gather_lines_kernel");
+}
+
 int fpssft_dft_forward(const void *lines, int64_t batch, int32_t L, void *out, int32_t precision,
                        void *stream) {
     if (L < 1) return fail(FPSSFT_EINVAL, "expected a nonempty 1-D array");
@@ -1960,10 +2004,31 @@ int fpssft_decode_spectra(const void *spectra, int64_t batch, const fpssft_shape
     if (batch == 0) return FPSSFT_OK;
     if (!spectra || !alpha_tau || !status || !freqs || !amps || !n_candidates)
         return fail(FPSSFT_EINVAL, "NULL buffer");
-    const int nt = block_threads(g, g.nlines, params->precision);
-    if (nt < 0) return fail(FPSSFT_EUNSUPPORTED, "line length too large for one CTA");
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
+    const int cs = params->precision == FPSSFT_F64 ? 16 : 8;
+    const int nt = block_threads(g, g.nlines, params->precision);
+    if (nt < 0 || (long long)spec_smem(g, g.nlines, cs) > max_smem_optin()) {
+        // long lines: classify straight from global memory, roots on chip
+        const size_t sm = align16((size_t)g.L * cs) + 64 * 8;
+        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
+        if (params->precision == FPSSFT_F64) {
+            e = cudaFuncSetAttribute(decode_kernel<double, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+            decode_kernel<double, true><<<(unsigned)batch, 1024, sm, st>>>(
+                (const cpx<double> *)spectra, g, alpha_tau, per_instance, kn, floor, status,
+                freqs, amps, n_candidates);
+        } else {
+            e = cudaFuncSetAttribute(decode_kernel<float, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+            decode_kernel<float, true><<<(unsigned)batch, 1024, sm, st>>>(
+                (const cpx<float> *)spectra, g, alpha_tau, per_instance, kn, floor, status,
+                freqs, amps, n_candidates);
+        }
+        return check_launch("decode_kernel");
+    }
     if (params->precision == FPSSFT_F64) {
         const size_t sm = spec_smem(g, g.nlines, 16);
         if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
@@ -1997,13 +2062,23 @@ int fpssft_project_onto_bins(const int32_t *freqs, const double *amps, const int
     if (k_max < 1) return fail(FPSSFT_EINVAL, "k_max must be >= 1");
     if (batch == 0) return FPSSFT_OK;
     if (!freqs || !amps || !counts || !alpha_tau || !out) return fail(FPSSFT_EINVAL, "NULL buffer");
-    const int nt = block_threads(g, 1, precision);
-    if (nt < 0) return fail(FPSSFT_EUNSUPPORTED, "line length too large for one CTA");
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
     const int cs = precision == FPSSFT_F64 ? 16 : 8;
+    const int nt = block_threads(g, 1, precision);
     const size_t sm = make_layout(g.D, g.L, k_max, cs).total;
-    if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "k_max too large");
+    if (nt < 0 || (long long)sm > max_smem_optin()) {
+        // large sets / long lines: one thread per bin scanning the entries
+        constexpr int BT = 64, CAP = 1536;
+        const dim3 grid((unsigned)((g.L + BT - 1) / BT), (unsigned)batch);
+        if (precision == FPSSFT_F64)
+            project_global_kernel<double, BT, CAP><<<grid, BT, 0, st>>>(
+                freqs, amps, counts, k_max, g, alpha_tau, per_instance, out);
+        else
+            project_global_kernel<float, BT, CAP><<<grid, BT, 0, st>>>(
+                freqs, amps, counts, k_max, g, alpha_tau, per_instance, out);
+        return check_launch("project_global_kernel");
+    }
     if (precision == FPSSFT_F64) {
         e = cudaFuncSetAttribute(project_kernel<double>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -1,0 +1,216 @@
+"""The recovery loop for problems whose recovered set or lines do not fit one
+CTA's shared memory: the imaging duality path (the
+512 x 576 frequency cube has L = lcm(512, 576) = 4608 and up to ~20k
+recovered pixels, in float64).
+
+The loop is the reference's (``driver.py:121-212``, restated step for step in
+``oracle/fps_oracle.py:recover``), driven from the host one step per launch:
+
+  gather the D+1 lines      fpssft_gather_lines   (lines.py:36-64)
+  1/L DFT of each line      fpssft_dft_forward    (transform.py:17-22)
+  peel the recovered set    fpssft_project_onto_bins, one call per offset,
+                            global-memory kernel for large sets
+                            (decoder.py:172-191, driver.py:150-154)
+  classify + decode + guard fpssft_decode_spectra (decoder.py:127-169,
+                            driver.py:156-176)
+  merge / prune / amp_sum   vectorised host slot arrays with the reference's
+                            dict semantics and order (driver.py:94-118)
+  peel the new entries,     device projection + max|S| (driver.py:189-204)
+  termination
+
+Every step runs on the device except the merge bookkeeping (numpy over the
+accepted entries); there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+from . import ops
+from .core import CubeShape, SparseSpectrum
+from .driver import (TERMINATED_MAX_ITERATIONS, TERMINATED_RESIDUAL_CLEAN, TERMINATED_STALL,
+                     C_ref, FpsSftConfig, IterationStats, RecoveryReport, _precision_code,
+                     default_max_iterations)
+from .schedule import schedule_from_seed
+
+
+def stepped_offsets(tau, dims):
+    """tau, tau + e_0, ..., tau + e_{D-1} (mod N_k) -- lines.py:55-64."""
+    out = [tuple(int(v) for v in tau)]
+    for k in range(len(dims)):
+        t = list(out[0])
+        t[k] = (t[k] + 1) % dims[k]
+        out.append(tuple(t))
+    return out
+
+
+def line_spectra_global(cube, shape: CubeShape, alpha, tau, *, precision: str = "fp64"):
+    """[D+1, L] spectra of one iteration's lines of one cube (complex64 or
+    complex128 CUDA tensor), lines staged in global memory."""
+    import torch
+
+    D, L = shape.ndim, shape.line_len
+    cube_prec = N.F64 if cube.dtype == torch.complex128 else N.F32
+    if cube.dtype not in (torch.complex64, torch.complex128):
+        raise TypeError("cube must be complex64 or complex128")
+    at = torch.as_tensor(np.stack([np.asarray(alpha, np.int32), np.asarray(tau, np.int32)])[None],
+                         device=cube.device)
+    dt = torch.complex128 if _precision_code(precision) == N.F64 else torch.complex64
+    lines = torch.empty((1, D + 1, L), dtype=dt, device=cube.device)
+    sh = N.make_shape(shape.dims, [int(s) for s in cube.stride()])
+    N.check(N.lib().fpssft_gather_lines(N.ptr(cube), cube_prec, 1, 0, C_ref(sh), N.ptr(at), 0,
+                                        N.ptr(lines), _precision_code(precision),
+                                        N.stream_ptr(cube.device)))
+    return ops.dft_forward(lines, precision=precision)[0]
+
+
+class _RecoveredSet:
+    """The reference's recovered-set dict (driver.py:94-118) as slot arrays:
+    slots in insertion order, a pruned key's slot zeroed and its key free to
+    be re-appended at the end -- the same order a Python dict gives, so the
+    device projections sum in the reference's order (a zero amplitude adds
+    +0.0, which changes no sum).  Linear-index -> slot table for O(1)
+    vectorised lookups; device copies grown by doubling."""
+
+    def __init__(self, shape: CubeShape, device):
+        import torch
+
+        self.shape, self.device = shape, device
+        self.slot_of = np.full(shape.n_total, -1, np.int64)
+        self.keys = np.zeros(0, np.int64)
+        self.freqs = np.zeros((0, shape.ndim), np.int32)
+        self.amps = np.zeros(0, np.complex128)
+        self.cap = 0
+        self.d_freqs = torch.zeros((1, 1, shape.ndim), dtype=torch.int32, device=device)
+        self.d_amps = torch.zeros((1, 1), dtype=torch.complex128, device=device)
+        self.d_count = torch.zeros(1, dtype=torch.int32, device=device)
+        self.n_up = 0
+
+    def __len__(self):
+        return int(np.count_nonzero(self.slot_of[self.keys] == np.arange(len(self.keys))))
+
+    def merge(self, freqs: np.ndarray, amps: np.ndarray, prune_tol: float):
+        """merge-by-sum then prune, for keys distinct within the call."""
+        lin = np.ravel_multi_index(tuple(freqs.T), self.shape.dims)
+        slot = self.slot_of[lin]
+        old = slot >= 0
+        v = self.amps[slot[old]] + amps[old]
+        self.amps[slot[old]] = v
+        dead = np.abs(v) <= prune_tol
+        self.amps[slot[old][dead]] = 0j
+        self.slot_of[lin[old][dead]] = -1
+        fresh = ~old & ~(np.abs(0j + amps) <= prune_tol)
+        n0 = len(self.keys)
+        nf = int(np.count_nonzero(fresh))
+        self.keys = np.concatenate([self.keys, lin[fresh]])
+        self.freqs = np.concatenate([self.freqs, freqs[fresh].astype(np.int32)])
+        self.amps = np.concatenate([self.amps, 0j + amps[fresh]])
+        self.slot_of[lin[fresh]] = np.arange(n0, n0 + nf)
+
+    def amp_total(self) -> float:
+        live = self.slot_of[self.keys] == np.arange(len(self.keys))
+        a = np.abs(self.amps[live])
+        return float(np.cumsum(a)[-1]) if a.size else 0.0  # sequential, like sum()
+
+    def upload(self):
+        """Device copies (count = slots incl. zeroed ones)."""
+        import torch
+
+        n = len(self.keys)
+        if n > self.cap:
+            self.cap = max(n, 2 * self.cap, 64)
+            f = torch.zeros((1, self.cap, self.shape.ndim), dtype=torch.int32, device=self.device)
+            f[0, :self.n_up] = self.d_freqs[0, :self.n_up]
+            self.d_freqs = f
+            self.d_amps = torch.zeros((1, self.cap), dtype=torch.complex128, device=self.device)
+        if n > self.n_up:
+            self.d_freqs[0, self.n_up:n] = torch.as_tensor(self.freqs[self.n_up:n],
+                                                           device=self.device)
+            self.n_up = n
+        self.d_amps[0, :n] = torch.as_tensor(self.amps, device=self.device)
+        self.d_count.fill_(n)
+
+    def entries(self):
+        live = self.slot_of[self.keys] == np.arange(len(self.keys))
+        return self.freqs[live].astype(np.int64), self.amps[live]
+
+
+def _project(shape, freqs, amps, count, k_cap, alpha, off, precision, device):
+    """Device projection of (freqs, amps)[:count] onto line (alpha, off)."""
+    import torch
+
+    at = torch.as_tensor(np.stack([np.asarray(alpha, np.int32), np.asarray(off, np.int32)])[None],
+                         device=device)
+    out = torch.empty((1, shape.line_len), dtype=torch.complex128, device=device)
+    N.check(N.lib().fpssft_project_onto_bins(N.ptr(freqs), N.ptr(amps), N.ptr(count), 1, k_cap,
+                                             C_ref(N.make_shape(shape.dims)), N.ptr(at), 0,
+                                             N.ptr(out), _precision_code(precision),
+                                             N.stream_ptr(device)))
+    return out[0]
+
+
+def fps_sft_large(cube, shape: CubeShape | None = None, config: FpsSftConfig = FpsSftConfig(),
+                  *, precision: str = "fp64", schedule=None) -> RecoveryReport:
+    """``fps_sft`` for a single large problem (CUDA tensor ``cube``).  Same
+    arguments, defaults, schedule and report as the reference's entry point;
+    float64 by default (the imaging path compares pixels to 1e-6)."""
+    import torch
+
+    shape = shape or CubeShape(tuple(cube.shape))
+    if tuple(cube.shape) != shape.dims:
+        raise ValueError(f"cube extents {tuple(cube.shape)} do not match {shape.dims}")
+    D, L, dims = shape.ndim, shape.line_len, shape.dims
+    dev = cube.device
+    t_max = config.max_iterations or default_max_iterations(shape)
+    if schedule is None:
+        schedule = schedule_from_seed(shape, config.seed, t_max)
+    schedule = np.asarray(schedule)
+    rs = _RecoveredSet(shape, dev)
+    amp_total = 0.0
+    stall, term, it = 0, TERMINATED_MAX_ITERATIONS, 0
+    log = []
+    for it in range(1, t_max + 1):
+        alpha = tuple(int(v) for v in schedule[it - 1, 0])
+        tau = tuple(int(v) for v in schedule[it - 1, 1])
+        offs = stepped_offsets(tau, dims)
+        spec = line_spectra_global(cube, shape, alpha, tau, precision=precision)
+        spec = spec.to(torch.complex128)
+        if len(rs.keys):
+            rs.upload()
+            for i, off in enumerate(offs):
+                spec[i] -= _project(shape, rs.d_freqs, rs.d_amps, rs.d_count, rs.cap, alpha, off,
+                                    precision, dev)
+        floor = max(config.energy_floor_abs, config.energy_floor * amp_total)
+        st, fr, am, nc = ops.decode_spectra_device(spec[None], alpha, tau, shape, config, floor,
+                                                   precision=precision)
+        acc_t = torch.nonzero(st[0] == 2).flatten()  # ascending bins, guard applied
+        new_f = fr[0, acc_t].cpu().numpy().astype(np.int64)
+        new_a = am[0, acc_t].cpu().numpy()
+        n_acc = len(new_a)
+        if n_acc:  # merge-by-sum and prune (driver.py:103-108)
+            rs.merge(new_f, new_a, config.amp_prune_tol)
+        amp_total = rs.amp_total()
+        n_cand = int(nc[0])
+        log.append(IterationStats(it, alpha, tau, n_cand, n_acc, n_cand - n_acc))
+        if n_acc:
+            stall = 0
+            nf = fr[0, acc_t].contiguous()[None]
+            na = am[0, acc_t].contiguous()[None]
+            cnt = torch.full((1,), n_acc, dtype=torch.int32, device=dev)
+            for i, off in enumerate(offs):
+                spec[i] -= _project(shape, nf, na, cnt, n_acc, alpha, off, precision, dev)
+        else:
+            stall += 1
+        if float(spec.abs().max()) <= max(config.energy_floor_abs,
+                                          config.residual_stop * amp_total):
+            term = TERMINATED_RESIDUAL_CLEAN
+            break
+        if stall >= config.stall_limit:
+            term = TERMINATED_STALL
+            break
+    freqs, amps = rs.entries()
+    order = np.lexsort(freqs.T[::-1]) if len(freqs) else np.zeros(0, np.int64)
+    return RecoveryReport(iterations_run=it, samples_used=it * (D + 1) * L,
+                          recovered=SparseSpectrum._trusted(shape, freqs[order], amps[order]),
+                          terminated_by=term, iteration_log=tuple(log))

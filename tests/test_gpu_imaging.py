@@ -1,0 +1,95 @@
+"""GPU parity of the imaging duality path against
+the unmodified reference's outputs (tests/golden/imaging.*,
+make_imaging_golden.py): small pixel-sparse images recovered exactly, and
+the paper's 512 x 576 phantom at three sparsity levels (L = 4608, up to
+~20k pixels) with the same iterations, samples and termination.  Also the
+global-memory kernels behind it against the oracle."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import fps_oracle as O  # noqa: E402
+
+import paper_1711_11407_b200 as P  # noqa: E402
+from paper_1711_11407_b200 import imaging as I  # noqa: E402
+from paper_1711_11407_b200 import ops  # noqa: E402
+from paper_1711_11407_b200.large import line_spectra_global  # noqa: E402
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+HERE = os.path.join(os.path.dirname(__file__), "golden")
+GOLD = json.load(open(os.path.join(HERE, "imaging.json")))
+ARR = np.load(os.path.join(HERE, "imaging.npz"))
+
+
+@pytest.mark.parametrize("case", GOLD["small"], ids=lambda c: c["name"])
+def test_small_images_match_reference(case):
+    px = ARR[f"{case['name']}/pixels"]
+    recon, rep = I.reconstruct_sparse_image(I.GrayImage(px), P.FpsSftConfig(**case["cfg"]))
+    assert rep.iterations_run == case["iterations_run"]
+    assert rep.samples_used == case["samples_used"]
+    assert rep.terminated_by == case["terminated_by"]
+    ref_f = ARR[f"{case['name']}/freqs"]
+    got_f = rep.recovered.freq_array.reshape(-1, 2)
+    np.testing.assert_array_equal(got_f, ref_f[np.lexsort(ref_f.T[::-1])] if len(ref_f) else ref_f)
+    assert np.abs(recon.pixels - ARR[f"{case['name']}/recon"]).max() <= 1e-9
+
+
+@pytest.mark.parametrize("row", GOLD["duality_512x576"], ids=lambda r: f"level{r['level']}")
+def test_paper_phantom_levels_match_reference(row):
+    ph = I.synthetic_phantom((512, 576), 1)
+    sparse = I.sparsify(ph, I.threshold_for_fraction(ph, row["target"]))
+    recon, rep = I.reconstruct_sparse_image(sparse, P.FpsSftConfig(**row["cfg"]))
+    assert rep.iterations_run == row["iterations_run"]
+    assert rep.samples_used == row["samples_used"]
+    assert rep.terminated_by == row["terminated_by"]
+    assert len(rep.recovered.entries) == row["recovered"]
+    err = float(np.abs(recon.pixels - sparse.pixels).max())
+    if row["max_pixel_error"] <= 1e-6:
+        assert err <= 1e-6
+    else:  # the reference does not finish this level either (max_iterations)
+        assert err == pytest.approx(row["max_pixel_error"], abs=1e-6)
+
+
+def test_long_line_spectra_and_large_projection_vs_oracle():
+    """L = 4608 float64: global-memory gather + mixed-radix DFT, the
+    global decode path and a 20k-entry projection, against the oracle."""
+    dims = (512, 576)
+    rng = np.random.default_rng(7)
+    k = 20000
+    flat = rng.choice(512 * 576, size=k, replace=False)
+    f = np.stack(np.unravel_index(flat, dims), axis=-1).astype(np.int64)
+    a = rng.uniform(0.5, 1.0, k) * np.exp(2j * np.pi * rng.random(k))
+    alpha, tau = (5, 7), (100, 301)
+    shape = P.CubeShape(dims)
+    ref = O.project(f, a, alpha, tau, dims)
+    got = ops.project_onto_bins(f, a, alpha, tau, shape, precision="fp64").cpu().numpy()
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(a).sum()
+    cube = torch.as_tensor(rng.standard_normal(dims) + 1j * rng.standard_normal(dims),
+                           device="cuda")
+    spec = line_spectra_global(cube, shape, alpha, tau).cpu().numpy()
+    ref_s = O.line_spectra(cube.cpu().numpy(), alpha, tau, dims)
+    assert np.abs(spec - ref_s).max() <= 1e-12 * np.abs(ref_s).max()
+    # decode of a clean 1-sparse set of bins through the global path
+    f2 = f[:300]
+    a2 = a[:300]
+    x = np.zeros(dims, complex)
+    for (m0, m1), amp in zip(f2, a2):
+        x += amp * np.exp(2j * np.pi * (np.arange(512)[:, None] * m0 / 512 +
+                                        np.arange(576)[None, :] * m1 / 576))
+    spec2 = line_spectra_global(torch.as_tensor(x, device="cuda"), shape, alpha, tau)
+    st, fr, am, nc = ops.decode_spectra_device(spec2[None], alpha, tau, shape,
+                                               P.FpsSftConfig(), 1e-12, precision="fp64")
+    bins, m, amp, n_cand = O.classify(spec2.cpu().numpy(), tau, dims, O.P64, 1e-12)
+    keep = O.bins_of(m, alpha, dims) == bins
+    acc = np.flatnonzero(st[0].cpu().numpy() == 2)
+    np.testing.assert_array_equal(acc, bins[keep])
+    np.testing.assert_array_equal(fr[0].cpu().numpy()[acc], m[keep])
+    assert int(nc[0]) == n_cand
