@@ -12,6 +12,8 @@ from .driver import (PROFILES, BatchResult, BatchRunner, FpsSftConfig, Iteration
                      RecoveryReport, default_max_iterations, fps_sft, fps_sft_batch, materialize,
                      max_k_cap)
 from .baseline import baseline_sft
+from .imaging import GrayImage, reconstruct_sparse_image, synthetic_phantom
+from .large import fps_sft_large
 from .schedule import (bins_of_frequencies, is_valid_slope, sample_slope, schedule_from_seed,
                        valid_slopes)
 
@@ -20,7 +22,8 @@ __version__ = "0.1.0"
 ALGORITHMS = {"fps-b200": fps_sft, "baseline-b200": baseline_sft}
 
 __all__ = ["ALGORITHMS", "BatchResult", "BatchRunner", "CubeShape", "DenseSource",
-           "FpsSftConfig", "FreqIndex", "IterationStats", "PROFILES", "RecoveryReport",
+           "FpsSftConfig", "FreqIndex", "GrayImage", "IterationStats", "PROFILES",
+           "RecoveryReport", "fps_sft_large", "reconstruct_sparse_image", "synthetic_phantom",
            "SignalSource", "Sinusoid", "SparseSpectrum", "baseline_sft", "bins_of_frequencies",
            "default_max_iterations", "fps_sft", "fps_sft_batch", "is_valid_slope",
            "make_dense_source", "materialize", "max_k_cap", "sample_slope",
