@@ -555,3 +555,21 @@ def test_misaligned_and_padded_rows_match_contiguous(dims, k, k_cap, mode):
     for name in ("count", "iterations", "terminated_by", "freqs", "amps"):
         assert torch.equal(getattr(r0, name), getattr(r1, name)), name
     assert int(r0.count[0]) > 0
+
+
+def test_spectrum_files_round_trip_through_the_device(tmp_path):
+    """fps_sft_batch -> save_batch (reference text format) -> load_batch ->
+    fpssft_synthesize gives the same grids as synthesising the device result."""
+    from paper_1711_11407_b200 import spectrum_io as S
+
+    w = W.CONFIGS[2]
+    _, cubes = _batch(w, 3)
+    res = P.fps_sft_batch(cubes, P.FpsSftConfig(**G.PROFILES["P32"]), k_cap=128)
+    paths = S.save_batch(res, tmp_path)
+    f, a, c, shape = S.load_batch(paths, k_cap=128)
+    assert shape == res.shape
+    assert torch.equal(c, res.count)
+    for b in range(3):
+        n = int(c[b])
+        assert torch.equal(f[b, :n], res.freqs[b, :n]) and torch.equal(a[b, :n], res.amps[b, :n])
+    assert torch.equal(ops.synthesize(f, a, c, shape=shape), ops.synthesize(res))
