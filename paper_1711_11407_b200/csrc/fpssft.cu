@@ -28,6 +28,15 @@
 #ifndef FPSSFT_TEAM_GATHER_NC
 #define FPSSFT_TEAM_GATHER_NC FPSSFT_GATHER_NC
 #endif
+#ifndef FPSSFT_SYNTH_WARPFFT
+#define FPSSFT_SYNTH_WARPFFT 1  // per-warp row FFTs in the static synthesis kernel
+#endif
+#ifndef SYNTH_RC
+#define SYNTH_RC 16  // rows per chunk of the static 512-point synthesis kernel
+#endif
+#ifndef SYNTH_NT
+#define SYNTH_NT 256
+#endif
 #ifndef FPSSFT_WARP_NT
 #define FPSSFT_WARP_NT 256  // largest CTA of the warp kernel (FPSSFT_WARP_NT / 32 instances)
 #endif
@@ -942,8 +951,14 @@ __global__ void __launch_bounds__(NT) synth_static_kernel(const int *__restrict_
     float2 *img = out + inst * out_stride;
     const R scale = (R)NL;
     const unsigned long long magicL = ~0ULL / (unsigned)L + 1ULL;
-    for (int r0 = 0; r0 < N0; r0 += RC) {
+    constexpr int NW = NT / 32, RW = RC / NW;  // rows per warp in the FFT phase
+    static_assert(!FPSSFT_SYNTH_WARPFFT || RC % NW == 0, "whole rows per warp");
+    const int warp = tid >> 5, lane = tid & 31;
+    if (FPSSFT_SYNTH_WARPFFT)
         for (int q = tid; q < RC * VROW; q += NT) V[q] = {(R)0, (R)0};
+    for (int r0 = 0; r0 < N0; r0 += RC) {
+        if (!FPSSFT_SYNTH_WARPFFT)
+            for (int q = tid; q < RC * VROW; q += NT) V[q] = {(R)0, (R)0};
         __syncthreads();
         // sparse part: one thread per non-empty column, all RC rows of the
         // chunk, entries in order; phase c0 n0 m0 mod L advanced by c0 m0 per row
@@ -970,11 +985,26 @@ __global__ void __launch_bounds__(NT) synth_static_kernel(const int *__restrict_
             for (int r = 0; r < RC; ++r) V[padi<true>(r * NL + c)] = {acc[r].re, -acc[r].im};
         }
         __syncthreads();
-        fft_static<R, NL, RC, NT, BlockTeam>(V, rootsN, tid);
+        if constexpr (FPSSFT_SYNTH_WARPFFT) {
+            // each warp transforms, writes and re-zeroes its own RW rows: the
+            // only block barriers left are around the sparse phase
+            cpx<R> *Vw = V + warp * RW * (NL + NL / 16);
+            fft_static<R, NL, RW, 32, WarpTeam>(Vw, rootsN, lane);
+            float2 *iw = img + (long long)(r0 + warp * RW) * NL;
 #pragma unroll 4
-        for (int q = tid; q < RC * NL; q += NT) {
-            const cpx<R> x = V[padi<true>(q)];
-            img[(long long)r0 * NL + q] = make_float2((float)(x.re * scale), (float)(-x.im * scale));
+            for (int q = lane; q < RW * NL; q += 32) {
+                const cpx<R> x = Vw[padi<true>(q)];
+                iw[q] = make_float2((float)(x.re * scale), (float)(-x.im * scale));
+                Vw[padi<true>(q)] = {(R)0, (R)0};
+            }
+        } else {
+            fft_static<R, NL, RC, NT, BlockTeam>(V, rootsN, tid);
+#pragma unroll 4
+            for (int q = tid; q < RC * NL; q += NT) {
+                const cpx<R> x = V[padi<true>(q)];
+                img[(long long)r0 * NL + q] =
+                    make_float2((float)(x.re * scale), (float)(-x.im * scale));
+            }
         }
         __syncthreads();
     }
@@ -1812,10 +1842,11 @@ int fpssft_synthesize(const int32_t *freqs, const double *amps, const int32_t *c
     if ((rc = make_geo(&row, &gr)) != FPSSFT_OK) return rc;
     const int NT = 256, NL = gr.L;
     const int cs = precision == FPSSFT_F64 ? 16 : 8;
-    if (gc.D == 2 && NL == 512 && gc.N[0] % 16 == 0 &&
+    if (gc.D == 2 && NL == 512 && gc.N[0] % SYNTH_RC == 0 &&
         (long long)gc.L * gc.N[0] < (1LL << 32)) {
-        constexpr int RC = 16;  // compile-time variant: config 5's 512 x 512 images
-        const size_t sm2 = align16((size_t)RC * (512 + 512 / 16 + 1) * cs) +  // V (padded)
+        // compile-time variant: config 5's 512 x 512 images, SYNTH_RC rows per
+        // chunk, SYNTH_NT threads
+        const size_t sm2 = align16((size_t)SYNTH_RC * (512 + 512 / 16 + 1) * cs) +  // V (padded)
                            align16((size_t)gc.L * cs) + align16((size_t)512 * cs) +
                            align16((size_t)k_cap * cs) + align16((size_t)k_cap * 4) +
                            align16((size_t)513 * 4) + align16((size_t)512 * 4) +
@@ -1824,17 +1855,17 @@ int fpssft_synthesize(const int32_t *freqs, const double *amps, const int32_t *c
             cudaStream_t st = (cudaStream_t)stream;
             cudaError_t e;
             if (precision == FPSSFT_F64) {
-                auto k = synth_static_kernel<double, 512, RC, 256>;
+                auto k = synth_static_kernel<double, 512, SYNTH_RC, SYNTH_NT>;
                 e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
                 if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(synth)");
-                k<<<(unsigned)batch, 256, sm2, st>>>(freqs, amps, counts, k_cap, gc,
-                                                     (float2 *)cubes, batch_stride);
+                k<<<(unsigned)batch, SYNTH_NT, sm2, st>>>(freqs, amps, counts, k_cap, gc,
+                                                          (float2 *)cubes, batch_stride);
             } else {
-                auto k = synth_static_kernel<float, 512, RC, 256>;
+                auto k = synth_static_kernel<float, 512, SYNTH_RC, SYNTH_NT>;
                 e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
                 if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(synth)");
-                k<<<(unsigned)batch, 256, sm2, st>>>(freqs, amps, counts, k_cap, gc,
-                                                     (float2 *)cubes, batch_stride);
+                k<<<(unsigned)batch, SYNTH_NT, sm2, st>>>(freqs, amps, counts, k_cap, gc,
+                                                          (float2 *)cubes, batch_stride);
             }
             return check_launch("synth_static_kernel");
         }
