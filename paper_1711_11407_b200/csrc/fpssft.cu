@@ -1617,7 +1617,7 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
                         bw = w;
                     }
                 }
-                if (bw && best_inst >= warp_warps)
+                if (bw)  // explicit opt-in (FPSSFT_IL): used whenever it fits
                     wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * bw, bw * ni,
                                     wl.roots + (size_t)bw * ni * wl.per_warp, ik};
             }
