@@ -12,6 +12,9 @@
 // Included by fpssft.cu after the warp kernel (shares its helpers).
 #pragma once
 // (included inside namespace fpssft)
+#ifndef TEAM_SORT_BITS
+#define TEAM_SORT_BITS 11  // output counting-sort buckets (2048)
+#endif
 #ifndef FPSSFT_TEAM_PROJ
 #define FPSSFT_TEAM_PROJ 1  // projection: 1 = warp match_any + ordered apply, 0 = counting sort
 #endif
@@ -29,7 +32,7 @@ __host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, 
     size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // padi() layout
     if (stage16_ok(D, L, cs, nt) && spec_bytes < (size_t)(D + 1) * L * 16)
         spec_bytes = (size_t)(D + 1) * L * 16;  // 16-byte staging slots (gather_lines_cg16)
-    const size_t sort_bytes = 1024 + (size_t)k_cap * 4;
+    const size_t sort_bytes = ((size_t)1 << TEAM_SORT_BITS) * 4 + (size_t)k_cap * 4;
     size_t o = 0;
     y.H = 2 * k_cap;
     y.spec = o;      o = align16(o + (spec_bytes > sort_bytes ? spec_bytes : sort_bytes));
@@ -402,14 +405,18 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
         }
     }
 
-    // ---- RecoveryReport: counting sort of the live keys (top 8 bits), then
-    //      insertion sort inside the buckets
+    // ---- RecoveryReport: counting sort of the live keys on their top
+    //      TEAM_SORT_BITS bits, then insertion sort inside the (short)
+    //      buckets.  Fine buckets matter: clustered spectra (config 4's blobs)
+    //      put dozens of entries in one 8-bit bucket, and a single thread's
+    //      quadratic sort then held the whole CTA at the barrier.
     __syncthreads();
+    constexpr int SB = TEAM_SORT_BITS, NB = 1 << SB;
     int *hist = (int *)spec;
-    int *sslot = hist + 256;
+    int *sslot = hist + NB;
     const int kb = g.key_bits_;
-    const int shift = kb > 8 ? kb - 8 : 0;
-    for (int i = tid; i < 256; i += NT) hist[i] = 0;
+    const int shift = kb > SB ? kb - SB : 0;
+    for (int i = tid; i < NB; i += NT) hist[i] = 0;
     __syncthreads();
     int my_live = 0;
     for (int s = tid; s < n_slots; s += NT)
@@ -418,33 +425,22 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
             atomicAdd(&hist[slot_key[s] >> shift], 1);
         }
     const int count = block_sum(my_live, ired);
-    if (tid < 32) {  // exclusive scan of the 256 buckets by warp 0
-        const int lane = tid;
-        int c[8], run = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            c[i] = hist[lane * 8 + i];
-            run += c[i];
-        }
-        int incl = run;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-        }
-        int start = incl - run;
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            hist[lane * 8 + i] = start;
-            start += c[i];
+    {   // exclusive scan of the bucket counts, NT at a time
+        int carry = 0;
+#pragma unroll 1
+        for (int j0 = 0; j0 < NB; j0 += NT) {
+            const int c = j0 + tid < NB ? hist[j0 + tid] : 0;
+            int tot;
+            const int pre = block_exscan(c, ired, &tot);
+            if (j0 + tid < NB) hist[j0 + tid] = carry + pre;  // the bucket's fill cursor
+            carry += tot;
+            __syncthreads();
         }
     }
-    __syncthreads();
     for (int s = tid; s < n_slots; s += NT)
         if (slot_live[s]) sslot[atomicAdd(&hist[slot_key[s] >> shift], 1)] = s;
     __syncthreads();
-    for (int bkt = tid; bkt < 256; bkt += NT) {
+    for (int bkt = tid; bkt < NB; bkt += NT) {
         const int en = hist[bkt], st = bkt ? hist[bkt - 1] : 0;
         for (int i = st + 1; i < en; ++i) {
             const int v = sslot[i], kv = slot_key[v];
