@@ -272,8 +272,11 @@ class BatchRunner:
     def run(self, cubes) -> BatchResult:
         import torch
 
-        if not (isinstance(cubes, torch.Tensor) and cubes.is_cuda):
+        if not isinstance(cubes, torch.Tensor):
             raise ValueError("cubes must be a CUDA tensor (use fps_sft for host arrays)")
+        if not cubes.is_cuda and not cubes.is_pinned():
+            raise ValueError("cubes must be a CUDA tensor or a pinned host tensor "
+                             "(use fps_sft for other host arrays)")
         if cubes.dtype != torch.complex64:
             raise ValueError(f"cubes must be complex64, got {cubes.dtype}")
         if tuple(cubes.shape[1:]) != self.shape.dims or cubes.shape[0] != self.batch:
@@ -281,11 +284,15 @@ class BatchRunner:
                              f"got {tuple(cubes.shape)}")
         # element strides (complex64 units) of one cube and between cubes
         sh = N.make_shape(self.shape.dims, [int(s) for s in cubes.stride()[1:]])
-        with torch.cuda.device(cubes.device):
+        # a pinned host tensor is read in place by the kernel (zero copy over the
+        # host link: only the gathered samples cross it, the sub-linear sample
+        # budget of the algorithm); its UVA address is valid on the device
+        dev = cubes.device if cubes.is_cuda else self.device
+        with torch.cuda.device(dev):
             N.check(N.lib().fpssft_run_batch(
                 N.ptr(cubes), self.batch, int(cubes.stride(0)), C_ref(sh), C_ref(self._params_c),
                 N.ptr(self.schedule), N.ptr(self.sched_index), int(self.schedule_host.shape[0]),
-                C_ref(self._out_c), N.stream_ptr(cubes.device)))
+                C_ref(self._out_c), N.stream_ptr(dev)))
         o = self.out
         return BatchResult(self.shape, self.k_cap, o["freqs"], o["amps"], o["count"],
                            o["iterations"], o["samples_used"], o["terminated_by"],

@@ -1,0 +1,270 @@
+"""Recovery of batches whose cubes live in pinned HOST memory.
+
+The reference's users hand ``fps_sft`` a host array (``make_dense_source``,
+``/root/reference/pkg/src/fps_sft/core.py:276-278``); at batch scale the
+cost of reaching the GPU is the host link, not the recovery kernel (config 2:
+2 GiB of cubes at ~55 GB/s = 39 ms against 0.2 ms of recovery).  FPS-SFT
+reads only ``samples_used`` of the N samples of each cube (sub-linear sample
+complexity, ``driver.py:208``), so a cube need not cross the link at all: the
+recovery kernel can gather its samples straight out of the pinned host
+buffer (zero copy, UVA).  This module moves every batch through two
+concurrent paths and splits the instances between them:
+
+* zero copy: the first ``Bz`` instances are recovered by ``BatchRunner.run``
+  on the pinned host tensor itself -- only the gathered samples cross the
+  link, at the host's random-read rate (~3.6e8 samples/s measured, 16-byte
+  requests; ``tools/host_gather_probe.cu``);
+* bulk copy: the remaining instances stream through double-buffered device
+  chunks (H2D on one stream, recovery on another, results back on a third),
+  at the host link's bulk rate.
+
+``mode="auto"`` sizes the split from a cost model (``zero_copy_split``) fed
+with the mean ``samples_used`` of the previous batch (the first batch goes
+through the copy path); ``tune()`` replaces the model by measuring a few
+splits on a real batch (untimed, like a cuFFT plan); ``"zero_copy"`` /
+``"copy"`` force one path, ``"split"`` takes an explicit fraction.  Results
+are identical whichever path an instance takes (the kernels are the same;
+tested).  Outputs land in pinned host tensors.
+
+Measured on one B200 behind PCIe Gen5 (``profiles/r01_hostpath.jsonl``):
+config 2 batches cross 2x faster split 0.8/0.2 than copied whole, config 4
+4.5x faster zero-copied; config 5 (30 % of each cube sampled, images
+returned) stays on the copy path, where H2D and D2H overlap.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .core import CubeShape
+from .driver import BatchRunner, FpsSftConfig, allocate_outputs, default_max_iterations
+
+# measured on the B200 pool (tools/host_gather_probe.cu, tools/zero_copy_probe.py)
+ZC_SAMPLES_PER_S = 3.6e8
+H2D_BYTES_PER_S = 5.5e10
+
+
+def zero_copy_split(mean_samples: float, cube_samples: int, *, zc_rate: float = ZC_SAMPLES_PER_S,
+                    h2d_rate: float = H2D_BYTES_PER_S) -> float:
+    """Fraction of a batch to gather in place from host memory: the split at
+    which the zero-copy part (``mean_samples`` random reads per instance at
+    ``zc_rate``) and the copied part (whole complex64 cubes at ``h2d_rate``)
+    take equal time.  Fractions below 5 % are not worth a second launch."""
+    if mean_samples <= 0:
+        return 1.0
+    t_z = mean_samples / zc_rate
+    t_c = cube_samples * 8 / h2d_rate
+    f = t_c / (t_z + t_c)
+    return f if f > 0.05 else 0.0
+
+
+class HostBatchRunner:
+    """Recover ``[batch, *dims]`` complex64 cubes held in pinned host memory.
+
+    ``run(host_cubes)`` returns the per-instance outputs as pinned host
+    tensors (the ``allocate_outputs`` dict); ``run(host_cubes, images)`` also
+    re-synthesises every recovered spectrum (config 5) into the pinned host
+    tensor ``images``.
+    """
+
+    def __init__(self, shape: CubeShape, config: FpsSftConfig, batch: int, *,
+                 k_cap: int = 256, precision: str = "fp32", device=None, mode: str = "auto",
+                 zero_copy_fraction: float | None = None, chunk: int | None = None,
+                 chunk_bytes: int = 256 << 20, schedule=None, sched_index=None):
+        import torch
+
+        if mode not in ("auto", "copy", "zero_copy", "split"):
+            raise ValueError("mode must be auto, copy, zero_copy or split")
+        if mode == "split" and zero_copy_fraction is None:
+            raise ValueError("split mode needs zero_copy_fraction")
+        self.shape, self.config, self.batch = shape, config, int(batch)
+        self.mode = mode
+        self.fraction = zero_copy_fraction
+        self.device = torch.device(device if device is not None else "cuda")
+        self.k_cap, self.precision = k_cap, precision
+        self.t_max = config.max_iterations or default_max_iterations(shape)
+        cube_bytes = shape.n_total * 8
+        self.chunk = int(chunk or max(1, min(self.batch, chunk_bytes // cube_bytes)))
+        self._schedule = schedule
+        self._sched_index = None if sched_index is None else np.asarray(sched_index, np.int32)
+        self.out = allocate_outputs(self.batch, shape, k_cap, self.t_max, "cpu")
+        for k, v in list(self.out.items()):
+            if v is not None:
+                self.out[k] = v.pin_memory()
+        self.last_mean_samples: float | None = None
+        self.tuned: dict | None = None
+        self._runners: dict = {}
+        self._bufs: list = []
+        self._img_bufs: list = []
+        self._streams = None
+
+    # ------------------------------------------------------------------ plan
+    def split_count(self) -> int:
+        """Instances that take the zero-copy path in the next ``run``."""
+        if self.mode == "copy":
+            return 0
+        if self.mode == "zero_copy":
+            return self.batch
+        if self.mode == "split":
+            return int(round(self.fraction * self.batch))
+        if self.last_mean_samples is None:
+            return 0
+        return int(self.batch * zero_copy_split(self.last_mean_samples, self.shape.n_total))
+
+    def tune(self, host_cubes, images=None, fractions=None) -> float:
+        """Measure a few zero-copy fractions on ``host_cubes`` (one timed run
+        each after a warm run) and keep the fastest (mode becomes "split").
+        Returns the chosen fraction."""
+        import time
+
+        if fractions is None:
+            self.run(host_cubes, images)  # learns the sample count
+            f0 = self.split_count() / max(1, self.batch)
+            fractions = sorted({0.0, 1.0, round(f0, 3), 0.5, 0.65, 0.8, 0.9})
+        best = None
+        for f in fractions:
+            self.mode, self.fraction = "split", float(f)
+            self.run(host_cubes, images)
+            t0 = time.perf_counter()
+            self.run(host_cubes, images)
+            dt = time.perf_counter() - t0
+            if best is None or dt < best[0]:
+                best = (dt, float(f))
+        self.fraction = best[1]
+        self.tuned = {"fraction": best[1], "ms": best[0] * 1e3}
+        return best[1]
+
+    def _runner(self, b0: int, n: int) -> BatchRunner:
+        key = (b0, n)
+        r = self._runners.get(key)
+        if r is None:
+            si = None if self._sched_index is None else self._sched_index[b0:b0 + n]
+            r = BatchRunner(self.shape, self.config, n, schedule=self._schedule, sched_index=si,
+                            k_cap=self.k_cap, precision=self.precision, device=self.device)
+            self._runners[key] = r
+        return r
+
+    def _ensure_buffers(self, synth: bool):
+        import torch
+
+        if self._streams is None:
+            self._streams = [torch.cuda.Stream(self.device) for _ in range(4)]
+        nbuf = 2
+        while len(self._bufs) < nbuf:
+            self._bufs.append(torch.empty((self.chunk, *self.shape.dims), dtype=torch.complex64,
+                                          device=self.device))
+        while synth and len(self._img_bufs) < nbuf:
+            self._img_bufs.append(torch.empty((self.chunk, *self.shape.dims),
+                                              dtype=torch.complex64, device=self.device))
+
+    def _copy_out(self, r: BatchRunner, b0: int, n: int):
+        for k, v in r.out.items():
+            if v is not None:
+                self.out[k][b0:b0 + n].copy_(v, non_blocking=True)
+
+    # ------------------------------------------------------------------- run
+    def run(self, host_cubes, images=None) -> dict:
+        """Recover every instance of the pinned host tensor ``host_cubes``;
+        with ``images`` (pinned host, same shape) also write each instance's
+        re-synthesised grid.  Blocks until the outputs are on the host."""
+        import torch
+
+        from .ops import synthesize
+
+        if not (isinstance(host_cubes, torch.Tensor) and not host_cubes.is_cuda
+                and host_cubes.is_pinned()):
+            raise ValueError("host_cubes must be a pinned host tensor")
+        if tuple(host_cubes.shape) != (self.batch, *self.shape.dims) or \
+                host_cubes.dtype != torch.complex64:
+            raise ValueError(f"host_cubes must be complex64 [{self.batch}, {self.shape.dims}]")
+        if not host_cubes.is_contiguous():
+            raise ValueError("host_cubes must be contiguous")
+        synth = images is not None
+        if synth and not (not images.is_cuda and images.is_pinned()
+                          and images.shape == host_cubes.shape):
+            raise ValueError("images must be a pinned host tensor shaped like host_cubes")
+        self._ensure_buffers(synth)
+        s_h2d, s_run, s_d2h, s_zc = self._streams
+        cur = torch.cuda.current_stream(self.device)
+        for s in self._streams:
+            s.wait_stream(cur)
+        bz = self.split_count()
+
+        # zero-copy part: gathered in place from host memory (one launch)
+        ev_zc = None
+        if bz:
+            with torch.cuda.stream(s_zc):
+                rz = self._runner(0, bz)
+                rz.run(host_cubes[:bz])
+                self._copy_out(rz, 0, bz)
+                ev_zc = torch.cuda.Event()
+                ev_zc.record(s_zc)
+
+        # bulk-copy part: double-buffered chunks, H2D || recovery || D2H
+        ev_free = [None, None]
+        k = 0
+        b0 = bz
+        while b0 < self.batch:
+            n = min(self.chunk, self.batch - b0)
+            i = k & 1
+            buf = self._bufs[i][:n]
+            with torch.cuda.stream(s_h2d):
+                if ev_free[i] is not None:
+                    s_h2d.wait_event(ev_free[i])
+                buf.copy_(host_cubes[b0:b0 + n], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_h2d)
+            with torch.cuda.stream(s_run):
+                s_run.wait_event(ev_in)
+                r = self._runner(b0, n)
+                res = r.run(buf)
+                self._copy_out(r, b0, n)
+                ev_done = torch.cuda.Event()
+                ev_done.record(s_run)
+                if synth:
+                    img = self._img_bufs[i][:n]
+                    synthesize(res, out=img)
+                    ev_img = torch.cuda.Event()
+                    ev_img.record(s_run)
+            if synth:
+                with torch.cuda.stream(s_d2h):
+                    s_d2h.wait_event(ev_img)
+                    images[b0:b0 + n].copy_(img, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(s_d2h)
+                    ev_free[i] = ev
+            else:
+                ev_free[i] = ev_done
+            b0 += n
+            k += 1
+
+        if synth and bz:
+            # the zero-copy instances' images: synthesised chunk-wise, sent back
+            s_run.wait_event(ev_zc)
+            c0 = 0
+            while c0 < bz:
+                n = min(self.chunk, bz - c0)
+                i = k & 1
+                with torch.cuda.stream(s_run):
+                    if ev_free[i] is not None:
+                        s_run.wait_event(ev_free[i])
+                    img = self._img_bufs[i][:n]
+                    o = self._runners[(0, bz)].out
+                    synthesize(o["freqs"][c0:c0 + n], o["amps"][c0:c0 + n],
+                               o["count"][c0:c0 + n], shape=self.shape, out=img)
+                    ev_img = torch.cuda.Event()
+                    ev_img.record(s_run)
+                with torch.cuda.stream(s_d2h):
+                    s_d2h.wait_event(ev_img)
+                    images[c0:c0 + n].copy_(img, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(s_d2h)
+                    ev_free[i] = ev
+                c0 += n
+                k += 1
+
+        for s in self._streams:
+            cur.wait_stream(s)
+        cur.synchronize()
+        self.last_mean_samples = float(self.out["samples_used"].double().mean())
+        return self.out

@@ -158,6 +158,9 @@ def synthesize(result_or_freqs, amps=None, counts=None, *, shape: CubeShape | No
     dev = freqs.device
     if out is None:
         out = torch.empty((B, *shape.dims), dtype=torch.complex64, device=dev)
+    elif not out.is_cuda and not out.is_pinned():
+        # a pinned host ``out`` is written in place over the host link
+        raise ValueError("out must be a CUDA tensor or a pinned host tensor")
     N.check(N.lib().fpssft_synthesize(N.ptr(freqs.contiguous()), N.ptr(amps.contiguous()),
                                       N.ptr(counts.contiguous()), B, k_cap,
                                       C_ref(N.make_shape(shape.dims)), N.ptr(out),

@@ -1,0 +1,88 @@
+"""Pinned-host batches (hostpath.HostBatchRunner): every path an instance can
+take -- gathered in place from host memory (zero copy), or copied through the
+double-buffered device chunks -- gives bit-identical outputs to the
+device-resident run, and config-5 images written back to the host equal the
+device re-synthesis."""
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1711_11407_b200 as P  # noqa: E402
+from paper_1711_11407_b200 import ops  # noqa: E402
+from paper_1711_11407_b200 import workloads as W  # noqa: E402
+from paper_1711_11407_b200.hostpath import HostBatchRunner  # noqa: E402
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+DEV = torch.device("cuda:0")
+
+
+def _cubes(cfg_id, count):
+    w = W.CONFIGS[cfg_id]
+    spectra = W.make_spectra(w, count, 0)
+    cubes = W.synthesize_batch_torch(w.dims, spectra, DEV, w.noise_var, noise_seed=w.seed)
+    cfg = P.FpsSftConfig(seed=cfg_id, **P.PROFILES[w.profile])
+    return w, cubes, cfg
+
+
+@pytest.mark.parametrize("mode,frac", [("copy", None), ("zero_copy", None), ("split", 0.4),
+                                       ("auto", None)])
+@pytest.mark.parametrize("cfg_id,count,k_cap", [(2, 37, 128), (4, 5, 2048), (3, 9, 512)])
+def test_host_paths_match_device(cfg_id, count, k_cap, mode, frac):
+    w, cubes, cfg = _cubes(cfg_id, count)
+    shape = P.CubeShape(w.dims)
+    dev_run = P.BatchRunner(shape, cfg, count, k_cap=k_cap, device=DEV)
+    dev_run.run(cubes)
+    want = {k: v.cpu() for k, v in dev_run.out.items() if v is not None}
+    host = torch.empty(cubes.shape, dtype=cubes.dtype, pin_memory=True)
+    host.copy_(cubes)
+    hr = HostBatchRunner(shape, cfg, count, k_cap=k_cap, device=DEV, mode=mode,
+                         zero_copy_fraction=frac, chunk=4)  # several chunks per batch
+    for _ in range(2):  # auto: the second run splits with the learnt sample count
+        got = hr.run(host)
+        for k in want:
+            assert torch.equal(got[k], want[k]), k
+    if mode == "zero_copy":
+        assert hr.split_count() == count
+    if mode == "copy":
+        assert hr.split_count() == 0
+
+
+def test_pinned_host_tensor_runs_in_place():
+    w, cubes, cfg = _cubes(2, 16)
+    shape = P.CubeShape(w.dims)
+    r = P.BatchRunner(shape, cfg, 16, k_cap=128, device=DEV)
+    r.run(cubes)
+    want = r.out["amps"].clone()
+    host = cubes.cpu().pin_memory()
+    r.run(host)
+    assert torch.equal(r.out["amps"], want)
+    with pytest.raises(ValueError):
+        r.run(cubes.cpu())  # pageable host memory is not device-accessible
+
+
+def test_cfg5_images_to_pinned_host():
+    w, cubes, cfg = _cubes(5, 6)
+    shape = P.CubeShape(w.dims)
+    r = P.BatchRunner(shape, cfg, 6, k_cap=1024, device=DEV)
+    want = ops.synthesize(r.run(cubes)).cpu()
+    host = torch.empty(cubes.shape, dtype=cubes.dtype, pin_memory=True)
+    host.copy_(cubes)
+    for mode, frac in (("copy", None), ("split", 0.5)):
+        images = torch.zeros(cubes.shape, dtype=cubes.dtype, pin_memory=True)
+        hr = HostBatchRunner(shape, cfg, 6, k_cap=1024, device=DEV, mode=mode,
+                             zero_copy_fraction=frac, chunk=2)
+        hr.run(host, images)
+        assert torch.equal(images, want), mode
+
+
+def test_tune_picks_a_measured_fraction():
+    w, cubes, cfg = _cubes(2, 64)
+    host = torch.empty(cubes.shape, dtype=cubes.dtype, pin_memory=True)
+    host.copy_(cubes)
+    hr = HostBatchRunner(P.CubeShape(w.dims), cfg, 64, k_cap=128, device=DEV, chunk=16)
+    f = hr.tune(host, fractions=[0.0, 0.5, 1.0])
+    assert f in (0.0, 0.5, 1.0) and hr.mode == "split" and hr.tuned["fraction"] == f

@@ -168,3 +168,19 @@ def test_sweep_seeds_and_generator_match_reference():  # oracle.py:88-139, 215-2
         order = np.lexsort(f.T[::-1])
         np.testing.assert_array_equal(f[order], ops[f"{e['key']}/freqs"])
         np.testing.assert_array_equal(a[order], ops[f"{e['key']}/amps"])
+
+
+def test_zero_copy_split_model():
+    from paper_1711_11407_b200.hostpath import zero_copy_split
+
+    # config 2: ~2300 of 65536 samples per instance -> mostly zero copy
+    f2 = zero_copy_split(2322.0, 256 * 256)
+    assert 0.5 < f2 < 1.0
+    # config 4: 1 % sampled -> almost all zero copy
+    assert zero_copy_split(21972.0, 1024 * 2048) > 0.8
+    # sampling every sample many times over -> copy everything
+    assert zero_copy_split(1e9, 64) == 0.0
+    assert zero_copy_split(0.0, 64) == 1.0
+    # monotone in the sample count
+    fs = [zero_copy_split(s, 512 * 512) for s in (1e3, 1e4, 1e5, 1e6)]
+    assert fs == sorted(fs, reverse=True)
