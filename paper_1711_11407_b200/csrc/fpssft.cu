@@ -31,6 +31,15 @@
 #ifndef FPSSFT_SYNTH_WARPFFT
 #define FPSSFT_SYNTH_WARPFFT 1  // per-warp row FFTs in the static synthesis kernel
 #endif
+#ifndef FPSSFT_SYNTH_REG
+#define FPSSFT_SYNTH_REG 1  // float32 512-point rows: register-FFT synthesis kernel
+#endif
+#ifndef FPSSFT_SYNTH_RC
+#define FPSSFT_SYNTH_RC 16  // rows per chunk of synth512_kernel
+#endif
+#ifndef FPSSFT_SYNTH_DB
+#define FPSSFT_SYNTH_DB 0  // synth512_kernel: double-buffered chunks (measured slower)
+#endif
 #ifndef SYNTH_RC
 #define SYNTH_RC 16  // rows per chunk of the static 512-point synthesis kernel
 #endif
@@ -863,6 +872,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
 
 #include "fpssft_team.cuh"
 #include "fpssft_warp_il.cuh"
+#include "fpssft_synth.cuh"
 
 // ------------------------------------------------------------ re-synthesis
 // x(n) = sum_i a_i exp(+2 pi j sum_k n_k m_ik / N_k) on the full grid of
@@ -1842,6 +1852,23 @@ int fpssft_synthesize(const int32_t *freqs, const double *amps, const int32_t *c
     if ((rc = make_geo(&row, &gr)) != FPSSFT_OK) return rc;
     const int NT = 256, NL = gr.L;
     const int cs = precision == FPSSFT_F64 ? 16 : 8;
+    if (FPSSFT_SYNTH_REG && precision != FPSSFT_F64 && gc.D == 2 && NL == 512 &&
+        gc.N[0] % FPSSFT_SYNTH_RC == 0 && (long long)gc.L * gc.N[0] < (1LL << 32)) {
+        // config 5's 512 x 512 images in float32: register row FFTs (fpssft_synth.cuh)
+        const size_t smr = align16((size_t)(FPSSFT_SYNTH_DB ? 2 : 1) * FPSSFT_SYNTH_RC * synth::VS * 8) +
+                           align16((size_t)gc.L * 8) +
+                           align16((size_t)k_cap * 8) + 2 * align16((size_t)k_cap * 4) +
+                           align16((size_t)513 * 4) + align16((size_t)512 * 4) + 64 * 8;
+        if ((long long)smr <= SMEM_PER_CTA) {
+            auto k = synth::synth512_kernel<FPSSFT_SYNTH_RC, 256, (bool)FPSSFT_SYNTH_DB>;
+            cudaError_t e =
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(synth512)");
+            k<<<(unsigned)batch, 256, smr, (cudaStream_t)stream>>>(freqs, amps, counts, k_cap, gc,
+                                                                   (float2 *)cubes, batch_stride);
+            return check_launch("synth512_kernel");
+        }
+    }
     if (gc.D == 2 && NL == 512 && gc.N[0] % SYNTH_RC == 0 &&
         (long long)gc.L * gc.N[0] < (1LL << 32)) {
         // compile-time variant: config 5's 512 x 512 images, SYNTH_RC rows per

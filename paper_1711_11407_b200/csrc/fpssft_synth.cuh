@@ -1,0 +1,275 @@
+// Re-synthesis of 2-D grids with 512-point rows (config 5: 512 x 512 images),
+// float32: x(n0, n1) = sum_i a_i root_L[(c0 n0 m0_i + c1 n1 m1_i) mod L], the
+// dense form of SyntheticSource.sample_many (reference core.py:176-217).
+//
+// One CTA per image, RC rows per chunk:
+//   sparse part  V[r][m1] = sum over entries of column m1 (entry order) of
+//                a * root_L[c0 n0 m0 mod L]  -- one thread per column, every
+//                column written (zeros included), so V needs no clearing;
+//   dense part   x[r][n1] = sum_m1 V[r][m1] e^{+2 pi i n1 m1 / 512} -- one
+//                warp per row, in registers: m1 = 32a + b, n1 = c + 16d.
+//                Lane b: 16-point DFT over a (in registers), twiddle
+//                e^{2 pi i b c / 512} (per-lane constants), one shared-memory
+//                exchange (stride 34: both sides conflict-free) to lanes
+//                (c, h) = (lane/2, lane%2) holding b = 2 beta + h, 16-point
+//                DFT over beta, radix-2 combine with the partner lane (shfl)
+//                gives n1 = c + 16 d' + 256 h: every warp store writes two
+//                full 128-byte lines, straight from registers.
+// Shared-memory traffic per row: 3 x 4 KB (V read, exchange write + read),
+// against 6 x 4 KB + twiddle loads for three radix-8 passes in shared memory.
+// Bound: the HBM write of the grid (2 MiB per 512 x 512 frame).
+
+// (included inside namespace fpssft)
+namespace synth {
+
+// constexpr e^{+2 pi i j / 16} and e^{+2 pi i j / 32}
+__device__ __forceinline__ float2 w16(int j) {
+    constexpr float C[16] = {1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                             0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                             -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f,
+                             0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
+    return make_float2(C[j & 15], C[(j + 12) & 15]);  // (cos, sin): sin x = cos(x - pi/2)
+}
+__device__ __forceinline__ float2 w32(int j) {
+    constexpr float C[32] = {
+        1.0f, 0.98078528040323044f, 0.92387953251128674f, 0.83146961230254524f,
+        0.70710678118654752f, 0.55557023301960218f, 0.38268343236508977f, 0.19509032201612826f,
+        0.0f, -0.19509032201612826f, -0.38268343236508977f, -0.55557023301960218f,
+        -0.70710678118654752f, -0.83146961230254524f, -0.92387953251128674f, -0.98078528040323044f,
+        -1.0f, -0.98078528040323044f, -0.92387953251128674f, -0.83146961230254524f,
+        -0.70710678118654752f, -0.55557023301960218f, -0.38268343236508977f, -0.19509032201612826f,
+        0.0f, 0.19509032201612826f, 0.38268343236508977f, 0.55557023301960218f,
+        0.70710678118654752f, 0.83146961230254524f, 0.92387953251128674f, 0.98078528040323044f};
+    return make_float2(C[j & 31], C[(j + 24) & 31]);
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 mul_i(float2 a) { return make_float2(-a.y, a.x); }  // * (+i)
+
+// X[k] = sum_n x[n] e^{+2 pi i n k / 4}
+__device__ __forceinline__ void dft4(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
+    const float2 t0 = cadd(x0, x2), t1 = csub(x0, x2), t2 = cadd(x1, x3), t3 = mul_i(csub(x1, x3));
+    x0 = cadd(t0, t2);
+    x2 = csub(t0, t2);
+    x1 = cadd(t1, t3);
+    x3 = csub(t1, t3);
+}
+
+// In place, natural order in and out: v[k] <- sum_n v[n] e^{+2 pi i n k / 16}
+// (n = 4 n1 + n2, k = k1 + 4 k2: DFT-4 over n1, twiddle, DFT-4 over n2).
+__device__ __forceinline__ void dft16(float2 *v) {
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
+    // v[4 k1 + n2] now holds Y[n2][k1]; twiddle by e^{2 pi i n2 k1 / 16}
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+        for (int k1 = 1; k1 < 4; ++k1) v[4 * k1 + n2] = cmul(v[4 * k1 + n2], w16(n2 * k1));
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+    // v[4 k1 + k2] holds X[k1 + 4 k2]: transpose the 4 x 4 index (registers only)
+    float2 t[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = v[i];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
+}
+
+constexpr int VS = 544;  // row stride of V (cpx): holds the 16 x 34 exchange tile
+
+template <int RC, int NT, bool DB>
+__global__ void __launch_bounds__(NT, 2) synth512_kernel(const int *__restrict__ freqs,
+                                                         const double *__restrict__ amps,
+                                                         const int *__restrict__ counts, int k_cap,
+                                                         Geo gc, float2 *out, long long out_stride) {
+    constexpr int NL = 512, NW = NT / 32, RW = RC / NW;
+    static_assert(RC % NW == 0 && NL % NT == 0, "whole rows per warp, whole column passes");
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int L = gc.L, N0 = gc.N[0], c0 = gc.cof[0];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long inst = blockIdx.x;
+    const int n = min(counts[inst], k_cap);
+    size_t o = 0;
+    float2 *V = (float2 *)(sm + o);      o = align16(o + (size_t)(DB ? 2 : 1) * RC * VS * 8);
+    float2 *rootsL = (float2 *)(sm + o); o = align16(o + (size_t)L * 8);
+    float2 *samp = (float2 *)(sm + o);   o = align16(o + (size_t)k_cap * 8);  // column-sorted
+    int *sm0 = (int *)(sm + o);          o = align16(o + (size_t)k_cap * 4);
+    int *ecol = (int *)(sm + o);         o = align16(o + (size_t)k_cap * 4);
+    int *col_start = (int *)(sm + o);    o = align16(o + (size_t)(NL + 1) * 4);
+    int *col_fill = (int *)(sm + o);     o = align16(o + (size_t)NL * 4);
+    int *ired = (int *)(sm + o);
+
+    for (int j = tid; j < L; j += NT) {
+        double s, c;
+        sincospi(2.0 * (double)j / (double)L, &s, &c);
+        rootsL[j] = make_float2((float)c, (float)s);
+    }
+    for (int c = tid; c < NL; c += NT) col_fill[c] = 0;
+    __syncthreads();
+    for (int e = tid; e < n; e += NT) {
+        const int c = freqs[(inst * k_cap + e) * 2 + 1];
+        ecol[e] = c;
+        atomicAdd(&col_fill[c], 1);
+    }
+    __syncthreads();
+    int carry = 0;
+    for (int j0 = 0; j0 < NL; j0 += NT) {  // column -> range of the column-sorted entries
+        const int c = j0 + tid;
+        const int cnt = c < NL ? col_fill[c] : 0;
+        int tot;
+        const int pre = block_exscan(cnt, ired, &tot);
+        if (c < NL) {
+            col_start[c] = carry + pre;
+            col_fill[c] = carry + pre;
+        }
+        carry += tot;
+    }
+    if (tid == 0) col_start[NL] = carry;
+    __syncthreads();
+    // entry order inside a column is the input order (deterministic sums):
+    // scatter by column, insertion-sort each (short) column, then gather the
+    // entries' m0 and amplitude into column-sorted arrays
+    for (int e = tid; e < n; e += NT) {
+        const int c = ecol[e];
+        sm0[atomicAdd(&col_fill[c], 1)] = e;  // sm0 holds entry ids for now
+    }
+    __syncthreads();
+    for (int c = tid; c < NL; c += NT) {
+        const int st = col_start[c], en = col_start[c + 1];
+        for (int i = st + 1; i < en; ++i) {
+            const int v = sm0[i];
+            int j = i - 1;
+            while (j >= st && sm0[j] > v) {
+                sm0[j + 1] = sm0[j];
+                --j;
+            }
+            sm0[j + 1] = v;
+        }
+    }
+    __syncthreads();
+    for (int p = tid; p < n; p += NT) {
+        const long long src = inst * k_cap + sm0[p];
+        samp[p] = make_float2((float)amps[src * 2], (float)amps[src * 2 + 1]);
+        ecol[p] = freqs[src * 2];  // m0, column-sorted
+    }
+    __syncthreads();
+    // columns by descending entry count (bucket min(count, 31)); the order
+    // inside a bucket does not matter: one thread sums one column
+    int *corder = col_fill;  // col_fill is free now
+    if (tid < 32) ired[tid] = 0;
+    __syncthreads();
+    for (int c = tid; c < NL; c += NT)
+        atomicAdd(&ired[31 - min(col_start[c + 1] - col_start[c], 31)], 1);
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the 32 bucket sizes -> cursors
+        const int v = ired[tid];
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, x, o);
+            if (tid >= o) x += y;
+        }
+        ired[tid] = x - v;
+    }
+    __syncthreads();
+    for (int c = tid; c < NL; c += NT)
+        corder[atomicAdd(&ired[31 - min(col_start[c + 1] - col_start[c], 31)], 1)] = c;
+    __syncthreads();
+    // per-lane twiddles e^{2 pi i lane c / 512}, c = 0..15 (exact table phases)
+    float2 tw[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) tw[c] = rootsL[lane * c * (L / NL)];
+    const unsigned long long magicL = ~0ULL / (unsigned)L + 1ULL;
+    float2 *img = out + inst * out_stride;
+    // sparse part of chunk r0 into buffer Vb (every column, zeros included),
+    // columns in descending entry count so the lanes of a warp run equally
+    // long loops; each entry's RC row phasors a w^{u0 + r step} by recurrence
+    // from the exact table value at the chunk's first row (|error| ~ RC ulp)
+    auto sparse = [&](int r0, float2 *Vb) {
+        const unsigned r0L = fastmod((unsigned)c0 * (unsigned)r0, magicL, (unsigned)L);
+        for (int i = 0; i < NL / NT; ++i) {
+            // snake over the count-sorted columns: warp w takes group w of even
+            // passes and group NW-1-w of odd ones, evening out the warps' loads
+            const int g = (i & 1) ? NW - 1 - warp : warp;
+            const int c = corder[i * NT + g * 32 + lane];
+            float2 acc[RC];
+#pragma unroll
+            for (int r = 0; r < RC; ++r) acc[r] = make_float2(0.f, 0.f);
+            const int en = col_start[c + 1];
+            for (int p = col_start[c]; p < en; ++p) {
+                const unsigned m0 = (unsigned)ecol[p];
+                const unsigned step = fastmod((unsigned)c0 * m0, magicL, (unsigned)L);
+                const unsigned u = fastmod(r0L * m0, magicL, (unsigned)L);
+                float2 z = cmul(samp[p], rootsL[u]);
+                const float2 ws = rootsL[step];
+#pragma unroll
+                for (int r = 0; r < RC; ++r) {
+                    acc[r] = cadd(acc[r], z);
+                    if (r + 1 < RC) z = cmul(z, ws);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < RC; ++r) Vb[r * VS + c] = acc[r];
+        }
+    };
+    // dense part of chunk r0 from buffer Vb: one warp per row
+    auto dense = [&](int r0, float2 *Vb) {
+#pragma unroll 1
+        for (int rr = 0; rr < RW; ++rr) {
+            const int r = warp * RW + rr;
+            float2 *Vr = Vb + r * VS;
+            float2 v[16];
+#pragma unroll
+            for (int a = 0; a < 16; ++a) v[a] = Vr[32 * a + lane];
+            dft16(v);
+#pragma unroll
+            for (int c = 1; c < 16; ++c) v[c] = cmul(v[c], tw[c]);
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 16; ++c) Vr[34 * c + lane] = v[c];
+            __syncwarp();
+            const int cc = lane >> 1, h = lane & 1;
+#pragma unroll
+            for (int b = 0; b < 16; ++b) v[b] = Vr[34 * cc + 2 * b + h];
+            dft16(v);
+            float2 *row = img + (long long)(r0 + r) * NL + cc + 256 * h;
+            const float sg = h ? -1.f : 1.f;
+#pragma unroll
+            for (int d = 0; d < 16; ++d) {
+                // lane h=1 holds E1 and sends t E1; lane h=0 holds E0 and sends E0:
+                // out = E0 + t E1 (h=0) = p + y;  E0 - t E1 (h=1) = p - y
+                const float2 tv = cmul(w32(d), v[d]);
+                const float2 y = h ? tv : v[d];
+                const float2 p = make_float2(__shfl_xor_sync(FULL, y.x, 1),
+                                             __shfl_xor_sync(FULL, y.y, 1));
+                __stcs(row + 16 * d, make_float2(fmaf(sg, y.x, p.x), fmaf(sg, y.y, p.y)));
+            }
+        }
+    };
+    // two V buffers: chunk k+1's sparse part and chunk k's dense part run in
+    // the same phase, so one barrier per chunk and the sparse part's uneven
+    // per-warp work is absorbed by the (even) dense work
+    if constexpr (DB) {
+        sparse(0, V);
+        __syncthreads();
+        for (int k = 0, r0 = 0; r0 < N0; ++k, r0 += RC) {
+            if (r0 + RC < N0) sparse(r0 + RC, V + ((k + 1) & 1) * RC * VS);
+            dense(r0, V + (k & 1) * RC * VS);
+            __syncthreads();
+        }
+    } else {
+        for (int r0 = 0; r0 < N0; r0 += RC) {
+            sparse(r0, V);
+            __syncthreads();
+            dense(r0, V);
+            __syncthreads();
+        }
+    }
+}
+
+}  // namespace synth
