@@ -106,14 +106,21 @@ def _segments_per_launch(shape, schedule, iterations, sched_index=None, seg=8):
     return total
 
 
-def _traffic(workload_name):
-    """DRAM bytes per launch from the committed ncu capture, if any."""
+def _traffic(workload_name, batch=None):
+    """DRAM bytes per launch from the committed ncu capture, if any (a capture
+    of a subset, "<cfgN>_recover_subset<n>", scaled to ``batch`` instances)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             d = json.load(fh)
-        return d.get(workload_name)
     except Exception:
         return None
+    if workload_name in d:
+        return d[workload_name]
+    pre = workload_name.split("_")[0] + "_recover_subset"
+    for k, v in d.items():
+        if k.startswith(pre) and batch:
+            return int(v * batch / int(k[len(pre):]))
+    return None
 
 
 # ---------------------------------------------------------------- CPU arm
@@ -266,6 +273,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "warp", "cta"],
+                    help="kernel family (auto: the planner's choice for this batch)")
     ap.add_argument("--batch", type=int, default=None, help="override instances per rank")
     ap.add_argument("--k-cap", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -324,14 +333,16 @@ def main():
     cubes = W.synthesize_batch_torch(w.dims, spectra, dev, w.noise_var,
                                      noise_seed=w.seed * 1000003 + b0)
     torch.cuda.synchronize()
-    runner = P.BatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision, device=dev)
+    runner = P.BatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision, device=dev,
+                           mode=args.mode)
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     res = runner.run(cubes)
     while int((res.terminated_by == 3).sum()) > 0:  # k_cap overflow: widen, untimed
         k_cap *= 2
-        runner = P.BatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision, device=dev)
+        runner = P.BatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision, device=dev,
+                               mode=args.mode)
         res = runner.run(cubes)
     for _ in range(max(3, args.warmup)):
         res = runner.run(cubes)
@@ -395,7 +406,7 @@ def main():
     rec_ms = sum(recover_ms) / args.steps
     achieved = bytes_per_launch / (rec_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": _traffic(w.name),
+                "frac": achieved / peak, "traffic": _traffic(w.name, B),
                 "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": bytes_per_launch,
                 "kernel": "recover (" + runner.plan["mode"] + " per instance)",

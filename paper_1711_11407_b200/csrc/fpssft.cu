@@ -1529,7 +1529,13 @@ const void *il_kernel_for(const Geo &g, int precision, int ni) {
 // instance), or nullptr if the shape has none.
 template <class R>
 const void *team_kernel_for_t(const Geo &g, int *nt) {
-    if (!g.off32 || g.D != 2) return nullptr;
+    if (!g.off32) return nullptr;
+    if (g.D == 3 && g.L == 64) {  // config 3: small batches leave SMs idle in warp mode
+        if (*nt == 64) return (const void *)recover_team_kernel<R, 64, 3, 64>;
+        *nt = 128;
+        return (const void *)recover_team_kernel<R, 64, 3, 128>;
+    }
+    if (g.D != 2) return nullptr;
     if (g.L == 2048) {
         if (*nt == 512) return (const void *)recover_team_kernel<R, 2048, 2, 512>;
         *nt = 1024;
