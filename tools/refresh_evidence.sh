@@ -24,4 +24,12 @@ timeout 900 $N -o $O/cfg4 $B --config 4 > $O/ncu_cfg4.log 2>&1
 timeout 900 $N -o $O/cfg5_recover $B --config 5 --batch 2048 --no-synth > $O/ncu_cfg5.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:synth -c 1 \
   -o $O/cfg5_synth python tools/synth_profile.py --reps 1 > $O/ncu_synth.log 2>&1
+# reports are ~25 MB each (gpurun brings back <= 64 MiB): keep CSV exports
+for r in $O/*.ncu-rep; do
+  b=${r%.ncu-rep}
+  ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
+  ncu -i $r --page source --csv --print-source=sass > $b.sass.csv 2>/dev/null
+  gzip -f $b.sass.csv
+  rm -f $r
+done
 ls -la $O

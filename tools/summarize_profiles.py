@@ -2,7 +2,7 @@
 """Summarise a gpurun evidence directory into profiles/: ncu --set full
 captures (key metrics + stall mix), DRAM traffic per launch, launch list.
 
-usage: tools/summarize_profiles.py <run dir> <round tag> name=report.ncu-rep ...
+usage: tools/summarize_profiles.py <run dir> <round tag> name=report.ncu-rep|report.raw.csv ...
 """
 import collections
 import csv
@@ -22,8 +22,11 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
 def raw(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.endswith(".csv"):  # a `--page raw --csv` export of the report
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
     return {h: (v, u) for h, u, v in zip(rows[0], rows[1], rows[2])}
 
