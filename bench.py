@@ -412,6 +412,10 @@ def main():
                 "kernel": "recover (" + runner.plan["mode"] + " per instance)",
                 "kernel_ms": rec_ms,
                 "note": "achieved = sum(samples_used)*8 B gathered per launch / mean launch time"}
+    if roofline["traffic"]:
+        # useful sample bytes per DRAM byte moved (ceiling ~0.33 for scattered 8-byte
+        # samples in 64-byte segments)
+        roofline["sector_efficiency"] = bytes_per_launch / roofline["traffic"]
     probe = _probe_rate()
     segs = _segments_per_launch(shape, runner.schedule_host, iters)
     roofline["gather"] = {

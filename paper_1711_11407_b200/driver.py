@@ -191,21 +191,50 @@ class BatchResult:
                               terminated_by=term, iteration_log=log)
 
 
+class Outputs(dict):
+    """The per-instance output tensors, all views of one allocation ``buf``
+    (so a whole batch's results move host<->device in one copy)."""
+
+    buf: "object" = None
+
+
+_OUT_FIELDS = (("freqs", "int32", 4), ("amps", "complex128", 16), ("count", "int32", 4),
+               ("iterations", "int32", 4), ("samples_used", "int64", 8),
+               ("terminated_by", "int32", 4), ("iter_stats", "int32", 4))
+
+
 def allocate_outputs(batch: int, shape: CubeShape, k_cap: int, t_max: int, device,
-                     iter_stats: bool = False) -> dict:
+                     iter_stats: bool = False, pin: bool = False) -> Outputs:
+    """Zeroed output tensors for ``batch`` instances, packed in one buffer
+    (pinned host memory with ``pin``)."""
     import torch
 
-    kw = dict(device=device)
-    return dict(
-        freqs=torch.zeros((batch, k_cap, shape.ndim), dtype=torch.int32, **kw),
-        amps=torch.zeros((batch, k_cap), dtype=torch.complex128, **kw),
-        count=torch.zeros(batch, dtype=torch.int32, **kw),
-        iterations=torch.zeros(batch, dtype=torch.int32, **kw),
-        samples_used=torch.zeros(batch, dtype=torch.int64, **kw),
-        terminated_by=torch.zeros(batch, dtype=torch.int32, **kw),
-        iter_stats=(torch.zeros((batch, t_max, 3), dtype=torch.int32, **kw)
-                    if iter_stats else None),
-    )
+    shapes = {"freqs": (batch, k_cap, shape.ndim), "amps": (batch, k_cap), "count": (batch,),
+              "iterations": (batch,), "samples_used": (batch,), "terminated_by": (batch,),
+              "iter_stats": (batch, t_max, 3) if iter_stats else None}
+    offs, o = {}, 0
+    for name, _, size in _OUT_FIELDS:
+        if shapes[name] is None:
+            continue
+        o = (o + 15) // 16 * 16
+        offs[name] = o
+        n = 1
+        for d in shapes[name]:
+            n *= d
+        o += n * size
+    buf = torch.zeros(max(16, o), dtype=torch.uint8, device=device, pin_memory=pin)
+    out = Outputs()
+    for name, dt, size in _OUT_FIELDS:
+        if shapes[name] is None:
+            out[name] = None
+            continue
+        n = 1
+        for d in shapes[name]:
+            n *= d
+        out[name] = buf[offs[name]:offs[name] + n * size].view(getattr(torch, dt)).view(
+            shapes[name])
+    out.buf = buf
+    return out
 
 
 def _schedule_tensor(schedule, shape: CubeShape, t_max: int, device):

@@ -87,10 +87,7 @@ class HostBatchRunner:
         self.chunk = int(chunk or max(1, min(self.batch, chunk_bytes // cube_bytes)))
         self._schedule = schedule
         self._sched_index = None if sched_index is None else np.asarray(sched_index, np.int32)
-        self.out = allocate_outputs(self.batch, shape, k_cap, self.t_max, "cpu")
-        for k, v in list(self.out.items()):
-            if v is not None:
-                self.out[k] = v.pin_memory()
+        self.out = allocate_outputs(self.batch, shape, k_cap, self.t_max, "cpu", pin=True)
         self.last_mean_samples: float | None = None
         self.tuned: dict | None = None
         self._runners: dict = {}
@@ -158,6 +155,9 @@ class HostBatchRunner:
                                               dtype=torch.complex64, device=self.device))
 
     def _copy_out(self, r: BatchRunner, b0: int, n: int):
+        if b0 == 0 and n == self.batch:  # same packed layout: one copy
+            self.out.buf.copy_(r.out.buf, non_blocking=True)
+            return
         for k, v in r.out.items():
             if v is not None:
                 self.out[k][b0:b0 + n].copy_(v, non_blocking=True)
