@@ -273,6 +273,10 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--layout", default="batch_major", choices=["batch_major", "interleaved"],
+                    help="HBM layout of the batch: [B, *dims], or [B/G, *dims, G] with G "
+                         "instances interleaved sample by sample (--group)")
+    ap.add_argument("--group", type=int, default=8)
     ap.add_argument("--mode", default="auto", choices=["auto", "warp", "cta"],
                     help="kernel family (auto: the planner's choice for this batch)")
     ap.add_argument("--batch", type=int, default=None, help="override instances per rank")
@@ -333,19 +337,22 @@ def main():
     cubes = W.synthesize_batch_torch(w.dims, spectra, dev, w.noise_var,
                                      noise_seed=w.seed * 1000003 + b0)
     torch.cuda.synchronize()
+    group = args.group if args.layout == "interleaved" else 1
+    run_cubes = P.interleave(cubes, group) if group > 1 else cubes
+    torch.cuda.synchronize()
     runner = P.BatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision, device=dev,
-                           mode=args.mode)
+                           mode=args.mode, group=group)
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    res = runner.run(cubes)
+    res = runner.run(run_cubes)
     while int((res.terminated_by == 3).sum()) > 0:  # k_cap overflow: widen, untimed
         k_cap *= 2
         runner = P.BatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision, device=dev,
-                               mode=args.mode)
-        res = runner.run(cubes)
+                               mode=args.mode, group=group)
+        res = runner.run(run_cubes)
     for _ in range(max(3, args.warmup)):
-        res = runner.run(cubes)
+        res = runner.run(run_cubes)
     torch.cuda.synchronize()
     count = res.count.cpu().numpy()
     term = res.terminated_by.cpu().numpy()
@@ -364,7 +371,7 @@ def main():
     t_end = time.perf_counter() + args.load_seconds
     while time.perf_counter() < t_end:  # sustained load so sampled clocks reflect it
         for _ in range(10):
-            runner.run(cubes)
+            runner.run(run_cubes)
         torch.cuda.synchronize()
 
     # ---- timed region: K steps, L2 flushed before each, events around each
@@ -375,14 +382,14 @@ def main():
     mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if synth:
-        ops.synthesize(runner.run(cubes), out=img)
+        ops.synthesize(runner.run(run_cubes), out=img)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     for i in range(args.steps):
         flush.fill_(i)
         starts[i].record(stream)
-        r = runner.run(cubes)
+        r = runner.run(run_cubes)
         mids[i].record(stream)
         if synth:
             ops.synthesize(r, out=img)

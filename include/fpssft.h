@@ -91,6 +91,18 @@ int fpssft_run_batch(const void *cubes, int64_t batch, int64_t batch_stride,
                      const int32_t *schedule, const int32_t *sched_index, int32_t n_sched,
                      const fpssft_out *out, void *stream);
 
+/* The same loop over a batch stored with `group` instances interleaved sample
+ * by sample: layout [ceil(B/group), *dims, group] complex64 (the 64-byte DRAM
+ * segment of a sample then serves 8 instances at group = 8).  Instance b's
+ * sample n sits at cubes + (b / group) * group_stride + (b % group) +
+ * sum_k n_k * shape->strides[k] (elements; the strides include the factor
+ * group).  group = 1 is fpssft_run_batch.  Same outputs, same errors. */
+int fpssft_run_batch_grouped(const void *cubes, int64_t batch, int32_t group,
+                             int64_t group_stride, const fpssft_shape *shape,
+                             const fpssft_params *params, const int32_t *schedule,
+                             const int32_t *sched_index, int32_t n_sched, const fpssft_out *out,
+                             void *stream);
+
 /*
  * D+1 line spectra of one iteration per instance.  Replaces
  *   [dft_forward(extract_line(DenseSource(cube), LineParams(alpha, off, L)))

@@ -9,8 +9,8 @@ consumes and produces, plus batched and per-step device entry points.
 from .core import (CubeShape, DenseSource, FreqIndex, SignalSource, Sinusoid, SparseSpectrum,
                    make_dense_source, spectra_match)
 from .driver import (PROFILES, BatchResult, BatchRunner, FpsSftConfig, IterationStats,
-                     RecoveryReport, default_max_iterations, fps_sft, fps_sft_batch, materialize,
-                     max_k_cap)
+                     RecoveryReport, default_max_iterations, fps_sft, fps_sft_batch, interleave,
+                     materialize, max_k_cap)
 from .baseline import baseline_sft
 from .imaging import GrayImage, reconstruct_sparse_image, synthetic_phantom
 from .large import fps_sft_large
@@ -25,6 +25,6 @@ __all__ = ["ALGORITHMS", "BatchResult", "BatchRunner", "CubeShape", "DenseSource
            "FpsSftConfig", "FreqIndex", "GrayImage", "IterationStats", "PROFILES",
            "RecoveryReport", "fps_sft_large", "reconstruct_sparse_image", "synthetic_phantom",
            "SignalSource", "Sinusoid", "SparseSpectrum", "baseline_sft", "bins_of_frequencies",
-           "default_max_iterations", "fps_sft", "fps_sft_batch", "is_valid_slope",
+           "default_max_iterations", "fps_sft", "fps_sft_batch", "interleave", "is_valid_slope",
            "make_dense_source", "materialize", "max_k_cap", "sample_slope",
            "schedule_from_seed", "spectra_match", "valid_slopes"]

@@ -20,7 +20,7 @@ MODES = {"auto": MODE_AUTO, "cta": MODE_CTA, "warp": MODE_WARP}
 TERM_NAMES = {0: "residual_clean", 1: "stall", 2: "max_iterations", 3: "k_cap_overflow",
               -1: "invalid_schedule"}
 
-EXPORTS = ("fpssft_run_batch", "fpssft_line_spectra", "fpssft_gather_lines", "fpssft_dft_forward",
+EXPORTS = ("fpssft_run_batch", "fpssft_run_batch_grouped", "fpssft_line_spectra", "fpssft_gather_lines", "fpssft_dft_forward",
            "fpssft_synthesize",
            "fpssft_decode_spectra", "fpssft_project_onto_bins", "fpssft_smem_bytes",
            "fpssft_block_threads", "fpssft_plan", "fpssft_launches_per_batch",
@@ -68,6 +68,8 @@ def lib() -> C.CDLL:
         P, I32, I64 = C.c_void_p, C.c_int32, C.c_int64
         h.fpssft_run_batch.argtypes = [P, I64, I64, C.POINTER(Shape), C.POINTER(Params), P, P,
                                        I32, C.POINTER(Out), P]
+        h.fpssft_run_batch_grouped.argtypes = [P, I64, I32, I64, C.POINTER(Shape),
+                                               C.POINTER(Params), P, P, I32, C.POINTER(Out), P]
         h.fpssft_line_spectra.argtypes = [P, I64, I64, C.POINTER(Shape), P, I32, P, I32, P]
         h.fpssft_dft_forward.argtypes = [P, I64, I32, P, I32, P]
         h.fpssft_gather_lines.argtypes = [P, I32, I64, I64, C.POINTER(Shape), P, I32, P, I32, P]

@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(1024, 1) recover_kernel(const float2 *__restri
 
     const int L = g.L, D = g.D, nl = g.nlines, NT = blockDim.x, tid = threadIdx.x;
     const int inst = blockIdx.x;
-    const float2 *cube = cubes + (long long)inst * batch_stride;
+    const float2 *cube = cube_base(cubes, (long long)inst, batch_stride, kn.group);
     int sidx = sched_index ? sched_index[inst] : 0;
     const bool sched_ok = sidx >= 0 && sidx < n_sched;
     if (!sched_ok) sidx = 0;
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     cpx<R> *scr_amp = (cpx<R> *)(base + lay.scr_amp);
 
     const int L = g.L, D = g.D, nl = g.nlines, H = lay.H;
-    const float2 *cube = cubes + inst * batch_stride;
+    const float2 *cube = cube_base(cubes, (long long)inst, batch_stride, kn.group);
     int sidx = sched_index ? sched_index[inst] : 0;
     const bool sched_ok = sidx >= 0 && sidx < n_sched;
     if (!sched_ok) sidx = 0;
@@ -1469,6 +1469,7 @@ int make_knobs(const fpssft_params *p, Knobs *k) {
     k->t_max = p->t_max;
     k->stall_limit = p->stall_limit;
     k->k_cap = p->k_cap;
+    k->group = 1;
     return FPSSFT_OK;
 }
 
@@ -1810,11 +1811,23 @@ int fpssft_run_batch(const void *cubes, int64_t batch, int64_t batch_stride,
                      const fpssft_shape *shape, const fpssft_params *params,
                      const int32_t *schedule, const int32_t *sched_index, int32_t n_sched,
                      const fpssft_out *out, void *stream) {
+    return fpssft_run_batch_grouped(cubes, batch, 1, batch_stride, shape, params, schedule,
+                                    sched_index, n_sched, out, stream);
+}
+
+int fpssft_run_batch_grouped(const void *cubes, int64_t batch, int32_t group,
+                             int64_t group_stride, const fpssft_shape *shape,
+                             const fpssft_params *params, const int32_t *schedule,
+                             const int32_t *sched_index, int32_t n_sched, const fpssft_out *out,
+                             void *stream) {
     Geo g;
     Knobs kn;
     int rc;
+    const int64_t batch_stride = group_stride;
     if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
     if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
+    if (group < 1 || group > 64) return fail(FPSSFT_EINVAL, "group must be in [1, 64]");
+    kn.group = group;
     set_noise_floor(&kn, g, params->precision);
     if (batch < 0) return fail(FPSSFT_EINVAL, "batch must be >= 0");
     if (batch > INT_MAX) return fail(FPSSFT_EINVAL, "batch exceeds the grid limit");

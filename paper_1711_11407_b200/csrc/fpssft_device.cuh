@@ -98,7 +98,17 @@ struct Knobs {
     double energy_floor, energy_floor_abs, residual_stop;
     double noise_coef;  // float32 rounding floor: coef * sqrt(sum |x|^2 over the D+1 lines)
     int t_max, stall_limit, k_cap;
+    int group;  // instances interleaved per sample (batch layout [B/group, *dims, group])
 };
+
+// Base of instance `inst`'s cube: batch layout [B/G, *dims, G] (G = kn.group
+// instances interleaved sample by sample; G = 1 is the plain [B, *dims]).
+template <class T>
+__device__ __forceinline__ const T *cube_base(const T *cubes, long long inst,
+                                              long long group_stride, int group) {
+    if (group == 1) return cubes + inst * group_stride;
+    return cubes + (inst / group) * group_stride + (inst % group);
+}
 
 // a mod d without division (Lemire): valid for any 32-bit a, d >= 1.
 __device__ __forceinline__ unsigned fastmod(unsigned a, unsigned long long M, unsigned d) {

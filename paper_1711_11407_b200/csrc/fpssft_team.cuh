@@ -50,8 +50,8 @@ __host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, 
     y.cand = u;      size_t b = align16(u + (size_t)L * 2);
     // the match_any projection's per-warp scratch also lives in this union
     const size_t c = align16(u + (size_t)(nt / 32) * 32 * ((MAXD + 1) * 4 + cs));
-    o = a > b ? a : b;
-    o = o > c ? o : c;
+    o = b > c ? b : c;
+    if (!FPSSFT_TEAM_PROJ) o = o > a ? o : a;  // the counting-sort projection's scratch
     y.red = o;       o = align16(o + 64 * 8);
     y.total = o;
     return y;
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
 
     const int tid = threadIdx.x, H = lay.H;
     const long long inst = blockIdx.x;
-    const float2 *cube = cubes + inst * batch_stride;
+    const float2 *cube = cube_base(cubes, (long long)inst, batch_stride, kn.group);
     int sidx = sched_index ? sched_index[inst] : 0;
     const bool sched_ok = sidx >= 0 && sidx < n_sched;
     if (!sched_ok) sidx = 0;

@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(128, 2) recover_warp_il_kernel(
         q.active = q.inst < batch;
         q.seq = -1;
         if (!q.active) continue;
-        q.cube = cubes + q.inst * batch_stride;
+        q.cube = cube_base(cubes, (long long)q.inst, batch_stride, kn.group);
         int sidx = sched_index ? sched_index[q.inst] : 0;
         const bool ok = sidx >= 0 && sidx < n_sched;
         q.sched = schedule + (long long)(ok ? sidx : 0) * kn.t_max * 2 * DC;

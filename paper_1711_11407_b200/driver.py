@@ -260,9 +260,12 @@ class BatchRunner:
 
     def __init__(self, shape: CubeShape, config: FpsSftConfig, batch: int, *, schedule=None,
                  sched_index=None, k_cap: int = 256, precision: str = "fp32",
-                 iter_stats: bool = False, device=None, mode: str = "auto"):
+                 iter_stats: bool = False, device=None, mode: str = "auto", group: int = 1):
         import torch
 
+        if not 1 <= int(group) <= 64:
+            raise ValueError("group must be in [1, 64]")
+        self.group = int(group)
         self.shape = shape
         self.config = config
         self.batch = int(batch)
@@ -308,24 +311,54 @@ class BatchRunner:
                              "(use fps_sft for other host arrays)")
         if cubes.dtype != torch.complex64:
             raise ValueError(f"cubes must be complex64, got {cubes.dtype}")
-        if tuple(cubes.shape[1:]) != self.shape.dims or cubes.shape[0] != self.batch:
-            raise ValueError(f"cubes must be [{self.batch}, {self.shape.dims}], "
-                             f"got {tuple(cubes.shape)}")
-        # element strides (complex64 units) of one cube and between cubes
-        sh = N.make_shape(self.shape.dims, [int(s) for s in cubes.stride()[1:]])
+        G = self.group
+        if G == 1:
+            if tuple(cubes.shape[1:]) != self.shape.dims or cubes.shape[0] != self.batch:
+                raise ValueError(f"cubes must be [{self.batch}, {self.shape.dims}], "
+                                 f"got {tuple(cubes.shape)}")
+            strides = [int(s) for s in cubes.stride()[1:]]
+        else:  # interleaved batch [ceil(B/G), *dims, G] (see ``interleave``)
+            want = ((self.batch + G - 1) // G, *self.shape.dims, G)
+            if tuple(cubes.shape) != want or cubes.stride(-1) != 1:
+                raise ValueError(f"grouped cubes must be {want} with unit last stride, "
+                                 f"got {tuple(cubes.shape)}")
+            strides = [int(s) for s in cubes.stride()[1:-1]]
+        # element strides (complex64 units) of one cube and between cubes (groups)
+        sh = N.make_shape(self.shape.dims, strides)
         # a pinned host tensor is read in place by the kernel (zero copy over the
         # host link: only the gathered samples cross it, the sub-linear sample
         # budget of the algorithm); its UVA address is valid on the device
         dev = cubes.device if cubes.is_cuda else self.device
         with torch.cuda.device(dev):
-            N.check(N.lib().fpssft_run_batch(
-                N.ptr(cubes), self.batch, int(cubes.stride(0)), C_ref(sh), C_ref(self._params_c),
-                N.ptr(self.schedule), N.ptr(self.sched_index), int(self.schedule_host.shape[0]),
-                C_ref(self._out_c), N.stream_ptr(dev)))
+            N.check(N.lib().fpssft_run_batch_grouped(
+                N.ptr(cubes), self.batch, G, int(cubes.stride(0)), C_ref(sh),
+                C_ref(self._params_c), N.ptr(self.schedule), N.ptr(self.sched_index),
+                int(self.schedule_host.shape[0]), C_ref(self._out_c), N.stream_ptr(dev)))
         o = self.out
         return BatchResult(self.shape, self.k_cap, o["freqs"], o["amps"], o["count"],
                            o["iterations"], o["samples_used"], o["terminated_by"],
                            o["iter_stats"], self.schedule_host, self.sched_index_host)
+
+
+def interleave(cubes, group: int = 8):
+    """The interleaved batch layout ``[ceil(B/G), *dims, G]`` of ``[B, *dims]``
+    cubes (a copy; the last group zero-padded): sample n of G consecutive
+    instances shares one 64-byte DRAM segment at G = 8, so a schedule shared
+    by the batch reads every segment once for G instances instead of once per
+    instance.  Run it with ``BatchRunner(..., group=G)``."""
+    import torch
+
+    B, dims = int(cubes.shape[0]), tuple(cubes.shape[1:])
+    ng = (B + group - 1) // group
+    out = torch.zeros((ng, *dims, group), dtype=cubes.dtype, device=cubes.device)
+    full = B // group
+    nd = len(dims)
+    if full:
+        out[:full].copy_(cubes[:full * group].reshape(full, group, *dims)
+                         .permute(0, *range(2, nd + 2), 1))
+    for b in range(full * group, B):
+        out[full][..., b - full * group] = cubes[b]
+    return out
 
 
 def launch_plan(shape: CubeShape, params: N.Params) -> dict:

@@ -86,3 +86,24 @@ def test_tune_picks_a_measured_fraction():
     hr = HostBatchRunner(P.CubeShape(w.dims), cfg, 64, k_cap=128, device=DEV, chunk=16)
     f = hr.tune(host, fractions=[0.0, 0.5, 1.0])
     assert f in (0.0, 0.5, 1.0) and hr.mode == "split" and hr.tuned["fraction"] == f
+
+
+@pytest.mark.parametrize("cfg_id,count,k_cap,group", [(2, 37, 128, 8), (2, 16, 128, 16),
+                                                      (3, 9, 512, 8), (4, 5, 2048, 4),
+                                                      (5, 6, 1024, 8), (1, 1, 64, 8)])
+def test_interleaved_layout_matches_batch_major(cfg_id, count, k_cap, group):
+    """The interleaved batch layout [ceil(B/G), *dims, G] (fpssft_run_batch_grouped)
+    gives bit-identical outputs, partial last group included."""
+    w, cubes, cfg = _cubes(cfg_id, count)
+    shape = P.CubeShape(w.dims)
+    ref = P.BatchRunner(shape, cfg, count, k_cap=k_cap, device=DEV)
+    ref.run(cubes)
+    g = P.BatchRunner(shape, cfg, count, k_cap=k_cap, device=DEV, group=group)
+    gi = P.interleave(cubes, group)
+    assert gi.shape == ((count + group - 1) // group, *w.dims, group)
+    g.run(gi)
+    for k, v in ref.out.items():
+        if v is not None:
+            assert torch.equal(v, g.out[k]), k
+    with pytest.raises(ValueError):
+        g.run(cubes)  # batch-major tensor handed to a grouped runner

@@ -184,3 +184,16 @@ def test_zero_copy_split_model():
     # monotone in the sample count
     fs = [zero_copy_split(s, 512 * 512) for s in (1e3, 1e4, 1e5, 1e6)]
     assert fs == sorted(fs, reverse=True)
+
+
+def test_interleave_layout_cpu():
+    import torch
+
+    from paper_1711_11407_b200 import interleave
+
+    x = torch.arange(5 * 3 * 4, dtype=torch.float32).reshape(5, 3, 4).to(torch.complex64)
+    y = interleave(x, 2)
+    assert y.shape == (3, 3, 4, 2)
+    for b in range(5):
+        assert torch.equal(y[b // 2, ..., b % 2], x[b])
+    assert torch.equal(y[2, ..., 1], torch.zeros(3, 4, dtype=torch.complex64))
