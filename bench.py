@@ -76,12 +76,23 @@ def _probe_rate():
     return None
 
 
-def _segments_per_launch(shape, schedule, iterations, sched_index=None, seg=8):
+def _segments_per_launch(shape, schedule, iterations, sched_index=None, seg=8, group=1):
     """Distinct 64-byte DRAM segments (seg = 8 complex64 samples) the gathers
     of one launch touch: per iteration, the (D+1) L sample offsets of the
     lines (row-major cube), counted once per instance that runs it.  With the
     .L2::64B fetch size a miss moves one such segment (config 2: 6.7 M
-    segments, 427 MB of DRAM reads under ncu)."""
+    segments, 427 MB of DRAM reads under ncu).  Interleaved layout (group G):
+    a group's G samples of an offset share segments, counted once per group
+    for as many iterations as its longest-running instance."""
+    if group > 1:
+        iters = np.asarray(iterations)
+        pad = (-len(iters)) % group
+        gi = np.concatenate([iters, np.zeros(pad, iters.dtype)]).reshape(-1, group).max(1)
+        si = None
+        if sched_index is not None:  # one schedule per group is what the model assumes
+            si = np.asarray(sched_index)[::group]
+        return _segments_per_launch(shape, schedule, gi, si, seg, -group)
+    G = -group if group < 0 else 1
     dims = np.asarray(shape.dims, np.int64)
     strides = np.cumprod(np.concatenate([[1], dims[::-1][:-1]]))[::-1]
     L = shape.line_len
@@ -100,7 +111,10 @@ def _segments_per_launch(shape, schedule, iterations, sched_index=None, seg=8):
                 if i:
                     tau[i - 1] = (tau[i - 1] + 1) % dims[i - 1]
                 offs.append((((l * al + tau) % dims) * strides).sum(1))
-            per_t.append(len(np.unique(np.concatenate(offs) // seg)))
+            o = np.concatenate(offs)
+            if G > 1:  # element index in the group block: offset * G + member
+                o = (o[:, None] * G + np.arange(G)[None, :]).ravel()
+            per_t.append(len(np.unique(o // seg)))
         per_t = np.asarray(per_t)
         total += int(sum(per_t[:n].sum() for n in its))
     return total
@@ -273,9 +287,10 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--layout", default="batch_major", choices=["batch_major", "interleaved"],
+    ap.add_argument("--layout", default="auto", choices=["auto", "batch_major", "interleaved"],
                     help="HBM layout of the batch: [B, *dims], or [B/G, *dims, G] with G "
-                         "instances interleaved sample by sample (--group)")
+                         "instances interleaved sample by sample (--group); auto = "
+                         "interleaved for batches of >= 64 instances")
     ap.add_argument("--group", type=int, default=8)
     ap.add_argument("--mode", default="auto", choices=["auto", "warp", "cta"],
                     help="kernel family (auto: the planner's choice for this batch)")
@@ -337,7 +352,10 @@ def main():
     cubes = W.synthesize_batch_torch(w.dims, spectra, dev, w.noise_var,
                                      noise_seed=w.seed * 1000003 + b0)
     torch.cuda.synchronize()
-    group = args.group if args.layout == "interleaved" else 1
+    layout = args.layout
+    if layout == "auto":
+        layout = "interleaved" if B >= 64 else "batch_major"
+    group = args.group if layout == "interleaved" else 1
     run_cubes = P.interleave(cubes, group) if group > 1 else cubes
     torch.cuda.synchronize()
     runner = P.BatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision, device=dev,
@@ -424,7 +442,7 @@ def main():
         # samples in 64-byte segments)
         roofline["sector_efficiency"] = bytes_per_launch / roofline["traffic"]
     probe = _probe_rate()
-    segs = _segments_per_launch(shape, runner.schedule_host, iters)
+    segs = _segments_per_launch(shape, runner.schedule_host, iters, group=group)
     roofline["gather"] = {
         "segments_per_launch": segs, "achieved_segments_per_s": segs / (rec_ms / 1e3),
         "peak_segments_per_s": probe,
@@ -518,6 +536,9 @@ def main():
                        "k": w.k, "profile": w.profile, "k_cap": k_cap,
                        "kernel": runner.plan,
                        "precision": args.precision, "parallelism": f"dp{world} (instances)",
+                       "layout": (f"interleaved [B/{group}, *dims, {group}] complex64 (group of "
+                                  f"{group} instances per 64-byte sample segment, DESIGN.md 4)"
+                                  if group > 1 else "batch-major [B, *dims] complex64"),
                        "l2": "flushed (256 MiB write) before every timed step",
                        "l2_fetch_granularity": {"set": args.l2_fetch, "driver_default": l2_default},
                        "mean_iterations": float(iters.mean()),
