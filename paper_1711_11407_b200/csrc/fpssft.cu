@@ -1657,10 +1657,11 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
     if (g.key_bits_ <= 31 && kn.k_cap <= 32768) {
         const char *env = std::getenv("FPSSFT_TEAM_NT");
         for (int want_nt : {512, 0}) {
-            if (env && std::atoi(env) != (want_nt ? want_nt : 1024)) continue;
-            int tnt = want_nt;
+            if (env && want_nt) continue;  // experiments: one pass at the requested size
+            const int req = env ? std::atoi(env) : want_nt;
+            int tnt = req;
             const void *tk = team_kernel_for(g, precision, &tnt);
-            if (!tk || (want_nt && tnt != want_nt)) continue;
+            if (!tk || (req && tnt != req)) continue;
             const TeamLayout tl = make_team_layout(g.D, g.L, kn.k_cap, cs, tnt);
             if ((long long)tl.total > SMEM_PER_CTA) continue;
             const int regs = (kernel_regs(tk, tnt >= 1024 ? 64 : 128) + 7) / 8 * 8;
