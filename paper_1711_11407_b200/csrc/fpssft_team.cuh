@@ -15,6 +15,9 @@
 #ifndef TEAM_SORT_BITS
 #define TEAM_SORT_BITS 11  // output counting-sort buckets (2048)
 #endif
+#ifndef FPSSFT_TEAM_PROJ_Q
+#define FPSSFT_TEAM_PROJ_Q 2  // projection sub-rounds per ordered apply (match_any path)
+#endif
 #ifndef FPSSFT_TEAM_PROJ
 #define FPSSFT_TEAM_PROJ 1  // projection: 1 = warp match_any + ordered apply, 0 = counting sort
 #endif
@@ -173,44 +176,59 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
             int *scr_u = (int *)(sm + lay.bin_start) + warp * 32 * (MAXD + 1);
             cpx<R> *scr_amp = (cpx<R> *)((int *)(sm + lay.bin_start) + NW * 32 * (MAXD + 1)) +
                               warp * 32;
+            // Q sub-rounds of NT slots per round: the warps' ordered apply (NW-1
+            // barriers) is paid once per Q * NT slots
+            constexpr int Q = FPSSFT_TEAM_PROJ_Q;
 #pragma unroll 1
-            for (int c0 = 0; c0 < n_slots; c0 += NT) {
-                const int s = c0 + tid;
-                const bool valid = s < n_slots && slot_live[s];
-                int b = -1 - lane;
-                if (valid) {
-                    int m[MAXD];
-                    unpack_key(slot_key[s], g, m);
-                    b = bin_of(m, g, al);
-                    const int u0 = phase_of(m, g, ta);
+            for (int c0 = 0; c0 < n_slots; c0 += Q * NT) {
+                cpx<R> P[Q][MAXD + 1];
+                int bq[Q];
+                bool leader[Q];
 #pragma unroll
-                    for (int i = 0; i < MAXD + 1; ++i)
-                        if (i < nl) scr_u[i * 32 + lane] = phase_step(u0, i, m, g);
-                    scr_amp[lane] = slot_amp[s];
-                }
-                __syncwarp();
-                const unsigned grp = __match_any_sync(FULL, b);
-                const bool leader = valid && lane == __ffs(grp) - 1;
-                cpx<R> P[MAXD + 1];
-#pragma unroll
-                for (int i = 0; i < MAXD + 1; ++i) P[i] = {(R)0, (R)0};
-                if (leader) {
-                    for (unsigned rest = grp; rest; rest &= rest - 1) {
-                        const int j = __ffs(rest) - 1;
-                        const cpx<R> aj = scr_amp[j];
+                for (int q = 0; q < Q; ++q) {
+                    const int s = c0 + q * NT + tid;
+                    const bool valid = s < n_slots && slot_live[s];
+                    int b = -1 - lane;
+                    if (q) __syncwarp();  // the previous sub-round's scratch is read
+                    if (valid) {
+                        int m[MAXD];
+                        unpack_key(slot_key[s], g, m);
+                        b = bin_of(m, g, al);
+                        const int u0 = phase_of(m, g, ta);
 #pragma unroll
                         for (int i = 0; i < MAXD + 1; ++i)
-                            if (i < nl) P[i] = P[i] + aj * roots[scr_u[i * 32 + j]];
+                            if (i < nl) scr_u[i * 32 + lane] = phase_step(u0, i, m, g);
+                        scr_amp[lane] = slot_amp[s];
+                    }
+                    __syncwarp();
+                    const unsigned grp = __match_any_sync(FULL, b);
+                    leader[q] = valid && lane == __ffs(grp) - 1;
+                    bq[q] = b;
+#pragma unroll
+                    for (int i = 0; i < MAXD + 1; ++i) P[q][i] = {(R)0, (R)0};
+                    if (leader[q]) {
+                        for (unsigned rest = grp; rest; rest &= rest - 1) {
+                            const int j = __ffs(rest) - 1;
+                            const cpx<R> aj = scr_amp[j];
+#pragma unroll
+                            for (int i = 0; i < MAXD + 1; ++i)
+                                if (i < nl) P[q][i] = P[q][i] + aj * roots[scr_u[i * 32 + j]];
+                        }
                     }
                 }
                 const int nw_live = min(NW, (n_slots - c0 + 31) / 32);
                 for (int w2 = 0; w2 < nw_live; ++w2) {
                     if (w2) __syncthreads();
-                    if (warp == w2 && leader) {
+                    if (warp == w2) {
 #pragma unroll
-                        for (int i = 0; i < MAXD + 1; ++i)
-                            if (i < nl)
-                                spec[padi<PAD>(i * L + b)] = spec[padi<PAD>(i * L + b)] - P[i];
+                        for (int q = 0; q < Q; ++q)
+                            if (leader[q]) {
+#pragma unroll
+                                for (int i = 0; i < MAXD + 1; ++i)
+                                    if (i < nl)
+                                        spec[padi<PAD>(i * L + bq[q])] =
+                                            spec[padi<PAD>(i * L + bq[q])] - P[q][i];
+                            }
                     }
                 }
                 __syncthreads();
