@@ -7,7 +7,7 @@ consumes and produces, plus batched and per-step device entry points.
 """
 
 from .core import (CubeShape, DenseSource, FreqIndex, SignalSource, Sinusoid, SparseSpectrum,
-                   make_dense_source, spectra_match)
+                   SyntheticSource, make_dense_source, make_synthetic_source, spectra_match)
 from .driver import (PROFILES, BatchResult, BatchRunner, FpsSftConfig, IterationStats,
                      RecoveryReport, default_max_iterations, fps_sft, fps_sft_batch, interleave,
                      materialize, max_k_cap)
@@ -24,7 +24,7 @@ ALGORITHMS = {"fps-b200": fps_sft, "baseline-b200": baseline_sft}
 __all__ = ["ALGORITHMS", "BatchResult", "BatchRunner", "CubeShape", "DenseSource",
            "FpsSftConfig", "FreqIndex", "GrayImage", "IterationStats", "PROFILES",
            "RecoveryReport", "fps_sft_large", "reconstruct_sparse_image", "synthetic_phantom",
-           "SignalSource", "Sinusoid", "SparseSpectrum", "baseline_sft", "bins_of_frequencies",
+           "SignalSource", "Sinusoid", "SyntheticSource", "SparseSpectrum", "baseline_sft", "bins_of_frequencies",
            "default_max_iterations", "fps_sft", "fps_sft_batch", "interleave", "is_valid_slope",
-           "make_dense_source", "materialize", "max_k_cap", "sample_slope",
+           "make_dense_source", "make_synthetic_source", "materialize", "max_k_cap", "sample_slope",
            "schedule_from_seed", "spectra_match", "valid_slopes"]

@@ -199,3 +199,37 @@ class DenseSource(SignalSource):
 def make_dense_source(cube, shape: CubeShape) -> DenseSource:
     """Sample oracle backed by a stored cube (core.py:276-278)."""
     return DenseSource(cube, shape)
+
+
+class SyntheticSource(SignalSource):
+    """Lazy sinusoid mixture x(n) = sum_i a_i exp(2j pi sum_k n_k m_ik / N_k)
+    (reference ``SyntheticSource``, core.py:176-217): samples on the host
+    with the same exact integer phases (multiples of 1/L of a turn); the
+    device path materialises the whole grid with ``fpssft_synthesize``
+    through ``spectrum`` (``driver.materialize``)."""
+
+    def __init__(self, spectrum: SparseSpectrum):
+        self.spectrum = spectrum
+        self._cube = spectrum.shape
+
+    def shape(self) -> CubeShape:
+        return self._cube
+
+    def sample(self, n: Sequence[int]) -> complex:
+        return complex(self.sample_many(np.asarray([self._cube.validate_index(n)]))[0])
+
+    def sample_many(self, indices: np.ndarray) -> np.ndarray:
+        sh = self._cube
+        idx = np.asarray(indices, dtype=np.int64).reshape(-1, sh.ndim)
+        f = self.spectrum.freq_array
+        a = self.spectrum.amp_array
+        L = sh.line_len
+        cof = np.asarray([L // d for d in sh.dims], np.int64)
+        u = ((idx * cof) @ f.T) % L  # [n, K] exact phase numerators
+        roots = np.exp(2j * np.pi * np.arange(L) / L)
+        return (roots[u] * a[None, :]).sum(axis=1)
+
+
+def make_synthetic_source(spec: SparseSpectrum) -> SyntheticSource:
+    """Sample oracle evaluating the mixture lazily (core.py:270-273)."""
+    return SyntheticSource(spec)
