@@ -132,3 +132,24 @@ def test_cli_recover_end_to_end(tmp_path):
     rc = cli.main(["recover", "--input", str(out / "recovered_spectrum.txt"), "--seed", "5",
                    "--out", str(tmp_path / "rec2")])
     assert rc == 0
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_interleaved_layout_with_per_instance_schedules(prec):
+    """Grouped layout with one schedule per instance (Monte Carlo style) and in
+    float64: still bit-identical to the batch-major run."""
+    import numpy as np
+
+    w, cubes, cfg = _cubes(2, 20)
+    shape = P.CubeShape(w.dims)
+    t_max = P.default_max_iterations(shape)
+    sch = np.stack([P.schedule_from_seed(shape, s, t_max) for s in range(3)])
+    si = np.random.default_rng(4).integers(0, 3, 20)
+    kw = dict(k_cap=128, device=DEV, precision=prec, schedule=sch, sched_index=si)
+    ref = P.BatchRunner(shape, cfg, 20, **kw)
+    ref.run(cubes)
+    g = P.BatchRunner(shape, cfg, 20, group=8, **kw)
+    g.run(P.interleave(cubes, 8))
+    for k, v in ref.out.items():
+        if v is not None:
+            assert torch.equal(v, g.out[k]), k
