@@ -70,7 +70,8 @@ class HostBatchRunner:
     def __init__(self, shape: CubeShape, config: FpsSftConfig, batch: int, *,
                  k_cap: int = 256, precision: str = "fp32", device=None, mode: str = "auto",
                  zero_copy_fraction: float | None = None, chunk: int | None = None,
-                 chunk_bytes: int = 256 << 20, schedule=None, sched_index=None):
+                 chunk_bytes: int = 256 << 20, schedule=None, sched_index=None,
+                 graphs: bool = True):
         import torch
 
         if mode not in ("auto", "copy", "zero_copy", "split"):
@@ -90,6 +91,8 @@ class HostBatchRunner:
         self.out = allocate_outputs(self.batch, shape, k_cap, self.t_max, "cpu", pin=True)
         self.last_mean_samples: float | None = None
         self.tuned: dict | None = None
+        self.graphs = graphs
+        self._graphs: dict = {}
         self._runners: dict = {}
         self._bufs: list = []
         self._img_bufs: list = []
@@ -154,6 +157,34 @@ class HostBatchRunner:
             self._img_bufs.append(torch.empty((self.chunk, *self.shape.dims),
                                               dtype=torch.complex64, device=self.device))
 
+    def _graph_for(self, host_cubes, runner: BatchRunner):
+        """CUDA graph of (zero-copy recovery + result copy) for this host
+        buffer: the launch sequence of a small batch costs more on the host
+        than on the device (config 1: one instance, 24 us of kernel).  None if
+        the capture is refused (then the stream path runs)."""
+        import torch
+
+        key = (host_cubes.data_ptr(), tuple(host_cubes.shape))
+        if key in self._graphs:
+            return self._graphs[key]
+        g = None
+        try:
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(side):  # warm: plans and attributes set outside capture
+                runner.run(host_cubes)
+                self._copy_out(runner, 0, self.batch)
+            side.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                runner.run(host_cubes)
+                self._copy_out(runner, 0, self.batch)
+        except RuntimeError:
+            g = None
+            torch.cuda.synchronize(self.device)
+        self._graphs[key] = g
+        return g
+
     def _copy_out(self, r: BatchRunner, b0: int, n: int):
         if b0 == 0 and n == self.batch:  # same packed layout: one copy
             self.out.buf.copy_(r.out.buf, non_blocking=True)
@@ -185,12 +216,18 @@ class HostBatchRunner:
             raise ValueError("images must be a pinned host tensor shaped like host_cubes")
         bz = self.split_count()
         if bz == self.batch and not synth:
-            # all gathered in place: one launch and the result copies, in stream order
+            # all gathered in place: one launch and the result copy, in stream order,
+            # replayed from a CUDA graph once captured for this host buffer
             rz = self._runner(0, bz)
-            rz.run(host_cubes)
-            self._copy_out(rz, 0, bz)
+            g = self._graph_for(host_cubes, rz) if self.graphs else None
+            if g is not None:
+                g.replay()
+            else:
+                rz.run(host_cubes)
+                self._copy_out(rz, 0, bz)
             torch.cuda.current_stream(self.device).synchronize()
-            self.last_mean_samples = float(self.out["samples_used"].double().mean())
+            if self.mode == "auto":
+                self.last_mean_samples = float(self.out["samples_used"].double().mean())
             return self.out
         self._ensure_buffers(synth)
         if bz == 0 and self.chunk >= self.batch and not synth:

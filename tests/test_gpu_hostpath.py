@@ -153,3 +153,22 @@ def test_interleaved_layout_with_per_instance_schedules(prec):
     for k, v in ref.out.items():
         if v is not None:
             assert torch.equal(v, g.out[k]), k
+
+
+def test_zero_copy_graph_replay_sees_new_host_data():
+    """The captured graph (zero copy + result copy) replays on whatever the
+    pinned host buffer holds now."""
+    w, cubes, cfg = _cubes(2, 12)
+    shape = P.CubeShape(w.dims)
+    other = W.synthesize_batch_torch(w.dims, W.make_spectra(w, 12, 100), DEV, 0.0, noise_seed=3)
+    ref = P.BatchRunner(shape, cfg, 12, k_cap=128, device=DEV)
+    host = torch.empty(cubes.shape, dtype=cubes.dtype, pin_memory=True)
+    hr = HostBatchRunner(shape, cfg, 12, k_cap=128, device=DEV, mode="zero_copy")
+    for src in (cubes, other, cubes):
+        host.copy_(src)
+        got = {k: v.clone() for k, v in hr.run(host).items() if v is not None}
+        ref.run(src)
+        for k, v in ref.out.items():
+            if v is not None:
+                assert torch.equal(v.cpu(), got[k]), k
+    assert hr._graphs and all(g is not None for g in hr._graphs.values())
