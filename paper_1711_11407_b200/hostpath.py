@@ -120,7 +120,8 @@ class HostBatchRunner:
         if fractions is None:
             self.run(host_cubes, images)  # learns the sample count
             f0 = self.split_count() / max(1, self.batch)
-            fractions = sorted({0.0, 1.0, round(f0, 3), 0.5, 0.65, 0.8, 0.9})
+            fractions = sorted({0.0, 1.0, round(f0, 3), 0.35, 0.5, 0.65, 0.7, 0.75, 0.8, 0.85,
+                                0.9, 0.95})
         best = None
         for f in fractions:
             self.mode, self.fraction = "split", float(f)
