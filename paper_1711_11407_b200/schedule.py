@@ -83,6 +83,38 @@ def schedule_from_seed(shape: CubeShape, seed: int, t_max: int) -> np.ndarray:
     return out
 
 
+_POOL = None
+
+
+def _schedule_job(args):
+    dims, seed, t_max = args
+    return schedule_from_seed(CubeShape(dims), seed, t_max)
+
+
+def schedules_from_seeds(shape: CubeShape, seeds, t_max: int, workers: int | None = None):
+    """int32 (S, t_max, 2, D): ``schedule_from_seed`` for every seed (Monte
+    Carlo trials each draw their own lines).  The replay is numpy's own
+    generator call by call (~50 us per iteration), so many trials are spread
+    over a pool of host processes (spawned: the parent may hold a CUDA
+    context); small requests run in place."""
+    import os
+
+    seeds = [int(s) for s in seeds]
+    if workers is None:
+        workers = os.cpu_count() or 1
+    if workers <= 1 or len(seeds) * t_max < 4000:
+        return np.stack([schedule_from_seed(shape, s, t_max) for s in seeds]) if seeds else \
+            np.empty((0, t_max, 2, shape.ndim), np.int32)
+    global _POOL
+    if _POOL is None:
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+
+        _POOL = ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn"))
+    jobs = [(shape.dims, s, t_max) for s in seeds]
+    return np.stack(list(_POOL.map(_schedule_job, jobs, chunksize=max(1, len(jobs) // (4 * workers)))))
+
+
 def bins_of_frequencies(freqs, alpha, shape: CubeShape) -> np.ndarray:
     """sum_k c_k alpha_k m_k mod L over a (K, D) array (numtheory.py:139-153)."""
     w = np.asarray([c * int(a) for c, a in zip(shape.cofactors, alpha)], dtype=np.int64)

@@ -24,7 +24,7 @@ import numpy as np
 
 from .core import CubeShape
 from .driver import PROFILES, FpsSftConfig, default_max_iterations, fps_sft_batch
-from .schedule import schedule_from_seed
+from .schedule import schedules_from_seeds
 
 CLUSTER_SIZES = {9: 1, 25: 2}  # cluster size -> block radius (oracle.py:31)
 PLACEMENTS = {"uniform": ("uniform", None), "clustered9": ("clustered", 9),
@@ -114,7 +114,7 @@ def run_cell(shape: CubeShape, k: int, placement: str, trials: int, seed: int,
     seeds = trial_seeds(seed, trials)
     t_max = config.max_iterations or default_max_iterations(shape)
     truths = [generate_spectrum(shape, k, g, kind, csize) for g, _ in seeds]
-    sched = np.stack([schedule_from_seed(shape, a, t_max) for _, a in seeds])
+    sched = schedules_from_seeds(shape, [a for _, a in seeds], t_max)
     k_in = 1 << max(0, (k - 1).bit_length())
     fr = torch.zeros((trials, k_in, shape.ndim), dtype=torch.int32)
     am = torch.zeros((trials, k_in), dtype=torch.complex128)

@@ -197,3 +197,16 @@ def test_interleave_layout_cpu():
     for b in range(5):
         assert torch.equal(y[b // 2, ..., b % 2], x[b])
     assert torch.equal(y[2, ..., 1], torch.zeros(3, 4, dtype=torch.complex64))
+
+
+def test_schedules_from_seeds_pool_matches_serial():
+    from paper_1711_11407_b200 import CubeShape
+    from paper_1711_11407_b200.schedule import schedule_from_seed, schedules_from_seeds
+
+    shape = CubeShape((32, 24))
+    seeds = [3, 99, 12345, 7, 2**40 + 1]
+    want = np.stack([schedule_from_seed(shape, s, 40) for s in seeds])
+    np.testing.assert_array_equal(schedules_from_seeds(shape, seeds, 40, workers=1), want)
+    # forced through the process pool
+    np.testing.assert_array_equal(schedules_from_seeds(shape, seeds * 30, 40, workers=2),
+                                  np.concatenate([want] * 30))
