@@ -870,6 +870,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     }
 }
 
+#include "fpssft_regfft.cuh"
 #include "fpssft_team.cuh"
 #include "fpssft_warp_il.cuh"
 #include "fpssft_synth.cuh"

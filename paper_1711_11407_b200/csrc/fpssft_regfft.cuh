@@ -1,0 +1,122 @@
+// 512-point DFTs held in the registers of one warp (float32), shared by the
+// re-synthesis kernel (inverse row transforms, fpssft_synth.cuh) and the team
+// recovery kernel (forward line transforms of config 5, fpssft_team.cuh).
+// 512 = 16 x 32: lane b holds x[32 a + b] (a = 0..15), a 16-point DFT over a in
+// registers, twiddle e^{2 pi i b c / 512}, one shared-memory exchange (row
+// stride 34, conflict-free both ways), a 16-point DFT over beta (b = 2 beta +
+// h) and a radix-2 combine with the partner lane; lane (c, h) ends with
+// X[c + 16 d + 256 h], d = 0..15.
+#pragma once
+// (included inside namespace fpssft)
+namespace regfft {
+
+// constexpr e^{+2 pi i j / 16} and e^{+2 pi i j / 32}
+__device__ __forceinline__ float2 w16(int j) {
+    constexpr float C[16] = {1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                             0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                             -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f,
+                             0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
+    return make_float2(C[j & 15], C[(j + 12) & 15]);  // (cos, sin): sin x = cos(x - pi/2)
+}
+__device__ __forceinline__ float2 w32(int j) {
+    constexpr float C[32] = {
+        1.0f, 0.98078528040323044f, 0.92387953251128674f, 0.83146961230254524f,
+        0.70710678118654752f, 0.55557023301960218f, 0.38268343236508977f, 0.19509032201612826f,
+        0.0f, -0.19509032201612826f, -0.38268343236508977f, -0.55557023301960218f,
+        -0.70710678118654752f, -0.83146961230254524f, -0.92387953251128674f, -0.98078528040323044f,
+        -1.0f, -0.98078528040323044f, -0.92387953251128674f, -0.83146961230254524f,
+        -0.70710678118654752f, -0.55557023301960218f, -0.38268343236508977f, -0.19509032201612826f,
+        0.0f, 0.19509032201612826f, 0.38268343236508977f, 0.55557023301960218f,
+        0.70710678118654752f, 0.83146961230254524f, 0.92387953251128674f, 0.98078528040323044f};
+    return make_float2(C[j & 31], C[(j + 24) & 31]);
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 mul_i(float2 a) { return make_float2(-a.y, a.x); }  // * (+i)
+
+// X[k] = sum_n x[n] e^{+2 pi i n k / 4}
+__device__ __forceinline__ void dft4(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
+    const float2 t0 = cadd(x0, x2), t1 = csub(x0, x2), t2 = cadd(x1, x3), t3 = mul_i(csub(x1, x3));
+    x0 = cadd(t0, t2);
+    x2 = csub(t0, t2);
+    x1 = cadd(t1, t3);
+    x3 = csub(t1, t3);
+}
+
+// In place, natural order in and out: v[k] <- sum_n v[n] e^{+2 pi i n k / 16}
+// (n = 4 n1 + n2, k = k1 + 4 k2: DFT-4 over n1, twiddle, DFT-4 over n2).
+__device__ __forceinline__ void dft16(float2 *v) {
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
+    // v[4 k1 + n2] now holds Y[n2][k1]; twiddle by e^{2 pi i n2 k1 / 16}
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+        for (int k1 = 1; k1 < 4; ++k1) v[4 * k1 + n2] = cmul(v[4 * k1 + n2], w16(n2 * k1));
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+    // v[4 k1 + k2] holds X[k1 + 4 k2]: transpose the 4 x 4 index (registers only)
+    float2 t[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = v[i];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
+}
+
+// Forward 1/L-normalised DFTs of `nlines` 512-point lines in the padded
+// spectra layout (padi), one warp per line (warps >= nlines idle): the
+// conjugate of the inverse transform of the conjugated line.  `roots` is the
+// L = 512 table e^{2 pi i j / 512}.  Returns this thread's share of sum |x|^2
+// over the input samples (each read once), like fft_static.  No block
+// barrier inside: the caller synchronises before (inputs) and after (outputs).
+template <int NT>
+__device__ __forceinline__ float fft512_lines_warp(cpx<float> *spec, int nlines,
+                                                   const cpx<float> *roots, int tid) {
+    const int warp = tid >> 5, lane = tid & 31;
+    const int cc = lane >> 1, h = lane & 1;
+    float energy = 0.f;
+    for (int line = warp; line < nlines; line += NT / 32) {
+        float2 *base = (float2 *)(spec + line * (512 + 32));  // padi(line * 512)
+        float2 v[16];
+#pragma unroll
+        for (int a = 0; a < 16; ++a) {
+            const int i = 32 * a + lane;
+            const float2 x = base[i + (i >> 4)];
+            energy += x.x * x.x + x.y * x.y;
+            v[a] = make_float2(x.x, -x.y);  // conjugate in
+        }
+        dft16(v);
+#pragma unroll
+        for (int c = 1; c < 16; ++c) {
+            const cpx<float> r = roots[lane * c];
+            v[c] = cmul(v[c], make_float2(r.re, r.im));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 16; ++c) base[34 * c + lane] = v[c];
+        __syncwarp();
+#pragma unroll
+        for (int b = 0; b < 16; ++b) v[b] = base[34 * cc + 2 * b + h];
+        dft16(v);
+        __syncwarp();  // every lane has read the exchange before it is overwritten
+        const float sg = h ? -1.f : 1.f, inv = 1.f / 512.f;
+#pragma unroll
+        for (int d = 0; d < 16; ++d) {
+            const float2 tv = cmul(w32(d), v[d]);
+            const float2 y = h ? tv : v[d];
+            const float2 p = make_float2(__shfl_xor_sync(FULL, y.x, 1),
+                                         __shfl_xor_sync(FULL, y.y, 1));
+            const int k = cc + 16 * d + 256 * h;
+            // conjugate out, 1/L (exact: a power of two)
+            base[k + (k >> 4)] = make_float2(fmaf(sg, y.x, p.x) * inv, -fmaf(sg, y.y, p.y) * inv);
+        }
+    }
+    return energy;
+}
+
+}  // namespace regfft

@@ -22,63 +22,8 @@
 // (included inside namespace fpssft)
 namespace synth {
 
-// constexpr e^{+2 pi i j / 16} and e^{+2 pi i j / 32}
-__device__ __forceinline__ float2 w16(int j) {
-    constexpr float C[16] = {1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
-                             0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
-                             -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f,
-                             0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
-    return make_float2(C[j & 15], C[(j + 12) & 15]);  // (cos, sin): sin x = cos(x - pi/2)
-}
-__device__ __forceinline__ float2 w32(int j) {
-    constexpr float C[32] = {
-        1.0f, 0.98078528040323044f, 0.92387953251128674f, 0.83146961230254524f,
-        0.70710678118654752f, 0.55557023301960218f, 0.38268343236508977f, 0.19509032201612826f,
-        0.0f, -0.19509032201612826f, -0.38268343236508977f, -0.55557023301960218f,
-        -0.70710678118654752f, -0.83146961230254524f, -0.92387953251128674f, -0.98078528040323044f,
-        -1.0f, -0.98078528040323044f, -0.92387953251128674f, -0.83146961230254524f,
-        -0.70710678118654752f, -0.55557023301960218f, -0.38268343236508977f, -0.19509032201612826f,
-        0.0f, 0.19509032201612826f, 0.38268343236508977f, 0.55557023301960218f,
-        0.70710678118654752f, 0.83146961230254524f, 0.92387953251128674f, 0.98078528040323044f};
-    return make_float2(C[j & 31], C[(j + 24) & 31]);
-}
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 mul_i(float2 a) { return make_float2(-a.y, a.x); }  // * (+i)
-
-// X[k] = sum_n x[n] e^{+2 pi i n k / 4}
-__device__ __forceinline__ void dft4(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
-    const float2 t0 = cadd(x0, x2), t1 = csub(x0, x2), t2 = cadd(x1, x3), t3 = mul_i(csub(x1, x3));
-    x0 = cadd(t0, t2);
-    x2 = csub(t0, t2);
-    x1 = cadd(t1, t3);
-    x3 = csub(t1, t3);
-}
-
-// In place, natural order in and out: v[k] <- sum_n v[n] e^{+2 pi i n k / 16}
-// (n = 4 n1 + n2, k = k1 + 4 k2: DFT-4 over n1, twiddle, DFT-4 over n2).
-__device__ __forceinline__ void dft16(float2 *v) {
-#pragma unroll
-    for (int n2 = 0; n2 < 4; ++n2) dft4(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
-    // v[4 k1 + n2] now holds Y[n2][k1]; twiddle by e^{2 pi i n2 k1 / 16}
-#pragma unroll
-    for (int n2 = 1; n2 < 4; ++n2)
-#pragma unroll
-        for (int k1 = 1; k1 < 4; ++k1) v[4 * k1 + n2] = cmul(v[4 * k1 + n2], w16(n2 * k1));
-#pragma unroll
-    for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
-    // v[4 k1 + k2] holds X[k1 + 4 k2]: transpose the 4 x 4 index (registers only)
-    float2 t[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) t[i] = v[i];
-#pragma unroll
-    for (int k1 = 0; k1 < 4; ++k1)
-#pragma unroll
-        for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
-}
+// helpers: regfft:: in fpssft_regfft.cuh
+using namespace regfft;
 
 constexpr int VS = 544;  // row stride of V (cpx): holds the 16 x 34 exchange tile
 

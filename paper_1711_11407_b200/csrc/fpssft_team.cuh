@@ -15,6 +15,9 @@
 #ifndef TEAM_SORT_BITS
 #define TEAM_SORT_BITS 11  // output counting-sort buckets (2048)
 #endif
+#ifndef FPSSFT_TEAM_REGFFT
+#define FPSSFT_TEAM_REGFFT 1  // 512-point lines: per-warp register FFTs (regfft::)
+#endif
 #ifndef FPSSFT_TEAM_PROJ_Q
 #define FPSSFT_TEAM_PROJ_Q 2  // projection sub-rounds per ordered apply (match_any path)
 #endif
@@ -159,7 +162,15 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
             if (staged) compact_stage16<LC, nl, NT, BlockTeam>((cpx<float> *)spec, par, dup, tid);
         }
         __syncthreads();
-        const R my_energy = fft_static<R, LC, nl, NT, BlockTeam>(spec, roots, tid);
+        R my_energy;
+        if constexpr (FPSSFT_TEAM_REGFFT && LC == 512 && sizeof(R) == 4 && NT / 32 >= nl) {
+            // one warp per line, in registers (regfft::): no block barrier inside
+            my_energy = regfft::fft512_lines_warp<NT>((cpx<float> *)spec, nl,
+                                                      (const cpx<float> *)roots, tid);
+            __syncthreads();
+        } else {
+            my_energy = fft_static<R, LC, nl, NT, BlockTeam>(spec, roots, tid);
+        }
         R noise_floor = (R)0;
         if (sizeof(R) == 4 && kn.noise_coef > 0)
             noise_floor = (R)kn.noise_coef * sqrt(block_sum(my_energy, rred));
