@@ -119,4 +119,76 @@ __device__ __forceinline__ float fft512_lines_warp(cpx<float> *spec, int nlines,
     return energy;
 }
 
+// Forward 1/L-normalised DFTs of `nlines` 2048-point lines (padded layout),
+// 128 threads (4 warps) per line, in registers: 2048 = 16 x 128.  Thread t
+// holds x[128 a + t] (a = 0..15): 16-point DFT over a, twiddle
+// e^{2 pi i t c / 2048}, one shared-memory exchange (row stride 136) inside
+// the line's own padded region, then 16 DFTs of 128 points: thread (c, q) =
+// (t / 8, t % 8) holds z[8 mu + q] (mu = 0..15) of DFT c: 16-point DFT over mu,
+// twiddle e^{2 pi i q d / 128}, and an 8-point DFT across the 8 lanes q by
+// shuffles (decimation in frequency: lane q ends with output 16 bitrev3(q)
+// + d).  Forward = conjugate of the inverse of the conjugate.  The 4 warps of
+// a line meet at named barriers (ids 1..nlines); no block barrier inside.
+__device__ __forceinline__ void bar_line(int id) {
+    asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
+template <int NT>
+__device__ __forceinline__ float fft2048_lines_team(cpx<float> *spec, int nlines,
+                                                    const cpx<float> *roots, int tid) {
+    constexpr int PADL = 2048 + 128, S = 136;
+    const int line = tid >> 7, t = tid & 127;
+    float energy = 0.f;
+    if (line >= nlines) return energy;
+    float2 *base = (float2 *)(spec + line * PADL);
+    float2 v[16];
+#pragma unroll
+    for (int a = 0; a < 16; ++a) {
+        const int i = 128 * a + t;
+        const float2 x = base[i + (i >> 4)];
+        energy += x.x * x.x + x.y * x.y;
+        v[a] = make_float2(x.x, -x.y);
+    }
+    dft16(v);
+#pragma unroll
+    for (int c = 1; c < 16; ++c) {
+        const cpx<float> r = roots[t * c];
+        v[c] = cmul(v[c], make_float2(r.re, r.im));
+    }
+    bar_line(1 + line);  // the line's inputs are read before the exchange overwrites them
+#pragma unroll
+    for (int c = 0; c < 16; ++c) base[c * S + t] = v[c];
+    bar_line(1 + line);
+    const int cq = t >> 3, q = t & 7;
+#pragma unroll
+    for (int mu = 0; mu < 16; ++mu) v[mu] = base[cq * S + 8 * mu + q];
+    dft16(v);
+#pragma unroll
+    for (int d = 1; d < 16; ++d) {
+        const cpx<float> r = roots[16 * q * d];
+        v[d] = cmul(v[d], make_float2(r.re, r.im));
+    }
+    // 8-point DFT across lanes q (partners xor 4, 2, 1), positive exponent
+    const cpx<float> r4 = roots[256 * (q & 3)], r2 = roots[512 * (q & 1)];
+    const float2 w4 = make_float2(r4.re, r4.im), w2 = make_float2(r2.re, r2.im);
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+        float2 x = v[d];
+        float2 p = make_float2(__shfl_xor_sync(FULL, x.x, 4), __shfl_xor_sync(FULL, x.y, 4));
+        x = (q & 4) ? cmul(csub(p, x), w4) : cadd(x, p);
+        p = make_float2(__shfl_xor_sync(FULL, x.x, 2), __shfl_xor_sync(FULL, x.y, 2));
+        x = (q & 2) ? cmul(csub(p, x), w2) : cadd(x, p);
+        p = make_float2(__shfl_xor_sync(FULL, x.x, 1), __shfl_xor_sync(FULL, x.y, 1));
+        v[d] = (q & 1) ? csub(p, x) : cadd(x, p);
+    }
+    const int s = ((q & 1) << 2) | (q & 2) | ((q >> 2) & 1);  // bitrev3(q)
+    bar_line(1 + line);  // every thread has read the exchange before outputs land in it
+    const float inv = 1.f / 2048.f;
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+        const int k = cq + 16 * (d + 16 * s);
+        base[k + (k >> 4)] = make_float2(v[d].x * inv, -v[d].y * inv);
+    }
+    return energy;
+}
+
 }  // namespace regfft

@@ -168,6 +168,12 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
             my_energy = regfft::fft512_lines_warp<NT>((cpx<float> *)spec, nl,
                                                       (const cpx<float> *)roots, tid);
             __syncthreads();
+        } else if constexpr (FPSSFT_TEAM_REGFFT && LC == 2048 && sizeof(R) == 4 &&
+                             NT >= 128 * nl && nl < 16) {
+            // four warps per line, in registers, named barriers per line
+            my_energy = regfft::fft2048_lines_team<NT>((cpx<float> *)spec, nl,
+                                                       (const cpx<float> *)roots, tid);
+            __syncthreads();
         } else {
             my_energy = fft_static<R, LC, nl, NT, BlockTeam>(spec, roots, tid);
         }
