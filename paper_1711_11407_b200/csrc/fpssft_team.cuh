@@ -86,11 +86,11 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
     int *slot_key = (int *)(sm + lay.slot_key);
     unsigned short *hash = (unsigned short *)(sm + lay.hash);
     unsigned char *slot_live = sm + lay.slot_live;
-    unsigned short *bin_start = (unsigned short *)(sm + lay.bin_start);
-    unsigned short *bin_fill = (unsigned short *)(sm + lay.bin_fill);
-    unsigned short *seg = (unsigned short *)(sm + lay.seg);
-    unsigned short *slot_bin = (unsigned short *)(sm + lay.slot_bin);
-    unsigned short *slot_u0 = (unsigned short *)(sm + lay.slot_u0);
+    [[maybe_unused]] unsigned short *bin_start = (unsigned short *)(sm + lay.bin_start);
+    [[maybe_unused]] unsigned short *bin_fill = (unsigned short *)(sm + lay.bin_fill);
+    [[maybe_unused]] unsigned short *seg = (unsigned short *)(sm + lay.seg);
+    [[maybe_unused]] unsigned short *slot_bin = (unsigned short *)(sm + lay.slot_bin);
+    [[maybe_unused]] unsigned short *slot_u0 = (unsigned short *)(sm + lay.slot_u0);
     unsigned short *cand = (unsigned short *)(sm + lay.cand);
     int *ired = (int *)(sm + lay.red);
     R *rred = (R *)(sm + lay.red + 256);

@@ -130,7 +130,7 @@ __device__ __forceinline__ void il_step(IlInst<R> &st, const Geo &g, const Knobs
                                         const cpx<R> *roots, const OutPtrs &out, int lane,
                                         int H, int &seq) {
     constexpr bool PAD = true;
-    const int L = LC, D = DC, nl = DC + 1;
+    const int L = LC, nl = DC + 1;
     const R mag_tol = (R)kn.mag_tol, round_tol = (R)kn.round_tol, verify_tol = (R)kn.verify_tol;
     const R prune = (R)kn.amp_prune_tol;
     const unsigned lt_mask = (1u << lane) - 1u;
