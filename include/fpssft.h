@@ -80,7 +80,9 @@ typedef struct fpssft_out {
  * The whole recovery loop for a batch of independent complex64 cubes.
  * Replaces fps_sft(make_dense_source(cube, shape), config)
  * (driver.py:121-212, core.py:276-278) for every instance b:
- *   cube_b    = cubes + b*batch_stride                       (device, complex64)
+ *   cube_b    = cubes + b*batch_stride                       (device, complex64;
+ *               or pinned, mapped host memory: UVA zero copy -- the kernels gather
+ *               only the sampled chunks over the host link)
  *   schedule  = int32 [n_sched, t_max, 2, D] (alpha, tau)     (device)
  *               the (alpha_t, tau_t) the reference draws from default_rng(seed)
  *               (driver.py:131,142-143); see paper_1711_11407_b200.schedule
