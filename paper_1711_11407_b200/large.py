@@ -136,16 +136,13 @@ class _RecoveredSet:
         return self.freqs[live].astype(np.int64), self.amps[live]
 
 
-def _project(shape, freqs, amps, count, k_cap, alpha, off, precision, device):
-    """Device projection of (freqs, amps)[:count] onto line (alpha, off)."""
-    import torch
-
-    at = torch.as_tensor(np.stack([np.asarray(alpha, np.int32), np.asarray(off, np.int32)])[None],
-                         device=device)
-    out = torch.empty((1, shape.line_len), dtype=torch.complex128, device=device)
+def _project(shape, freqs, amps, count, k_cap, at, out, precision, device, shape_c=None):
+    """Device projection of (freqs, amps)[:count] onto the line whose
+    (alpha, offset) int32 [1, 2, D] device tensor is ``at``, into ``out`` [1, L]
+    (buffers made once per iteration by the caller: the loop is launch-bound)."""
     N.check(N.lib().fpssft_project_onto_bins(N.ptr(freqs), N.ptr(amps), N.ptr(count), 1, k_cap,
-                                             C_ref(N.make_shape(shape.dims)), N.ptr(at), 0,
-                                             N.ptr(out), _precision_code(precision),
+                                             C_ref(shape_c or N.make_shape(shape.dims)), N.ptr(at),
+                                             0, N.ptr(out), _precision_code(precision),
                                              N.stream_ptr(device)))
     return out[0]
 
@@ -167,6 +164,7 @@ def fps_sft_large(cube, shape: CubeShape | None = None, config: FpsSftConfig = F
         schedule = schedule_from_seed(shape, config.seed, t_max)
     schedule = np.asarray(schedule)
     rs = _RecoveredSet(shape, dev)
+    shape_c = N.make_shape(shape.dims)
     amp_total = 0.0
     stall, term, it = 0, TERMINATED_MAX_ITERATIONS, 0
     log = []
@@ -176,11 +174,16 @@ def fps_sft_large(cube, shape: CubeShape | None = None, config: FpsSftConfig = F
         offs = stepped_offsets(tau, dims)
         spec = line_spectra_global(cube, shape, alpha, tau, precision=precision)
         spec = spec.to(torch.complex128)
+        # the D+1 lines' (alpha, offset) and projection outputs, one transfer per iteration
+        at_all = torch.as_tensor(np.stack([np.stack([np.asarray(alpha, np.int32),
+                                                     np.asarray(off, np.int32)]) for off in offs]),
+                                 device=dev)
+        proj = torch.empty((D + 1, 1, L), dtype=torch.complex128, device=dev)
         if len(rs.keys):
             rs.upload()
-            for i, off in enumerate(offs):
-                spec[i] -= _project(shape, rs.d_freqs, rs.d_amps, rs.d_count, rs.cap, alpha, off,
-                                    precision, dev)
+            for i in range(D + 1):
+                spec[i] -= _project(shape, rs.d_freqs, rs.d_amps, rs.d_count, rs.cap,
+                                    at_all[i:i + 1], proj[i], precision, dev, shape_c)
         floor = max(config.energy_floor_abs, config.energy_floor * amp_total)
         st, fr, am, nc = ops.decode_spectra_device(spec[None], alpha, tau, shape, config, floor,
                                                    precision=precision)
@@ -198,8 +201,9 @@ def fps_sft_large(cube, shape: CubeShape | None = None, config: FpsSftConfig = F
             nf = fr[0, acc_t].contiguous()[None]
             na = am[0, acc_t].contiguous()[None]
             cnt = torch.full((1,), n_acc, dtype=torch.int32, device=dev)
-            for i, off in enumerate(offs):
-                spec[i] -= _project(shape, nf, na, cnt, n_acc, alpha, off, precision, dev)
+            for i in range(D + 1):
+                spec[i] -= _project(shape, nf, na, cnt, n_acc, at_all[i:i + 1], proj[i],
+                                    precision, dev, shape_c)
         else:
             stall += 1
         if float(spec.abs().max()) <= max(config.energy_floor_abs,
