@@ -210,3 +210,28 @@ def test_schedules_from_seeds_pool_matches_serial():
     # forced through the process pool
     np.testing.assert_array_equal(schedules_from_seeds(shape, seeds * 30, 40, workers=2),
                                   np.concatenate([want] * 30))
+
+
+def test_segment_model_batch_major_and_interleaved():
+    """bench.py's DRAM-segment model: batch-major counts a segment per instance
+    that runs the iteration; the interleaved layout (group 8) counts each
+    sample position once per group, for its longest-running instance."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    from paper_1711_11407_b200 import CubeShape, schedule_from_seed
+
+    shape = CubeShape((16, 16))
+    sch = schedule_from_seed(shape, 3, 5)[None]
+    one = bench._segments_per_launch(shape, sch, np.array([1]))
+    assert bench._segments_per_launch(shape, sch, np.full(16, 1)) == 16 * one
+    # group of 8 with equal iteration counts: every (line, sample) position is its own
+    # segment, shared by the group
+    positions = bench._segments_per_launch(shape, sch, np.array([1]), seg=1)
+    assert bench._segments_per_launch(shape, sch, np.full(16, 1), group=8) == 2 * positions
+    # a group runs as long as its slowest member
+    its = np.array([1] * 7 + [2] + [1] * 8)
+    two = bench._segments_per_launch(shape, sch, np.array([2]), seg=1)
+    assert bench._segments_per_launch(shape, sch, its, group=8) == two + positions
