@@ -49,6 +49,12 @@
 #ifndef FPSSFT_WARP_NT
 #define FPSSFT_WARP_NT 256  // largest CTA of the warp kernel (FPSSFT_WARP_NT / 32 instances)
 #endif
+#ifndef FPSSFT_WARP_W
+#define FPSSFT_WARP_W 0  // A/B builds only: force the warp kernel's instances per CTA (0 = planner)
+#endif
+#ifndef FPSSFT_TEAM_NT
+#define FPSSFT_TEAM_NT 0  // A/B builds only: force the team kernel's CTA size (0 = planner)
+#endif
 #ifndef FPSSFT_WARP_MINB
 #define FPSSFT_WARP_MINB 2  // CTAs of FPSSFT_WARP_NT threads per SM its registers must allow
 #endif
@@ -872,7 +878,6 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
 
 #include "fpssft_regfft.cuh"
 #include "fpssft_team.cuh"
-#include "fpssft_warp_il.cuh"
 #include "fpssft_synth.cuh"
 
 // ------------------------------------------------------------ re-synthesis
@@ -1505,28 +1510,6 @@ const void *warp_kernel_for(const Geo &g, int precision) {
     return precision == FPSSFT_F64 ? warp_kernel_for_t<double>(g) : warp_kernel_for_t<float>(g);
 }
 
-// Instances per warp of the interleaved warp kernel; off (1) by default:
-// measured on config 2/3 it loses to one instance per warp (half the warps
-// resident, 0.33 vs 0.225 ms) -- the loop is bound by per-warp dependency
-// latency, not by gather/compute phase alignment.  FPSSFT_IL=2|3 enables it.
-int il_instances_per_warp() {
-    const char *e = std::getenv("FPSSFT_IL");
-    const int v = e ? std::atoi(e) : 1;
-    return v < 1 ? 1 : (v > 3 ? 3 : v);
-}
-const void *il_kernel_for(const Geo &g, int precision, int ni) {
-    if (precision != FPSSFT_F32 || !g.off32) return nullptr;
-#define FPSSFT_IL_CASE(L_, D_)                                                             \
-    if (g.L == L_ && g.D == D_)                                                            \
-        return ni == 2 ? (const void *)recover_warp_il_kernel<float, L_, D_, 2>             \
-                       : (const void *)recover_warp_il_kernel<float, L_, D_, 3>;
-    FPSSFT_IL_CASE(256, 2)
-    FPSSFT_IL_CASE(512, 2)
-    FPSSFT_IL_CASE(64, 3)
-#undef FPSSFT_IL_CASE
-    return nullptr;
-}
-
 // The compile-time team kernel for a shape (one CTA of *nt threads per
 // instance), or nullptr if the shape has none.
 template <class R>
@@ -1601,10 +1584,9 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
             const int regs = (warp_kernel_regs(gw, precision) + 7) / 8 * 8;
             const long long reg_warps = 65536 / (regs * 32);
             int best_w = 0;
-            const char *wenv = std::getenv("FPSSFT_WARP_W");  // occupancy experiments
             for (int w : {8, 7, 6, 5, 4, 3, 2, 1}) {
                 if (32 * w > FPSSFT_WARP_NT) continue;
-                if (wenv && std::atoi(wenv) != w) continue;
+                if (FPSSFT_WARP_W && w != FPSSFT_WARP_W) continue;  // compile-time A/B
                 const long long smem = (long long)wl.roots + w * (long long)wl.per_warp;
                 if (smem > SMEM_PER_CTA) continue;
                 const long long ctas = std::min<long long>(
@@ -1618,27 +1600,6 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
                 wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * best_w, best_w,
                                 wl.roots + (size_t)best_w * wl.per_warp,
                                 warp_kernel_for(gw, precision)};
-            // interleaved variant (NI instances per warp, float32, compile-time
-            // shapes): same resident instances with the gathers pipelined
-            const int ni = il_instances_per_warp();
-            const void *ik = ni > 1 ? il_kernel_for(gw, precision, ni) : nullptr;
-            if (best_w && ik) {
-                long long best_inst = 0;
-                int bw = 0;
-                for (int w : {4, 2, 1}) {
-                    const long long smem = (long long)wl.roots + (long long)w * ni * wl.per_warp;
-                    if (smem > SMEM_PER_CTA) continue;
-                    const long long ctas = std::min<long long>(
-                        {32, SMEM_PER_SM / (smem + SMEM_RESERVED), 64 / w, reg_warps / w});
-                    if (ctas * w * ni > best_inst) {
-                        best_inst = ctas * w * ni;
-                        bw = w;
-                    }
-                }
-                if (bw)  // explicit opt-in (FPSSFT_IL): used whenever it fits
-                    wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * bw, bw * ni,
-                                    wl.roots + (size_t)bw * ni * wl.per_warp, ik};
-            }
         }
         if (want == FPSSFT_MODE_WARP) {
             if (!warp_warps)
@@ -1656,10 +1617,9 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
     long long team_warps = 0, team_inst = 0;
     LaunchPlan tp{};
     if (g.key_bits_ <= 31 && kn.k_cap <= 32768) {
-        const char *env = std::getenv("FPSSFT_TEAM_NT");
         for (int want_nt : {512, 0}) {
-            if (env && want_nt) continue;  // experiments: one pass at the requested size
-            const int req = env ? std::atoi(env) : want_nt;
+            if (FPSSFT_TEAM_NT && want_nt) continue;  // compile-time A/B: one pass at that size
+            const int req = FPSSFT_TEAM_NT ? FPSSFT_TEAM_NT : want_nt;
             int tnt = req;
             const void *tk = team_kernel_for(g, precision, &tnt);
             if (!tk || (req && tnt != req)) continue;

@@ -109,31 +109,6 @@ def test_interleaved_layout_matches_batch_major(cfg_id, count, k_cap, group):
         g.run(cubes)  # batch-major tensor handed to a grouped runner
 
 
-def test_cli_recover_end_to_end(tmp_path):
-    """``python -m paper_1711_11407_b200 recover`` (reference cli.py:117-171):
-    generated truth, device recovery, files written, exit 0 on a match."""
-    import json as _json
-
-    from paper_1711_11407_b200 import cli
-    from paper_1711_11407_b200.spectrum_io import load_spectrum
-
-    out = tmp_path / "rec"
-    rc = cli.main(["recover", "--shape", "32x32", "--k", "5", "--seed", "3", "--out", str(out)])
-    assert rc == 0
-    rep = _json.loads((out / "report.json").read_text())
-    assert rep["success"] and rep["k_recovered"] == 5 and rep["k_true"] == 5
-    assert rep["samples_used"] == rep["iterations_run"] * 3 * 32
-    got = load_spectrum(out / "recovered_spectrum.txt")
-    args = cli.build_parser().parse_args(["recover", "--shape", "32x32", "--k", "5"])
-    truth = cli.truth_spectrum(args, cli.split_seed(3)[0])
-    assert list(got.entries) == list(truth.entries)
-    assert (out / "manifest.json").exists()
-    # round trip through a spectrum file as the ground truth
-    rc = cli.main(["recover", "--input", str(out / "recovered_spectrum.txt"), "--seed", "5",
-                   "--out", str(tmp_path / "rec2")])
-    assert rc == 0
-
-
 @pytest.mark.parametrize("prec", ["fp32", "fp64"])
 def test_interleaved_layout_with_per_instance_schedules(prec):
     """Grouped layout with one schedule per instance (Monte Carlo style) and in

@@ -424,26 +424,6 @@ def test_sweep_paper_anchors_c5_c6():
     assert 0.04 <= row.mean_percent_samples <= 0.08, row
 
 
-def test_interleaved_warp_kernel_matches_oracle(monkeypatch):
-    """The opt-in interleaved warp kernel (FPSSFT_IL=2) makes the same
-    decisions as the oracle."""
-    monkeypatch.setenv("FPSSFT_IL", "2")
-    w = W.CONFIGS[2]
-    inst, cubes = _batch(w, 12)
-    cfg = P.FpsSftConfig(seed=2, **G.PROFILES["P32"])
-    r = P.BatchRunner(P.CubeShape(w.dims), cfg, 12, k_cap=128, iter_stats=True, device=DEV)
-    assert r.plan["instances_per_cta"] % 2 == 0  # the interleaved kernel was planned
-    res = r.run(cubes)
-    prof = O.Profile(**G.PROFILES["P32"])
-    for b, (_, _, cube) in enumerate(inst):
-        ref = O.recover(cube, w.dims, prof, seed=2)
-        exp = dict(freqs=ref.freqs, amps=ref.amps, terminated_by=ref.terminated_by,
-                   iterations_run=ref.iterations_run, samples_used=ref.samples_used,
-                   log_alpha=[x[0] for x in ref.log], log_tau=[x[1] for x in ref.log],
-                   log_counts=[x[2:] for x in ref.log])
-        _check_report(res.report(b), exp, 1e-4)
-
-
 def test_lazy_spectrum_source_synthesised_on_device():
     """A lazy mixture exposing ``spectrum`` (like the reference's
     SyntheticSource) is materialised with fpssft_synthesize and recovered."""
