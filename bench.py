@@ -3,33 +3,42 @@
 instances (BASELINE.json config 2 by default: 4096 x 256x256 complex64,
 K=100, noiseless, profile P32).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--scaling strong|weak]
     python bench.py --impl reference ...      # the CPU reference arm
 
 One step = one ``fpssft_run_batch`` (one fused kernel launch) over the
 rank's batch, cubes resident in HBM.  L2 is flushed (256 MiB write) before
-every timed step and only the step is inside the CUDA events.  Multi-GPU
-(torchrun): every rank owns its own slice of the instance stream (weak
-scaling, no data-path collective); time = max over ranks.
+every timed step and only the step is inside the CUDA events.
+
+Multi-GPU: ``--gpus N`` is N ranks, one process per GPU -- started by
+torchrun, or spawned here (``shard.launch``) when the environment has no
+``WORLD_SIZE``.  ``--scaling strong`` (default) splits the config's global
+batch (4096 instances for config 2, 16384 frames for config 5) into N
+contiguous slices; ``weak`` gives every rank the whole batch.  No
+collective sits on the data path: each rank times its own launches, the job
+time is the max over ranks, and the padded results are gathered to rank 0
+over NCCL after the timed region (timed separately, ``gather``).
 
 The JSON line adds ``roofline`` (algorithmic gather bytes per launch over
 the launch time vs the measured HBM copy peak), ``cpu_baseline`` (the CPU
 oracle port on this host's cores over a bounded sample of the same
-inputs), ``e2e`` (through the public API from pinned host buffers, copies
-included) and ``clocks`` (nvidia-smi sampled during the run).
+inputs), ``parity`` (the GPU results of exactly those instances against the
+oracle's), ``batch_major`` (the same step on the drop-in [B, *dims] layout),
+``e2e`` (through the public API from pinned host buffers, copies included)
+and ``clocks`` (nvidia-smi sampled during the run).
 """
 
 from __future__ import annotations
 
 import argparse
+import glob
 import json
-import math
 import os
+import re
 import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 import numpy as np
@@ -40,9 +49,12 @@ sys.path.insert(0, ROOT)
 METRIC = "FPS-SFT transforms/sec"
 UNIT = "transforms/s"
 # recovered-set capacity per config (power of two >= K plus false positives);
-# an overflow seen in the untimed warm-up doubles it (reported in config)
+# an overflow seen in the untimed warm-up doubles it (reported in run.k_cap)
 K_CAP = {1: 64, 2: 128, 3: 512, 4: 2048, 5: 1024}
 FLUSH_BYTES = 256 << 20
+# north-star amplitude tolerance (BASELINE.json): noiseless / noisy profiles
+AMP_TOL = {"P32": 1e-4, "P64": 1e-4, "PN": 1e-3}
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
 def _cfg(w, seed):
@@ -64,8 +76,6 @@ def _probe_rate():
     """Random 64-byte-segment fetch rate of this GPU measured by
     tools/gather_probe.cu (variant 2: 8-byte loads with the .L2::64B fetch
     size, 2^28-element array, all SMs)."""
-    import re
-
     try:
         for line in open(os.path.join(ROOT, "profiles", "r01_gather_probe.txt")):
             m = re.search(r"2\^28 x8B\s+ctas\s+1184\s+variant 2:.*?([0-9.]+) Gsamples/s", line)
@@ -120,63 +130,117 @@ def _segments_per_launch(shape, schedule, iterations, sched_index=None, seg=8, g
     return total
 
 
-def _traffic(workload_name, batch=None):
-    """DRAM bytes per launch from the committed ncu capture, if any (a capture
-    of a subset, "<cfgN>_recover_subset<n>", scaled to ``batch`` instances)."""
+def _traffic(workload_name, batch, full_batch):
+    """DRAM bytes per launch of ``batch`` instances from the committed ncu
+    capture: a capture of the config's full batch (``full_batch``) or of a
+    subset ("<cfgN>_recover_subset<n>"), scaled linearly to ``batch``."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             d = json.load(fh)
     except Exception:
         return None
     if workload_name in d:
-        return d[workload_name]
+        return int(d[workload_name] * batch / full_batch)
     pre = workload_name.split("_")[0] + "_recover_subset"
     for k, v in d.items():
-        if k.startswith(pre) and batch:
+        if k.startswith(pre):
             return int(v * batch / int(k[len(pre):]))
     return None
 
 
-# ---------------------------------------------------------------- CPU arm
-_SAMPLE = None  # (cubes, dims, profile kwargs, seed) inherited by forked workers
+def batch_plan(args, w, world):
+    """(global batch, instances per rank) for the scaling mode."""
+    B = args.batch or w.batch
+    if args.scaling == "weak":
+        return B * world, B
+    if B % world:
+        raise SystemExit(f"strong scaling: global batch {B} is not divisible by {world} ranks")
+    return B, B // world
 
 
-def _oracle_chunk(idx):
+def workload_config(args, w, world):
+    """The ``config`` dict of both arms (static: what was asked for, not
+    what the run observed), so the driver can match the two lines."""
+    B, per = batch_plan(args, w, world)
+    return {"workload": w.name, "global_batch": B, "instances_per_rank": per,
+            "dims": list(w.dims), "k": w.k, "profile": w.profile,
+            "precision": args.precision, "scaling": args.scaling,
+            "parallelism": f"dp{world} (instances)",
+            "l2": "flushed (256 MiB write) before every timed step"}
+
+
+# ---------------------------------------------------------------- CPU arms
+_SAMPLE = None  # (cubes, dims, profile kwargs, seed, synth, kind) inherited by forked workers
+
+
+def _ref_module():
+    """The unmodified reference package installed in baseline/_ref, or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "fps_sft")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import fps_sft
+    except Exception:
+        return None
+    if not os.path.abspath(fps_sft.__file__).startswith(REF_DIR):
+        return None
+    return fps_sft
+
+
+def _cpu_chunk(idx):
+    """Worker: recover ``cubes[idx]`` (and re-synthesise, config 5) with the
+    oracle port or the unmodified reference.  Returns (busy seconds,
+    per-instance results)."""
+    cubes, dims, prof, seed, synth, kind = _SAMPLE
+    out = []
+    if kind == "reference":
+        R = _ref_module()
+        shape = R.CubeShape(tuple(dims))
+        cfg = R.FpsSftConfig(seed=seed, **prof)
+        grid = np.indices(dims).reshape(len(dims), -1).T if synth else None
+        t0 = time.perf_counter()
+        for i in idx:
+            rep = R.fps_sft(R.make_dense_source(cubes[i], shape), cfg)
+            if synth:  # the reference's own evaluation of the recovered mixture
+                R.make_synthetic_source(rep.recovered).sample_many(grid)
+            out.append((i, rep.iterations_run, rep.terminated_by, None, None))
+        return time.perf_counter() - t0, out
     from oracle import fps_oracle as O
 
-    cubes, dims, prof, seed, synth = _SAMPLE
     p = O.Profile(**prof)
     t0 = time.perf_counter()
-    its = 0
     for i in idx:
         rep = O.recover(cubes[i], dims, p, seed=seed)
-        its += rep.iterations_run
         if synth:  # config 5 also re-synthesises the image (numpy ifftn of the spectrum)
             O.synthesize(dims, rep.freqs, rep.amps)
-    return time.perf_counter() - t0, its
+        out.append((i, rep.iterations_run, rep.terminated_by, rep.freqs, rep.amps))
+    return time.perf_counter() - t0, out
 
 
-def cpu_oracle_throughput(cubes: np.ndarray, dims, prof: dict, seed: int, workers: int,
-                          synth: bool = False):
-    """instances/s of the CPU oracle port over ``cubes`` on ``workers``
-    processes (the reference's own ProcessPoolExecutor parallelism,
-    oracle.py:275-277): instances / max worker busy time."""
+def cpu_throughput(cubes: np.ndarray, dims, prof: dict, seed: int, workers: int,
+                   synth: bool = False, kind: str = "port"):
+    """instances/s of the CPU path over ``cubes`` on ``workers`` processes
+    (the reference's own ProcessPoolExecutor parallelism, oracle.py:275-277):
+    instances / max worker busy time.  Also returns the per-instance results
+    in instance order."""
     import multiprocessing as mp
 
     global _SAMPLE
-    _SAMPLE = (cubes, tuple(dims), prof, seed, synth)
+    _SAMPLE = (cubes, tuple(dims), prof, seed, synth, kind)
     n = len(cubes)
     parts = [list(range(i, n, workers)) for i in range(workers)]
     parts = [p for p in parts if p]
     t0 = time.perf_counter()
     if len(parts) == 1:
-        res = [_oracle_chunk(parts[0])]
+        res = [_cpu_chunk(parts[0])]
     else:
         with mp.get_context("fork").Pool(len(parts)) as pool:
-            res = pool.map(_oracle_chunk, parts)
+            res = pool.map(_cpu_chunk, parts)
     wall = time.perf_counter() - t0
     busy = max(r[0] for r in res)
-    return n / busy, wall, sum(r[1] for r in res) / n
+    reports = sorted((x for r in res for x in r[1]), key=lambda x: x[0])
+    return n / busy, wall, reports
 
 
 def _host_sample(w, count, start=0):
@@ -185,47 +249,53 @@ def _host_sample(w, count, start=0):
     return np.stack([W.make_instance(w, r)[2] for r in W.instance_rngs(w.seed, count, start)])
 
 
-def _estimate_oracle_seconds(cubes, dims, prof, seed):
-    from oracle import fps_oracle as O
+def _estimate_seconds(cubes, dims, prof, seed, kind, synth=False):
+    global _SAMPLE
+    _SAMPLE = (cubes, tuple(dims), prof, seed, synth, kind)
+    n = min(2, len(cubes))
+    busy, _ = _cpu_chunk(list(range(n)))
+    return busy / n
 
-    t0 = time.perf_counter()
-    for c in cubes[:2]:
-        O.recover(c, dims, O.Profile(**prof), seed=seed)
-    return (time.perf_counter() - t0) / min(2, len(cubes))
 
-
-def run_reference(args, w):
+def run_reference(args, w, world):
+    """``--impl reference``: the unmodified reference (baseline/_ref, its
+    public ``fps_sft`` over ``make_dense_source``) on this host's cores, or
+    the oracle port when baseline/_ref is absent; bounded sample per step."""
     import paper_1711_11407_b200 as P
 
     cores = os.cpu_count() or 1
+    kind = "reference" if _ref_module() is not None else "port"
     prof = P.PROFILES[w.profile]
+    synth = args.config == 5
     probe = _host_sample(w, 2)
-    per = _estimate_oracle_seconds(probe, w.dims, prof, args.config)
+    per = _estimate_seconds(probe, w.dims, prof, args.config, kind, synth)
+    B, _ = batch_plan(args, w, world)
     # each step: a bounded sample sized for ~args.ref_step_seconds of wall time
-    count = int(max(cores, min(w.batch, args.ref_step_seconds * cores / max(per, 1e-4))))
+    count = int(max(cores, min(B, args.ref_step_seconds * cores / max(per, 1e-4))))
     cubes = _host_sample(w, count)
     for _ in range(args.warmup_ref):
-        cpu_oracle_throughput(cubes[:cores], w.dims, prof, args.config, cores)
+        cpu_throughput(cubes[:cores], w.dims, prof, args.config, cores, synth, kind)
     times, its = [], []
     for _ in range(args.steps):
-        rate, wall, mean_it = cpu_oracle_throughput(cubes, w.dims, prof, args.config, cores,
-                                                    synth=args.config == 5)
+        rate, wall, reps = cpu_throughput(cubes, w.dims, prof, args.config, cores, synth, kind)
         times.append(count / rate)
-        its.append(mean_it)
+        its.append(np.mean([r[1] for r in reps]))
     total = sum(times)
     value = count * args.steps / total
-    sample = (f"{count} of the {w.batch} instances of {w.name} (instances 0..{count - 1}), "
-              f"numpy float64 oracle port, {cores} worker processes"
-              + (", recovery + numpy re-synthesis" if args.config == 5 else ""))
+    what = ("unmodified reference fps_sft 0.1.0 (baseline/_ref) on make_dense_source"
+            if kind == "reference" else "numpy float64 oracle port (baseline/_ref absent)")
+    sample = (f"{count} of the {B} instances of {w.name} (instances 0..{count - 1}) per step, "
+              f"{what}, {cores} worker processes"
+              + (", recovery + re-synthesis of each frame" if synth else ""))
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; BASELINE.json names no dataset)",
-        "config": {"workload": w.name, "batch_per_step": count, "profile": w.profile,
-                   "mean_iterations": float(np.mean(its))},
+        "config": workload_config(args, w, world),
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "run": {"mean_iterations": float(np.mean(its)), "batch_per_step": count},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -278,76 +348,122 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded)}
 
 
+# ---------------------------------------------------------------- parity
+def parity_summary(gpu: dict, reports, tol: float) -> dict:
+    """GPU results of the sampled instances vs the oracle's reports of the
+    same cubes: support, iterations/termination and amplitudes (north-star
+    tolerance ``tol``, relative, on identical supports)."""
+    from paper_1711_11407_b200 import _native as N
+
+    n = len(reports)
+    same_sup = same_it = 0
+    worst = 0.0
+    for i, its, term, freqs, amps in reports:
+        c = int(gpu["count"][i])
+        f = gpu["freqs"][i, :c].astype(np.int64)
+        a = gpu["amps"][i, :c]
+        if f.shape == freqs.shape and np.array_equal(f, freqs):
+            same_sup += 1
+            if c:
+                worst = max(worst, float(np.max(np.abs(a - amps) / np.abs(amps))))
+        same_it += (int(gpu["iterations"][i]) == its
+                    and N.TERM_NAMES[int(gpu["terminated_by"][i])] == term)
+    return {"instances": n, "identical_support": same_sup, "identical_iterations": same_it,
+            "max_rel_amp_err": worst, "tolerance": tol,
+            "pass": same_sup == n and same_it == n and worst <= tol,
+            "oracle": "oracle/fps_oracle.py (float64 numpy port, pinned to the reference's "
+                      "golden runs), same complex64 cubes and schedule"}
+
+
+# ---------------------------------------------------------------- NCCL evidence
+def _nccl_log_setup(rank):
+    if "NCCL_DEBUG" in os.environ:
+        return None
+    path = os.path.join(tempfile.gettempdir(), f"fpssft_bench_nccl.{os.getpid()}.log")
+    os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,NVLS",
+                      NCCL_DEBUG_FILE=path)
+    return path
+
+
+def _nccl_log_summary(path):
+    if not path:
+        return None
+    txt = ""
+    for p in glob.glob(path + "*") + [path]:
+        try:
+            txt += open(p).read()
+        except OSError:
+            pass
+    m = re.findall(r"nRanks (\d+)", txt)
+    return {"nranks": int(m[-1]) if m else None,
+            "nvls": bool(re.search(r"NVLS multicast support is available", txt)),
+            "version": (re.findall(r"NCCL version ([0-9.]+)", txt) or [None])[-1]}
+
+
 # ---------------------------------------------------------------- GPU arm
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--layout", default="auto", choices=["auto", "batch_major", "interleaved"],
-                    help="HBM layout of the batch: [B, *dims], or [B/G, *dims, G] with G "
-                         "instances interleaved sample by sample (--group); auto = "
-                         "interleaved for batches of >= 64 instances")
-    ap.add_argument("--group", type=int, default=8)
-    ap.add_argument("--mode", default="auto", choices=["auto", "warp", "cta"],
-                    help="kernel family (auto: the planner's choice for this batch)")
-    ap.add_argument("--batch", type=int, default=None, help="override instances per rank")
-    ap.add_argument("--k-cap", type=int, default=None)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0,
-                    help="CPU-seconds budget of the cpu_baseline sample")
-    ap.add_argument("--ref-step-seconds", type=float, default=4.0)
-    ap.add_argument("--warmup-ref", type=int, default=1)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-synth", action="store_true", help="config 5 without re-synthesis")
-    ap.add_argument("--l2-fetch", type=int, default=32,
-                    help="cudaLimitMaxL2FetchGranularity in bytes (0 = leave the driver default)")
-    ap.add_argument("--load-seconds", type=float, default=1.0,
-                    help="back-to-back steps before the timed region (clock ramp/sampling)")
-    args = ap.parse_args()
+def _time_steps(run, steps, stream, flush, after=None):
+    """Per-step CUDA-event times (ms) of ``run()`` (and ``after(result)``),
+    L2 flushed before each step, outside the events."""
+    import torch
 
-    from paper_1711_11407_b200 import workloads as W
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    mids = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for i in range(steps):
+        flush.fill_(i)
+        starts[i].record(stream)
+        r = run()
+        mids[i].record(stream)
+        if after is not None:
+            after(r)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    return ([s.elapsed_time(e) for s, e in zip(starts, ends)],
+            [s.elapsed_time(e) for s, e in zip(starts, mids)],
+            [s.elapsed_time(e) for s, e in zip(mids, ends)])
 
-    w = W.CONFIGS[args.config]
-    if args.batch:
-        w = W.Workload(w.name, w.dims, args.batch, w.k, w.placement, w.magnitude, w.noise_var,
-                       w.profile, w.seed)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
 
-    if args.impl == "reference":
-        if rank == 0:
-            run_reference(args, w)
-        return
-
+def gpu_rank(args):
     import torch
 
     import paper_1711_11407_b200 as P
     from paper_1711_11407_b200 import ops
-    from paper_1711_11407_b200.shard import instance_range
+    from paper_1711_11407_b200 import shard
+    from paper_1711_11407_b200 import workloads as W
 
+    rank, local, world = shard.env_rank()
+    w = W.CONFIGS[args.config]
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the GPU arm has no CPU path)")
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} wants cuda:{local} but only "
+                         f"{torch.cuda.device_count()} GPU(s) are visible")
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     l2_default = P._native.get_l2_fetch_granularity(dev)
     if args.l2_fetch:
         P._native.set_l2_fetch_granularity(args.l2_fetch, dev)
     dist = None
+    nccl_log = None
     if world > 1:
         import torch.distributed as dist
 
+        nccl_log = _nccl_log_setup(rank)
         dist.init_process_group("nccl", device_id=dev)
+        ones = torch.ones(1, device=dev)
+        dist.all_reduce(ones)  # communicator up; its size is checked below
+        comm_check = int(ones.item())
 
-    B = w.batch
-    b0, b1 = instance_range(rank, world, per_rank=B)
+    B_total, B = batch_plan(args, w, world)
+    if args.scaling == "weak":
+        b0, b1 = shard.instance_range(rank, world, per_rank=B)
+    else:
+        b0, b1 = shard.instance_range(rank, world, total=B_total)
     shape = P.CubeShape(w.dims)
     cfg = _cfg(w, args.config)
     k_cap = args.k_cap or K_CAP[args.config]
 
-    # ---- inputs: spectra on the host, cubes synthesised on the device
+    # ---- inputs: this rank's spectra on the host, cubes synthesised on its device
     spectra = W.make_spectra(w, B, b0)
     cubes = W.synthesize_batch_torch(w.dims, spectra, dev, w.noise_var,
                                      noise_seed=w.seed * 1000003 + b0)
@@ -358,30 +474,31 @@ def main():
     group = args.group if layout == "interleaved" else 1
     run_cubes = P.interleave(cubes, group) if group > 1 else cubes
     torch.cuda.synchronize()
-    runner = P.BatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision, device=dev,
-                           mode=args.mode, group=group)
+
+    def make_runner(kc, grp):
+        return P.BatchRunner(shape, cfg, B, k_cap=kc, precision=args.precision, device=dev,
+                             mode=args.mode, group=grp)
+
+    runner = make_runner(k_cap, group)
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     res = runner.run(run_cubes)
     while int((res.terminated_by == 3).sum()) > 0:  # k_cap overflow: widen, untimed
         k_cap *= 2
-        runner = P.BatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision, device=dev,
-                               mode=args.mode, group=group)
+        runner = make_runner(k_cap, group)
         res = runner.run(run_cubes)
     for _ in range(max(3, args.warmup)):
         res = runner.run(run_cubes)
     torch.cuda.synchronize()
-    count = res.count.cpu().numpy()
-    term = res.terminated_by.cpu().numpy()
-    samples = res.samples_used.cpu().numpy()
-    iters = res.iterations.cpu().numpy()
+    host_res = {k: v.cpu().numpy() for k, v in runner.out.items() if v is not None}
+    count, term = host_res["count"], host_res["terminated_by"]
+    samples, iters = host_res["samples_used"], host_res["iterations"]
     bytes_per_launch = int(samples.sum()) * 8  # complex64 samples gathered (driver.py:208)
 
     gpu_id = str(local)
     try:
-        uuid = torch.cuda.get_device_properties(dev).uuid
-        gpu_id = f"GPU-{uuid}"
+        gpu_id = f"GPU-{torch.cuda.get_device_properties(dev).uuid}"
     except Exception:
         pass
     clocks = ClockSampler(gpu_id)
@@ -396,50 +513,69 @@ def main():
     # config 5 recovers *and* re-synthesises every image (BASELINE.json)
     synth = args.config == 5 and not args.no_synth
     img = torch.empty_like(cubes) if synth else None
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if synth:
         ops.synthesize(runner.run(run_cubes), out=img)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    for i in range(args.steps):
-        flush.fill_(i)
-        starts[i].record(stream)
-        r = runner.run(run_cubes)
-        mids[i].record(stream)
-        if synth:
-            ops.synthesize(r, out=img)
-        ends[i].record(stream)
-    torch.cuda.synchronize()
+    step_ms, recover_ms, synth_ms = _time_steps(
+        lambda: runner.run(run_cubes), args.steps, stream, flush,
+        (lambda r: ops.synthesize(r, out=img)) if synth else None)
     if dist:
         dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    recover_ms = [s.elapsed_time(e) for s, e in zip(starts, mids)]
-    synth_ms = [s.elapsed_time(e) for s, e in zip(mids, ends)]
-    total_ms = sum(step_ms)
     clk = clocks.stop()
-    if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = shard.max_over_ranks(sum(step_ms), dev)
     ms_per_step = total_ms / args.steps
-    value = world * B / (ms_per_step / 1e3)
+    value = B_total / (ms_per_step / 1e3)
+
+    # ---- the same step on the batch-major layout the drop-in receives
+    batch_major = None
+    if group > 1 and not args.no_batch_major:
+        bm = make_runner(k_cap, 1)
+        for _ in range(max(3, args.warmup)):
+            bm.run(cubes)
+        torch.cuda.synchronize()
+        bm_ms, _, _ = _time_steps(lambda: bm.run(cubes), args.steps, stream, flush)
+        bm_total = shard.max_over_ranks(sum(bm_ms), dev)
+        same = all(torch.equal(bm.out[k], runner.out[k]) for k in bm.out if bm.out[k] is not None)
+        batch_major = {"value": B_total / (bm_total / args.steps / 1e3), "unit": UNIT,
+                       "ms_per_step": bm_total / args.steps,
+                       "layout": "batch-major [B, *dims] complex64 (what fps_sft_batch and "
+                                 "make_dense_source users hand in)",
+                       "outputs_identical_to_interleaved": bool(same)}
+        del bm
+
+    # ---- result gather to rank 0 over NCCL (after the timed region, timed alone)
+    gather = None
+    if dist:
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        got = shard.gather_results(runner.out, dst=0)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        g_ms = shard.max_over_ranks(g0.elapsed_time(g1), dev)
+        ok = None
+        if rank == 0:
+            ok = int(got["count"].shape[0]) == B * world
+        gather = {"ms": g_ms, "bytes_per_rank": shard.result_bytes(runner.out),
+                  "collective": "torch.distributed.gather to rank 0 (NCCL)",
+                  "rows_on_rank0": int(got["count"].shape[0]) if rank == 0 else None,
+                  "complete": ok}
 
     peak, peak_kind = _peaks()
     rec_ms = sum(recover_ms) / args.steps
     achieved = bytes_per_launch / (rec_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": _traffic(w.name, B),
+                "frac": achieved / peak, "traffic": _traffic(w.name, B, w.batch),
                 "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": bytes_per_launch,
                 "kernel": "recover (" + runner.plan["mode"] + " per instance)",
                 "kernel_ms": rec_ms,
                 "note": "achieved = sum(samples_used)*8 B gathered per launch / mean launch time"}
     if roofline["traffic"]:
-        # useful sample bytes per DRAM byte moved (ceiling ~0.33 for scattered 8-byte
-        # samples in 64-byte segments)
+        # useful sample bytes per DRAM byte moved
         roofline["sector_efficiency"] = bytes_per_launch / roofline["traffic"]
     probe = _probe_rate()
     segs = _segments_per_launch(shape, runner.schedule_host, iters, group=group)
@@ -458,10 +594,7 @@ def main():
                                  "frac": wbytes / (s_ms / 1e3) / 1e9 / peak}
 
     # ---- e2e through the public API: cubes in pinned host memory -> recovered
-    #      spectra (and config-5 images) in pinned host memory.  HostBatchRunner
-    #      splits each host batch between zero-copy gathers (only the sampled
-    #      bytes cross the host link) and double-buffered bulk copies, with the
-    #      split tuned untimed on this batch (hostpath.py).
+    #      spectra (and config-5 images) in pinned host memory (hostpath.py)
     e2e = None
     if not args.no_e2e:
         from paper_1711_11407_b200.hostpath import HostBatchRunner
@@ -493,15 +626,11 @@ def main():
         h2d = n_host * ((hb - bz) * cube_bytes + 16 * zc_samples)
         d2h = n_host * (sum(v.numel() * v.element_size() for v in o.values() if v is not None)
                         + (himg.numel() * himg.element_size() if synth else 0))
-        e_total = sum(e_ms)
-        if dist:
-            t = torch.tensor([e_total], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_total = float(t.item())
-        e2e = {"value": world * B * e_steps / (e_total / 1e3), "unit": UNIT,
+        e_total = shard.max_over_ranks(sum(e_ms), dev)
+        e2e = {"value": B_total * e_steps / (e_total / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": e_total / e_steps,
-               "path": f"{n_host} x {hb} instances from pinned host memory per step: "
+               "path": f"{n_host} x {hb} instances from pinned host memory per step per rank: "
                        f"{bz} gathered in place (zero copy), {hb - bz} copied in "
                        f"{hr.chunk}-instance double-buffered chunks (split {frac:.2f} tuned "
                        f"untimed); results{' and images' if synth else ''} to pinned host",
@@ -509,48 +638,105 @@ def main():
                        "sample (one 16-byte read request each) for the zero-copy part"}
         del host, himg, hr
 
-    # ---- CPU baseline on this host (rank 0, N=1), same inputs
-    cpu = None
+    # ---- CPU baseline on this host (rank 0, N=1), same inputs; parity of the
+    #      GPU results of exactly those instances against the oracle's
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        probe = cubes[:2].cpu().numpy()
-        per = _estimate_oracle_seconds(probe, w.dims, P.PROFILES[w.profile], args.config)
+        prof = P.PROFILES[w.profile]
+        probe_c = cubes[:2].cpu().numpy()
+        per = _estimate_seconds(probe_c, w.dims, prof, args.config, "port", synth)
         n = int(max(cores, min(B, args.cpu_seconds / max(per, 1e-4))))
         sample = cubes[:n].cpu().numpy()
-        rate, wall, mean_it = cpu_oracle_throughput(sample, w.dims, P.PROFILES[w.profile],
-                                                    args.config, cores, synth=synth)
+        rate, wall, reps = cpu_throughput(sample, w.dims, prof, args.config, cores,
+                                          synth=synth)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"instances 0..{n - 1} of this run's {w.name} batch (same complex64 "
                          f"cubes), numpy float64 oracle port, {cores} processes, "
                          f"{wall:.1f} s wall",
-               "mean_iterations": mean_it}
+               "mean_iterations": float(np.mean([r[1] for r in reps]))}
+        parity = parity_summary(host_res, reps, AMP_TOL[w.profile])
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f32" if args.precision == "fp32" else "f64",
             "data": "synthetic (seeded; BASELINE.json names no dataset)",
-            "config": {"workload": w.name, "instances_per_gpu": B, "dims": list(w.dims),
-                       "k": w.k, "profile": w.profile, "k_cap": k_cap,
-                       "kernel": runner.plan,
-                       "precision": args.precision, "parallelism": f"dp{world} (instances)",
-                       "layout": (f"interleaved [B/{group}, *dims, {group}] complex64 (group of "
-                                  f"{group} instances per 64-byte sample segment, DESIGN.md 4)"
-                                  if group > 1 else "batch-major [B, *dims] complex64"),
-                       "l2": "flushed (256 MiB write) before every timed step",
-                       "l2_fetch_granularity": {"set": args.l2_fetch, "driver_default": l2_default},
-                       "mean_iterations": float(iters.mean()),
-                       "recovered_per_instance_mean": float(count.mean()),
-                       "terminated_clean": int((term == 0).sum())},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "config": workload_config(args, w, world),
+            "run": {"k_cap": k_cap, "kernel": runner.plan,
+                    "layout": (f"interleaved [B/{group}, *dims, {group}] complex64 (group of "
+                               f"{group} instances per 64-byte sample segment, DESIGN.md 4)"
+                               if group > 1 else "batch-major [B, *dims] complex64"),
+                    "l2_fetch_granularity": {"set": args.l2_fetch, "driver_default": l2_default},
+                    "mean_iterations": float(iters.mean()),
+                    "recovered_per_instance_mean": float(count.mean()),
+                    "terminated_clean": int((term == 0).sum()),
+                    "rank0_instances": [b0, b1]},
+            "roofline": roofline, "parity": parity, "cpu_baseline": cpu,
+            "batch_major": batch_major, "e2e": e2e, "clocks": clk,
             "gpu_launches": args.steps * (int(P._native.lib().fpssft_launches_per_batch())
                                           + (1 if synth else 0)),
         }
+        if world > 1:
+            line["comm"] = {"backend": "nccl", "world": world, "allreduce_ones": comm_check,
+                            "log": _nccl_log_summary(nccl_log)}
+            line["gather"] = gather
         print(json.dumps(line), flush=True)
     if dist:
+        dist.barrier()
         dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's global batch split over the ranks; weak: the "
+                         "whole batch on every rank")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--layout", default="auto", choices=["auto", "batch_major", "interleaved"],
+                    help="HBM layout of the batch: [B, *dims], or [B/G, *dims, G] with G "
+                         "instances interleaved sample by sample (--group); auto = "
+                         "interleaved for batches of >= 64 instances")
+    ap.add_argument("--group", type=int, default=8)
+    ap.add_argument("--mode", default="auto", choices=["auto", "warp", "cta"],
+                    help="kernel family (auto: the planner's choice for this batch)")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="override the global batch (strong) / per-rank batch (weak)")
+    ap.add_argument("--k-cap", type=int, default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="CPU-seconds budget of the cpu_baseline sample")
+    ap.add_argument("--ref-step-seconds", type=float, default=4.0)
+    ap.add_argument("--warmup-ref", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-batch-major", action="store_true")
+    ap.add_argument("--no-synth", action="store_true", help="config 5 without re-synthesis")
+    ap.add_argument("--l2-fetch", type=int, default=32,
+                    help="cudaLimitMaxL2FetchGranularity in bytes (0 = leave the driver default)")
+    ap.add_argument("--load-seconds", type=float, default=1.0,
+                    help="back-to-back steps before the timed region (clock ramp/sampling)")
+    args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+
+    from paper_1711_11407_b200 import shard
+    from paper_1711_11407_b200 import workloads as W
+
+    if args.impl == "reference":
+        rank, _, world = shard.env_rank()
+        if "WORLD_SIZE" not in os.environ:
+            world = args.gpus
+        if rank == 0:  # one CPU measurement for the job; other ranks have no work
+            run_reference(args, W.CONFIGS[args.config], world)
+        return
+    shard.launch(args.gpus, gpu_rank, args)
 
 
 if __name__ == "__main__":

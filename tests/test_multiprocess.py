@@ -72,3 +72,85 @@ def test_gather_results_gloo_world2():
     assert iters == [1, 1, 1, 2, 2, 2]
     assert amps == [0j, 0j, 0j, (1 - 1j), (1 - 1j), (1 - 1j)]
     assert fshape == (6, 4, 2)
+
+
+# ---- the bench's N-rank launcher (shard.launch) end to end on CPU ranks
+def _bench_like_rank(out_path, total):
+    """One rank of a strong-scaled job: its contiguous slice of ``total``
+    tiny instances recovered (by the CPU oracle, standing in for the device
+    kernel), padded results gathered to rank 0, the time reduced as a max."""
+    import numpy as np
+
+    from oracle import fps_oracle as O
+    from paper_1711_11407_b200 import shard
+    from paper_1711_11407_b200 import workloads as W
+
+    rank, local, world = shard.env_rank()
+    dist.init_process_group("gloo")
+    try:
+        b0, b1 = shard.instance_range(rank, world, total=total)
+        outs = _oracle_outputs(W, O, np, b0, b1)
+        got = shard.gather_results(outs)
+        t = shard.max_over_ranks(float(rank + 1))
+        if rank == 0:
+            torch.save({"world": world, "span": (b0, b1), "t": t,
+                        **{k: v for k, v in got.items()}}, out_path)
+    finally:
+        dist.destroy_process_group()
+
+
+def _oracle_outputs(W, O, np, b0, b1, k_cap=16):
+    dims = (16, 12)
+    w = W.Workload("t", dims, b1 - b0, 6, "uniform", "unit", 0.0, "P32", 77)
+    n = b1 - b0
+    outs = {"count": torch.zeros(n, dtype=torch.int32),
+            "iterations": torch.zeros(n, dtype=torch.int32),
+            "samples_used": torch.zeros(n, dtype=torch.int64),
+            "terminated_by": torch.zeros(n, dtype=torch.int32),
+            "freqs": torch.zeros((n, k_cap, 2), dtype=torch.int32),
+            "amps": torch.zeros((n, k_cap), dtype=torch.complex128)}
+    for j, r in enumerate(W.instance_rngs(77, n, b0)):
+        _, _, cube = W.make_instance(w, r)
+        rep = O.recover(cube, dims, O.P32, seed=5)
+        c = len(rep.amps)
+        outs["count"][j] = c
+        outs["iterations"][j] = rep.iterations_run
+        outs["samples_used"][j] = rep.samples_used
+        outs["freqs"][j, :c] = torch.as_tensor(rep.freqs.astype(np.int32))
+        outs["amps"][j, :c] = torch.as_tensor(rep.amps)
+    return outs
+
+
+def test_launch_spawns_world2_and_gathers(tmp_path):
+    """``shard.launch(2, ...)`` without torchrun spawns two ranks with the
+    torchrun environment; their disjoint slices gather on rank 0 into the
+    single-rank result, and the job time is the max over ranks."""
+    import numpy as np
+
+    from oracle import fps_oracle as O
+    from paper_1711_11407_b200 import shard
+    from paper_1711_11407_b200 import workloads as W
+
+    out = str(tmp_path / "r0.pt")
+    env = {k: os.environ.pop(k) for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK") if k in os.environ}
+    try:
+        shard.launch(2, _bench_like_rank, out, 6)
+    finally:
+        os.environ.update(env)
+    got = torch.load(out)
+    assert got["world"] == 2 and tuple(got["span"]) == (0, 3) and got["t"] == 2.0
+    want = _oracle_outputs(W, O, np, 0, 6)
+    for k, v in want.items():
+        assert torch.equal(got[k], v), k
+
+
+def test_launch_under_torchrun_env_checks_world(monkeypatch):
+    from paper_1711_11407_b200 import shard
+
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    with pytest.raises(ValueError):
+        shard.launch(2, lambda: None)
+    seen = []
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    shard.launch(2, lambda x: seen.append(x), 7)
+    assert seen == [7]
