@@ -662,10 +662,11 @@ def gpu_rank(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None,
-            "dtype": "f32" if args.precision == "fp32" else "f64",
+            "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic (seeded; BASELINE.json names no dataset)",
             "config": workload_config(args, w, world),
             "run": {"k_cap": k_cap, "kernel": runner.plan,
+                    "arithmetic": {0: "fp32", 1: "fp64", 2: "fp32-guarded"}[runner.prec],
                     "layout": (f"interleaved [B/{group}, *dims, {group}] complex64 (group of "
                                f"{group} instances per 64-byte sample segment, DESIGN.md 4)"
                                if group > 1 else "batch-major [B, *dims] complex64"),
@@ -699,7 +700,10 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: the config's global batch split over the ranks; weak: the "
                          "whole batch on every rank")
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--precision", default="auto",
+                    choices=["auto", "fp32", "fp32-guarded", "fp64"],
+                    help="auto: float32, guarded (exact float64 decisions) for the noisy "
+                         "profile; see driver._precision_code")
     ap.add_argument("--layout", default="auto", choices=["auto", "batch_major", "interleaved"],
                     help="HBM layout of the batch: [B, *dims], or [B/G, *dims, G] with G "
                          "instances interleaved sample by sample (--group); auto = "

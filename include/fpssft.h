@@ -34,6 +34,12 @@ extern "C" {
 /* arithmetic the path computes in (input cubes are always complex64) */
 #define FPSSFT_F32 0
 #define FPSSFT_F64 1
+/* float32 arithmetic with the float64 reference's decisions: float64
+ * amplitudes and line-0 transform, and every decision whose float32 statistic
+ * lies within its error bound of the threshold re-evaluated in float64
+ * (decoder.py:146-163, driver.py:103-108).  Shapes without a guarded kernel
+ * run the float64 kernels. */
+#define FPSSFT_F32_GUARDED 2
 
 /* execution mode: one warp or one whole CTA per instance (AUTO picks) */
 #define FPSSFT_MODE_AUTO 0

@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("FPSSFT_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libfpssft.so")  # FPSSFT_LIB: A/B builds
 MAX_DIMS = 4
 
-F32, F64 = 0, 1
+F32, F64, F32_GUARDED = 0, 1, 2
 MODE_AUTO, MODE_CTA, MODE_WARP = 0, 1, 2
 MODES = {"auto": MODE_AUTO, "cta": MODE_CTA, "warp": MODE_WARP}
 TERM_NAMES = {0: "residual_clean", 1: "stall", 2: "max_iterations", 3: "k_cap_overflow",

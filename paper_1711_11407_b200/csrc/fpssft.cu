@@ -18,6 +18,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <type_traits>
 
 #include "../../include/fpssft.h"
 #include "fpssft_device.cuh"
@@ -458,6 +459,8 @@ __global__ void __launch_bounds__(1024, 1) recover_kernel(const float2 *__restri
     }
 }
 
+#include "fpssft_guard.cuh"
+
 // ------------------------------------------------------ warp-per-instance
 // For short lines ((D+1) L <= 2048) one warp owns one instance: the same loop
 // as recover_kernel, but every step is warp-synchronous (__syncwarp, ballots,
@@ -470,12 +473,15 @@ __global__ void __launch_bounds__(1024, 1) recover_kernel(const float2 *__restri
 // open-addressing hash, and 32-entry scratch for the projection step.
 struct WarpLayout {
     size_t spec, slot_amp, slot_key, hash, slot_live, cand, scr_u, scr_amp;
-    size_t per_warp, roots;
+    size_t x0d, pabs;  // GUARD only
+    size_t per_warp, roots, roots64;
     int H;
 };
 
-__host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, int cs) {
+__host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, int cs,
+                                                       bool guard = false) {
     WarpLayout y;
+    const int acs = guard ? 16 : cs;  // slot amplitude bytes (complex128 when guarded)
     size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // room for padi()
     if (stage16_ok(D, L, cs, 32) && spec_bytes < (size_t)(D + 1) * L * 16)
         spec_bytes = (size_t)(D + 1) * L * 16;  // 16-byte staging slots (gather_lines_cg16)
@@ -483,15 +489,22 @@ __host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, 
     size_t o = 0;
     y.H = 2 * k_cap;
     y.spec = o;      o = align16(o + (spec_bytes > sort_bytes ? spec_bytes : sort_bytes));
-    y.slot_amp = o;  o = align16(o + (size_t)k_cap * cs);
+    y.slot_amp = o;  o = align16(o + (size_t)k_cap * acs);
     y.slot_key = o;  o = align16(o + (size_t)k_cap * 4);
     y.hash = o;      o = align16(o + (size_t)y.H * 2);
     y.slot_live = o; o = align16(o + (size_t)k_cap);
     y.cand = o;      o = align16(o + (size_t)L * 2);
     y.scr_u = o;     o = align16(o + 32 * 4 * (size_t)(D + 1));
-    y.scr_amp = o;   o = align16(o + 32 * (size_t)cs);
+    y.scr_amp = o;   o = align16(o + 32 * (size_t)acs);
+    y.x0d = y.pabs = o;
+    if (guard) {
+        y.x0d = o;   o = align16(o + (size_t)(L + L / 16 + 1) * 16);
+        y.pabs = o;  o = align16(o + (size_t)L * 4);
+    }
     y.per_warp = o;
-    y.roots = align16((size_t)L * cs);
+    // per CTA: the float32 root table, then (guarded) the float64 one
+    y.roots64 = align16((size_t)L * cs);  // lo half of Roots64Split (guarded)
+    y.roots = y.roots64 + (guard ? align16((size_t)L * 8) : 0);
     return y;
 }
 
@@ -526,25 +539,35 @@ __device__ __forceinline__ void hash16_insert(unsigned short *hash, int H, int k
 }
 
 // LC / DC: compile-time line length and dimensionality (0 = runtime), so the
-// benchmark shapes get fully unrolled gathers, FFTs and bin loops.
-template <class R, int LC, int DC>
+// benchmark shapes get fully unrolled gathers, FFTs and bin loops.  GUARD
+// (float32, compile-time shapes): the float64 reference's decisions
+// (fpssft_guard.cuh) -- float64 slot amplitudes and line-0 transform, guard
+// flags on every float32 decision statistic, flagged bins re-evaluated in
+// float64 by the whole warp.
+template <class R, int LC, int DC, bool GUARD = false>
 __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp_kernel(const float2 *__restrict__ cubes,
                                                            long long batch, long long batch_stride,
                                                            Geo g_in, Knobs kn,
                                                            const int *__restrict__ schedule,
                                                            const int *__restrict__ sched_index,
                                                            int n_sched, OutPtrs out) {
+    static_assert(!GUARD || (sizeof(R) == 4 && LC != 0 && DC != 0),
+                  "guarded mode: float32 with a compile-time shape");
     extern __shared__ __align__(16) unsigned char sm[];
     constexpr bool PAD = LC != 0;  // padded spectra layout (see padi)
+    using A = typename std::conditional<GUARD, double, R>::type;  // slot amplitude type
     Geo g = g_in;
     if (LC) g.L = LC;
     if (DC) {
         g.D = DC;
         g.nlines = DC + 1;
     }
-    const WarpLayout lay = make_warp_layout(g.D, g.L, kn.k_cap, (int)sizeof(cpx<R>));
+    const WarpLayout lay = make_warp_layout(g.D, g.L, kn.k_cap, (int)sizeof(cpx<R>), GUARD);
     cpx<R> *roots = (cpx<R> *)sm;
+    [[maybe_unused]] cpx<float> *roots_lo = (cpx<float> *)(sm + lay.roots64);
+    [[maybe_unused]] const Roots64Split roots64{(const cpx<float> *)roots, roots_lo};
     build_roots(roots, g.L);
+    if constexpr (GUARD) build_roots_lo(roots_lo, g.L);
     __syncthreads();  // the only block-wide barrier: warps run independently below
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -552,13 +575,15 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     if (inst >= batch) return;
     unsigned char *base = sm + lay.roots + (size_t)warp * lay.per_warp;
     cpx<R> *spec = (cpx<R> *)(base + lay.spec);
-    cpx<R> *slot_amp = (cpx<R> *)(base + lay.slot_amp);
+    cpx<A> *slot_amp = (cpx<A> *)(base + lay.slot_amp);
     int *slot_key = (int *)(base + lay.slot_key);
     unsigned short *hash = (unsigned short *)(base + lay.hash);
     unsigned char *slot_live = base + lay.slot_live;
     unsigned short *cand = (unsigned short *)(base + lay.cand);
     int *scr_u = (int *)(base + lay.scr_u);
-    cpx<R> *scr_amp = (cpx<R> *)(base + lay.scr_amp);
+    cpx<A> *scr_amp = (cpx<A> *)(base + lay.scr_amp);
+    [[maybe_unused]] cpx<double> *x0d = (cpx<double> *)(base + lay.x0d);
+    [[maybe_unused]] float *pabs = (float *)(base + lay.pabs);
 
     const int L = g.L, D = g.D, nl = g.nlines, H = lay.H;
     const float2 *cube = cube_base(cubes, (long long)inst, batch_stride, kn.group);
@@ -567,7 +592,6 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     if (!sched_ok) sidx = 0;
     const int *sched = schedule + (long long)sidx * kn.t_max * 2 * D;
     const R mag_tol = (R)kn.mag_tol, round_tol = (R)kn.round_tol, verify_tol = (R)kn.verify_tol;
-    const R prune = (R)kn.amp_prune_tol;
     const unsigned lt_mask = (1u << lane) - 1u;
 
     for (int h = lane; h < H; h += 32) hash[h] = HASH_EMPTY;
@@ -575,7 +599,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
 
     int n_slots = 0, stall = 0, it_run = 0;
     int term = sched_ok ? FPSSFT_TERM_MAX_ITERATIONS : -1;
-    R amp_sum = (R)0;
+    A amp_sum = (A)0;
 
     // the schedule is data-independent: iteration t+1's (alpha, tau) load
     // while iteration t runs
@@ -631,11 +655,23 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
                     line_params_ok(g, nal, nta))
                     prefetch_lines_l2<LC>(cube, g, nal, nta, lane);
             }
+            if constexpr (GUARD)
+                for (int b = lane; b < L; b += 32) pabs[b] = 0.f;
             cp_async_wait_all();
             __syncwarp();
             if constexpr (LC != 0 && stage16_ok(DC, LC, 8, 32)) {
                 if (staged) {
-                    compact_stage16<LC, DC + 1, 32, WarpTeam>(spec, par, dup, lane);
+                    compact_stage16<LC, DC + 1, 32, WarpTeam>(spec, par, dup, lane,
+                                                              GUARD ? x0d : nullptr);
+                    __syncwarp();
+                }
+            }
+            if constexpr (GUARD) {
+                if (!staged) {  // line 0's samples into the float64 buffer
+                    for (int l = lane; l < L; l += 32) {
+                        const cpx<R> v = spec[padi<PAD>(l)];
+                        x0d[padi<PAD>(l)] = {(double)v.re, (double)v.im};
+                    }
                     __syncwarp();
                 }
             }
@@ -654,15 +690,22 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         if constexpr (LC != 0) {
             const R e = fft_static<R, LC, DC + 1>(spec, roots, lane);
             if (sizeof(R) == 4) my_energy = e;
+            if constexpr (GUARD) fft_static<double, LC, 1, 32, WarpTeam, Roots64Split>(x0d, roots64, lane);
         } else
             fft_lines_warp<R>(spec, nl, g, roots, lane);
         R noise_floor = (R)0;
-        if (sizeof(R) == 4 && kn.noise_coef > 0)
+        [[maybe_unused]] float Ef = 0.f;  // GUARD: transform part of the error bound
+        if constexpr (GUARD) {
+            Ef = (float)(kn.guard_coef *
+                         sqrt((double)__shfl_sync(FULL, warp_sum(my_energy), 0)));
+        } else if (sizeof(R) == 4 && kn.noise_coef > 0) {
             noise_floor = (R)kn.noise_coef * sqrt(__shfl_sync(FULL, warp_sum(my_energy), 0));
+        }
 
         // (3) construction-subtraction, 32 slots at a time in slot order;
         //     each lane stages its slot's phase on every line, slots sharing
-        //     a bin are summed by their lowest lane in lane (= slot) order
+        //     a bin are summed by their lowest lane in lane (= slot) order.
+        //     GUARD: also the float64 line-0 projection and the bins' sum |a|
         for (int c0 = 0; c0 < n_slots; c0 += 32) {
             const int s = c0 + lane;
             const bool valid = s < n_slots && slot_live[s];
@@ -681,50 +724,128 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             const unsigned grp = __match_any_sync(FULL, b);
             if (valid && lane == __ffs(grp) - 1) {
                 cpx<R> P[MAXD + 1];
+                [[maybe_unused]] cpx<double> P0 = {0.0, 0.0};
+                [[maybe_unused]] float pa = 0.f;
 #pragma unroll
                 for (int i = 0; i < MAXD + 1; ++i) P[i] = {(R)0, (R)0};
                 for (unsigned rest = grp; rest; rest &= rest - 1) {
                     const int j = __ffs(rest) - 1;
-                    const cpx<R> aj = scr_amp[j];
+                    const cpx<A> aj = scr_amp[j];
+                    const cpx<R> ar = {(R)aj.re, (R)aj.im};
 #pragma unroll
                     for (int i = 0; i < MAXD + 1; ++i)
-                        if (i < nl) P[i] = P[i] + aj * roots[scr_u[i * 32 + j]];
+                        if (i < nl) P[i] = P[i] + ar * roots[scr_u[i * 32 + j]];
+                    if constexpr (GUARD) {
+                        P0 = P0 + cpx<double>{(double)aj.re, (double)aj.im} * roots64[scr_u[j]];
+                        pa += cabs(ar);
+                    }
                 }
 #pragma unroll
                 for (int i = 0; i < MAXD + 1; ++i)
                     if (i < nl) spec[padi<PAD>(i * L + b)] = spec[padi<PAD>(i * L + b)] - P[i];
+                if constexpr (GUARD) {
+                    x0d[padi<PAD>(b)] = x0d[padi<PAD>(b)] - P0;
+                    pabs[b] += pa;
+                }
             }
             __syncwarp();
         }
 
         // (4) classify + (5) merge, 32 bins at a time in ascending order
-        const R floor =
-            max(max((R)kn.energy_floor_abs, (R)kn.energy_floor * amp_sum), noise_floor);
+        const A floor_a = max(max((A)kn.energy_floor_abs, (A)kn.energy_floor * amp_sum),
+                              (A)noise_floor);
+        const R floor = (R)floor_a;
         // 1-sparse magnitude test on every bin, candidates compacted in
         // ascending order so the decode runs on dense batches of 32.  The
         // termination residual (max |S|) is folded in: non-candidate bins keep
         // their values, candidates are re-read after the merge below.
+        // GUARD: bins inside the guard band join the list, flagged.
         int n_cand = 0, n_acc = 0;
         R resid = (R)0;
         for (int c0 = 0; c0 < L; c0 += 32) {
             const int b = c0 + lane;
             R top = (R)0;
-            const bool ok = b < L && bin_is_candidate<R, PAD>(spec, g, b, mag_tol, floor, &top);
-            if (!ok) resid = max(resid, top);
-            const unsigned msk = __ballot_sync(FULL, ok);
-            if (ok) cand[n_cand + __popc(msk & lt_mask)] = (unsigned short)b;
+            bool ok = false, fl = false;
+            if (b < L) {
+                if constexpr (GUARD)
+                    ok = bin_is_candidate_guarded<PAD>((const cpx<float> *)spec, g, b,
+                                                       (float)mag_tol, (float)floor,
+                                                       Ef + GUARD_KP * pabs[b], (float *)&top, &fl);
+                else
+                    ok = bin_is_candidate<R, PAD>(spec, g, b, mag_tol, floor, &top);
+            }
+            if (!ok && !fl) resid = max(resid, top);
+            const unsigned msk = __ballot_sync(FULL, ok || fl);
+            if (ok || fl)
+                cand[n_cand + __popc(msk & lt_mask)] =
+                    (unsigned short)b | (unsigned short)(fl ? CAND_FLAG : 0);
             n_cand += __popc(msk);
         }
         __syncwarp();
         bool overflow = false;
+        int n_cand_x = 0;
         for (int c0 = 0; c0 < n_cand; c0 += 32) {
-            const int b = c0 + lane < n_cand ? cand[c0 + lane] : -1;
+            const int ce = c0 + lane < n_cand ? cand[c0 + lane] : -1;
+            const int b = ce >= 0 ? (ce & ~(int)CAND_FLAG) : -1;
             int m[MAXD];
             cpx<R> a;
             int st = 0;
-            if (b >= 0)
-                st = decode_candidate<R, PAD>(spec, g, b, al, ta, roots, round_tol, verify_tol, m, &a);
+            if constexpr (GUARD) {
+                const bool mflag = ce >= 0 && ((ce & CAND_FLAG) || FPSSFT_GUARD_CALIB == 1);
+                if (b >= 0 && !mflag)
+                    st = decode_candidate_guarded<PAD>((const cpx<float> *)spec, g, b, al, ta,
+                                                       (const cpx<float> *)roots,
+                                                       (float)round_tol, (float)verify_tol,
+                                                       Ef + GUARD_KP * pabs[b], m);
+                const unsigned need = __ballot_sync(FULL, b >= 0 && (mflag || st == ST_FLAG));
+#if FPSSFT_GUARD_CALIB == 2
+                if (lane == 0 && need) atomicAdd(&g_guard_calib_count, (unsigned long long)__popc(need));
+#endif
+                // exact float64 re-evaluation of the flagged bins, one at a
+                // time by the whole warp
+                for (unsigned rest = need; rest; rest &= rest - 1) {
+                    const int owner = __ffs(rest) - 1;
+                    const int bf = __shfl_sync(FULL, b, owner);
+                    cpx<double> dft[MAXD], prj[MAXD];
+                    exact_bin_partials<A>(bf, cube, g, al, ta, roots64, n_slots, slot_key,
+                                          slot_live, slot_amp, lane, 32, dft, prj);
+                    cpx<double> S[MAXD + 1];
+                    S[0] = x0d[padi<PAD>(bf)];
+#pragma unroll
+                    for (int i = 0; i < MAXD; ++i)
+                        if (i < D)
+                            S[i + 1] = {warp_sum(dft[i].re) / (double)L - warp_sum(prj[i].re),
+                                        warp_sum(dft[i].im) / (double)L - warp_sum(prj[i].im)};
+                    int mx[MAXD];
+                    cpx<double> ax;
+                    // every lane holds the same sums: each decides, the owner keeps it
+                    const int sx = classify_values<double, Roots64Split>(S, g, bf, al, ta, roots64, kn.mag_tol,
+                                                           kn.round_tol, kn.verify_tol,
+                                                           (double)floor_a, mx, &ax);
+                    if (lane == owner) {
+                        st = sx;
+#pragma unroll
+                        for (int k = 0; k < MAXD; ++k) m[k] = mx[k];
+#if FPSSFT_GUARD_CALIB == 1
+                        const double unit = (double)Ef / GUARD_KF + U32 * pabs[bf];
+                        double worst = 0.0;
+                        for (int i = 0; i <= D; ++i) {
+                            const cpx<R> v = spec[padi<PAD>(i * L + bf)];
+                            worst = fmax(worst, hypot((double)v.re - S[i].re,
+                                                      (double)v.im - S[i].im));
+                        }
+                        atomicMax(&g_guard_calib_max, __float_as_uint((float)(worst / unit)));
+                        atomicAdd(&g_guard_calib_count, 1ull);
+#endif
+                    }
+                }
+            } else {
+                if (b >= 0)
+                    st = decode_candidate<R, PAD>(spec, g, b, al, ta, roots, round_tol,
+                                                  verify_tol, m, &a);
+            }
             const unsigned acc = __ballot_sync(FULL, st == 2);
+            if constexpr (GUARD) n_cand_x += __popc(__ballot_sync(FULL, st >= 1));
             int key = 0, found = -1;
             if (st == 2) {
                 key = pack_key(m, g);
@@ -737,7 +858,14 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             }
             n_acc += __popc(acc);
             if (st == 2) {
-                cpx<R> v = a;
+                cpx<A> av;
+                if constexpr (GUARD) {  // the float64 amplitude (decoder.py:160)
+                    av = mulc(x0d[padi<PAD>(b)], roots64[phase_of(m, g, ta)]);
+                    a = {(R)av.re, (R)av.im};
+                } else {
+                    av = a;
+                }
+                cpx<A> v = av;
                 int s;
                 if (found < 0) {
                     s = n_slots + __popc(fresh & lt_mask);
@@ -745,10 +873,10 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
                     hash16_insert(hash, H, key, s);
                 } else {
                     s = found;
-                    v = slot_amp[s] + a;  // a pruned slot holds 0: entries.get(f, 0) + a
+                    v = slot_amp[s] + av;  // a pruned slot holds 0: entries.get(f, 0) + a
                 }
-                const bool keep = !(cabs(v) <= prune);
-                slot_amp[s] = keep ? v : cpx<R>{(R)0, (R)0};
+                const bool keep = !(cabs(v) <= (A)kn.amp_prune_tol);
+                slot_amp[s] = keep ? v : cpx<A>{(A)0, (A)0};
                 slot_live[s] = keep;
                 const int u0 = phase_of(m, g, ta);  // driver.py:189-194
                 for (int i = 0; i < nl; ++i)
@@ -759,6 +887,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             n_slots += __popc(fresh);
             __syncwarp();
         }
+        if constexpr (GUARD) n_cand = n_cand_x;
         if (overflow) {
             term = FPSSFT_TERM_K_CAP_OVERFLOW;
             if (lane == 0 && out.iter_stats) {
@@ -772,14 +901,14 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         __syncwarp();
 
         // (6) amp_sum = sum |a| over the recovered set        driver.py:108
-        R my = (R)0;
+        A my = (A)0;
         for (int s = lane; s < n_slots; s += 32)
             if (slot_live[s]) my += cabs(slot_amp[s]);
         amp_sum = __shfl_sync(FULL, warp_sum(my), 0);
         stall = n_acc > 0 ? 0 : stall + 1;
 
         // (7) termination                                     driver.py:196-204
-        const R clean = max((R)kn.energy_floor_abs, (R)kn.residual_stop * amp_sum);
+        const R clean = (R)max((A)kn.energy_floor_abs, (A)kn.residual_stop * amp_sum);
         const R worst = warp_max(resid);  // |S|^2 (float) or |S| (double)
         const bool is_clean = sizeof(R) == 8 ? worst <= clean : worst <= clean * clean;
         if (lane == 0 && out.iter_stats) {
@@ -1460,8 +1589,9 @@ int make_knobs(const fpssft_params *p, Knobs *k) {
                            "energy_floor", "energy_floor_abs", "residual_stop"};
     for (int i = 0; i < 7; ++i)
         if (!(v[i] > 0)) return fail(FPSSFT_EINVAL, std::string(names[i]) + " must be positive");
-    if (p->precision != FPSSFT_F32 && p->precision != FPSSFT_F64)
-        return fail(FPSSFT_EINVAL, "precision must be FPSSFT_F32 or FPSSFT_F64");
+    if (p->precision != FPSSFT_F32 && p->precision != FPSSFT_F64 &&
+        p->precision != FPSSFT_F32_GUARDED)
+        return fail(FPSSFT_EINVAL, "precision must be FPSSFT_F32, FPSSFT_F64 or FPSSFT_F32_GUARDED");
     if (p->mode < FPSSFT_MODE_AUTO || p->mode > FPSSFT_MODE_WARP)
         return fail(FPSSFT_EINVAL, "mode must be FPSSFT_MODE_AUTO, _CTA or _WARP");
     k->mag_tol = p->mag_tol;
@@ -1472,6 +1602,7 @@ int make_knobs(const fpssft_params *p, Knobs *k) {
     k->energy_floor_abs = p->energy_floor_abs;
     k->residual_stop = p->residual_stop;
     k->noise_coef = 0.0;
+    k->guard_coef = 0.0;
     k->t_max = p->t_max;
     k->stall_limit = p->stall_limit;
     k->k_cap = p->k_cap;
@@ -1483,12 +1614,14 @@ int make_knobs(const fpssft_params *p, Knobs *k) {
 // transform's per-bin error is ~ eps sqrt(log2 L + 1) ||x_line|| / L; bins
 // below kappa times that are treated as empty.  Zero in float64 mode, where
 // the reference's own floors are far above the rounding level.
+// Guarded float32 (fpssft_guard.cuh): no rounding floor (the guard band
+// re-evaluates what float32 cannot resolve); the transform part of the error
+// bound is guard_coef * sqrt(sum |x|^2 over the D+1 lines).
 void set_noise_floor(Knobs *k, const Geo &g, int precision) {
     const double kappa = 8.0, eps32 = 5.9604644775390625e-08;
-    k->noise_coef = precision == FPSSFT_F64
-                        ? 0.0
-                        : kappa * eps32 * std::sqrt(std::log2((double)g.L) + 1.0) /
-                              ((double)g.L * std::sqrt((double)g.nlines));
+    const double unit = eps32 * std::sqrt(std::log2((double)g.L) + 1.0) / (double)g.L;
+    k->noise_coef = precision == FPSSFT_F32 ? kappa * unit / std::sqrt((double)g.nlines) : 0.0;
+    k->guard_coef = precision == FPSSFT_F32_GUARDED ? GUARD_KF * unit : 0.0;
 }
 
 int check_launch(const char *where) {
@@ -1507,6 +1640,10 @@ const void *warp_kernel_for_t(const Geo &g) {
     return (const void *)recover_warp_kernel<R, 0, 0>;
 }
 const void *warp_kernel_for(const Geo &g, int precision) {
+    if (precision == FPSSFT_F32_GUARDED)  // guarded float32: the noisy config-3 shape
+        return g.off32 && g.D == 3 && g.L == 64
+                   ? (const void *)recover_warp_kernel<float, 64, 3, true>
+                   : nullptr;
     return precision == FPSSFT_F64 ? warp_kernel_for_t<double>(g) : warp_kernel_for_t<float>(g);
 }
 
@@ -1532,7 +1669,22 @@ const void *team_kernel_for_t(const Geo &g, int *nt) {
     }
     return nullptr;
 }
+// Guarded float32 team kernels (fpssft_guard.cuh): the shapes of the noisy
+// configs (3: 64^3, 5: 512 x 512).
+const void *team_guard_kernel_for(const Geo &g, int *nt) {
+    if (!g.off32) return nullptr;
+    if (g.D == 2 && g.L == 512) {
+        *nt = 128;
+        return (const void *)recover_team_kernel<float, 512, 2, 128, true>;
+    }
+    if (g.D == 3 && g.L == 64) {
+        *nt = 128;
+        return (const void *)recover_team_kernel<float, 64, 3, 128, true>;
+    }
+    return nullptr;
+}
 const void *team_kernel_for(const Geo &g, int precision, int *nt) {
+    if (precision == FPSSFT_F32_GUARDED) return team_guard_kernel_for(g, nt);
     return precision == FPSSFT_F64 ? team_kernel_for_t<double>(g, nt)
                                    : team_kernel_for_t<float>(g, nt);
 }
@@ -1572,15 +1724,17 @@ int warp_kernel_regs(const Geo &g, int precision) {
 
 int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) {
     const int cs = precision == FPSSFT_F64 ? 16 : 8;
+    const bool guard = precision == FPSSFT_F32_GUARDED;
     // candidate 1: warp per instance
     long long warp_warps = 0;
     LaunchPlan wp{};
     Geo gw = g;
     if (want != FPSSFT_MODE_CTA) {
         bool ok = g.key_bits_ <= 31 && kn.k_cap <= 32768 && (long long)g.nlines * g.L <= 2048 &&
-                  (g.L & (g.L - 1)) == 0 && plan_fft(&gw, g.nlines, precision, 32) > 0;
+                  (g.L & (g.L - 1)) == 0 && plan_fft(&gw, g.nlines, precision, 32) > 0 &&
+                  (!guard || warp_kernel_for(g, precision) != nullptr);
         if (ok) {
-            const WarpLayout wl = make_warp_layout(g.D, g.L, kn.k_cap, cs);
+            const WarpLayout wl = make_warp_layout(g.D, g.L, kn.k_cap, cs, guard);
             const int regs = (warp_kernel_regs(gw, precision) + 7) / 8 * 8;
             const long long reg_warps = 65536 / (regs * 32);
             int best_w = 0;
@@ -1623,7 +1777,7 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
             int tnt = req;
             const void *tk = team_kernel_for(g, precision, &tnt);
             if (!tk || (req && tnt != req)) continue;
-            const TeamLayout tl = make_team_layout(g.D, g.L, kn.k_cap, cs, tnt);
+            const TeamLayout tl = make_team_layout(g.D, g.L, kn.k_cap, cs, tnt, guard);
             if ((long long)tl.total > SMEM_PER_CTA) continue;
             const int regs = (kernel_regs(tk, tnt >= 1024 ? 64 : 128) + 7) / 8 * 8;
             const long long ctas = std::min<long long>(
@@ -1649,6 +1803,8 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
         *lp = tp;
         return FPSSFT_OK;
     }
+    if (guard)  // no guarded kernel for this shape: the caller runs float64
+        return fail(FPSSFT_EUNSUPPORTED, "no guarded float32 kernel for this shape");
     const int nt = plan_fft(&g, g.nlines, precision, 0);
     if (nt < 0) return fail(FPSSFT_EUNSUPPORTED, "line length too large for one CTA");
     const Layout lay = make_layout(g.D, g.L, kn.k_cap, cs);
@@ -1681,12 +1837,23 @@ void set_carveout(const void *kernel, long long grid, int threads, size_t smem) 
     cudaGetLastError();  // a hint: never an error
 }
 
+// The arithmetic a launch really uses: FPSSFT_F32_GUARDED falls back to the
+// float64 kernels (exact decisions too) for shapes without a guarded kernel.
+int effective_precision(const Geo &g, const Knobs &kn, int precision, int mode) {
+    if (precision != FPSSFT_F32_GUARDED) return precision;
+    Geo gg = g;
+    LaunchPlan lp;
+    if (make_plan(gg, kn, precision, mode, &lp) == FPSSFT_OK) return precision;
+    return FPSSFT_F64;
+}
+
 template <class R>
 int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
                 const Knobs &kn, int want_mode, const int32_t *schedule,
                 const int32_t *sched_index, int32_t n_sched, const OutPtrs &o, cudaStream_t st) {
     LaunchPlan lp;
-    const int prec = sizeof(R) == 8 ? FPSSFT_F64 : FPSSFT_F32;
+    const int prec = sizeof(R) == 8 ? FPSSFT_F64
+                                    : (kn.guard_coef > 0 ? FPSSFT_F32_GUARDED : FPSSFT_F32);
     int rc = make_plan(g, kn, prec, want_mode, &lp);
     if (rc != FPSSFT_OK) return rc;
     cudaError_t e;
@@ -1742,6 +1909,25 @@ const char *fpssft_last_error(void) { return g_err.c_str(); }
 int fpssft_abi_version(void) { return 1; }
 int fpssft_launches_per_batch(void) { return 1; }
 
+#if FPSSFT_GUARD_CALIB
+// Calibration builds only: the largest float32 bin-value error seen against
+// the exact values, in units of the kappa = 1 guard bound, and how many bins
+// were measured; resets both.
+int fpssft_guard_calib(float *max_ratio, unsigned long long *count) {
+    unsigned int m = 0;
+    unsigned long long c = 0;
+    cudaMemcpyFromSymbol(&m, g_guard_calib_max, sizeof m);
+    cudaMemcpyFromSymbol(&c, g_guard_calib_count, sizeof c);
+    unsigned int z = 0;
+    unsigned long long zc = 0;
+    cudaMemcpyToSymbol(g_guard_calib_max, &z, sizeof z);
+    cudaMemcpyToSymbol(g_guard_calib_count, &zc, sizeof zc);
+    std::memcpy(max_ratio, &m, sizeof m);
+    *count = c;
+    return FPSSFT_OK;
+}
+#endif
+
 int fpssft_set_l2_fetch_granularity(int32_t bytes) {
     if (bytes < 0 || bytes > 128 || (bytes & (bytes - 1)))
         return fail(FPSSFT_EINVAL, "L2 fetch granularity must be 0 or a power of two <= 128");
@@ -1790,7 +1976,8 @@ int fpssft_run_batch_grouped(const void *cubes, int64_t batch, int32_t group,
     if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
     if (group < 1 || group > 64) return fail(FPSSFT_EINVAL, "group must be in [1, 64]");
     kn.group = group;
-    set_noise_floor(&kn, g, params->precision);
+    const int prec = effective_precision(g, kn, params->precision, params->mode);
+    set_noise_floor(&kn, g, prec);
     if (batch < 0) return fail(FPSSFT_EINVAL, "batch must be >= 0");
     if (batch > INT_MAX) return fail(FPSSFT_EINVAL, "batch exceeds the grid limit");
     if (batch > 0 && (!cubes || !schedule || !out || !out->freqs || !out->amps || !out->count ||
@@ -1805,7 +1992,7 @@ int fpssft_run_batch_grouped(const void *cubes, int64_t batch, int32_t group,
               out ? out->terminated_by : nullptr,
               out ? out->iter_stats : nullptr};
     cudaStream_t st = (cudaStream_t)stream;
-    if (params->precision == FPSSFT_F64)
+    if (prec == FPSSFT_F64)
         return run_batch_t<double>(cubes, batch, batch_stride, g, kn, params->mode, schedule,
                                    sched_index, n_sched, o, st);
     return run_batch_t<float>(cubes, batch, batch_stride, g, kn, params->mode, schedule,
@@ -1913,7 +2100,8 @@ int fpssft_plan(const fpssft_shape *shape, const fpssft_params *params, int32_t 
     if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
     if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
     LaunchPlan lp;
-    if ((rc = make_plan(g, kn, params->precision, params->mode, &lp)) != FPSSFT_OK) return rc;
+    const int prec = effective_precision(g, kn, params->precision, params->mode);
+    if ((rc = make_plan(g, kn, prec, params->mode, &lp)) != FPSSFT_OK) return rc;
     if (mode) *mode = lp.mode;
     if (threads_per_cta) *threads_per_cta = lp.threads;
     if (instances_per_cta) *instances_per_cta = lp.per_cta;

@@ -97,6 +97,7 @@ struct Knobs {
     double mag_tol, verify_tol, round_tol, amp_prune_tol;
     double energy_floor, energy_floor_abs, residual_stop;
     double noise_coef;  // float32 rounding floor: coef * sqrt(sum |x|^2 over the D+1 lines)
+    double guard_coef;  // guarded float32: transform error bound coef * sqrt(sum |x|^2)
     int t_max, stall_limit, k_cap;
     int group;  // instances interleaved per sample (batch layout [B/group, *dims, group])
 };
@@ -184,6 +185,24 @@ __device__ __forceinline__ void build_roots(cpx<R> *roots, int L) {
         double s, c;
         sincospi(2.0 * (double)j / (double)L, &s, &c);
         roots[j] = {(R)c, (R)s};
+    }
+}
+
+// float64 roots as a float32 pair: hi = the float32 table (build_roots),
+// lo = float32(root - hi); hi + lo carries ~2^-49 relative error, against
+// 2^-53 for a float64 table, at half its shared memory.
+struct Roots64Split {
+    const cpx<float> *hi, *lo;
+    __device__ __forceinline__ cpx<double> operator[](int j) const {
+        const cpx<float> h = hi[j], l = lo[j];
+        return {(double)h.re + (double)l.re, (double)h.im + (double)l.im};
+    }
+};
+__device__ __forceinline__ void build_roots_lo(cpx<float> *lo, int L) {
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+        double s, c;
+        sincospi(2.0 * (double)j / (double)L, &s, &c);
+        lo[j] = {(float)(c - (double)(float)c), (float)(s - (double)(float)s)};
     }
 }
 
@@ -483,7 +502,7 @@ __device__ __forceinline__ unsigned gather_lines_cg16(float4 *stage, const float
 // samples flagged in dup are carried in registers from the line-0 batch.
 template <int LC, int NL, int NTC, class Team>
 __device__ __forceinline__ void compact_stage16(cpx<float> *spec, unsigned par, unsigned dup,
-                                                int tid) {
+                                                int tid, cpx<double> *x0d = nullptr) {
     constexpr int J = LC / NTC;
     const float4 *stage = (const float4 *)spec;
     float2 hold[J];
@@ -504,6 +523,9 @@ __device__ __forceinline__ void compact_stage16(cpx<float> *spec, unsigned par, 
         Team::sync();
 #pragma unroll
         for (int j = 0; j < J; ++j) spec[padi<true>(NTC * (i * J + j) + tid)] = {v[j].x, v[j].y};
+        if (i == 0 && x0d != nullptr)  // guarded mode: line 0 also in float64
+#pragma unroll
+            for (int j = 0; j < J; ++j) x0d[padi<true>(NTC * j + tid)] = {(double)v[j].x, (double)v[j].y};
     }
 }
 // L2 prefetch of a future iteration's line samples (compile-time line
@@ -819,8 +841,9 @@ struct StageCap {  // butterflies per thread that fit the register budget
     static constexpr int value = RAD == 16 ? 1 : (RAD == 8 ? 2 : 4);
 };
 
-template <class R, int L, int NL, int RAD, int NS, bool LAST, int NT, class Team>
-__device__ __forceinline__ R stage_static(cpx<R> *x, const cpx<R> *roots, int tid) {
+template <class R, int L, int NL, int RAD, int NS, bool LAST, int NT, class Team,
+          class RT = const cpx<R> *>
+__device__ __forceinline__ R stage_static(cpx<R> *x, RT roots, int tid) {
     constexpr int M = L / RAD;                                   // butterflies per line
     constexpr int CAPB = StageCap<R, RAD>::value;
     constexpr int G0 = CAPB * NT / M;
@@ -855,7 +878,7 @@ __device__ __forceinline__ R stage_static(cpx<R> *x, const cpx<R> *roots, int ti
                 } else {
                     ob[j] = line * L + jj * RAD;
                 }
-                Bfly<R, RAD>::run(v[j], roots, L);
+                Bfly<R, RAD>::run(v[j], (const cpx<R> *)nullptr, L);  // radix 4/8/16: no table
             }
         }
         Team::sync();
@@ -881,33 +904,34 @@ struct HasStaticPlan {
 };
 
 // Returns this thread's share of sum |x|^2 of the input samples.
-template <class R, int L, int NL, int NT = 32, class Team = WarpTeam>
-__device__ __forceinline__ R fft_static(cpx<R> *x, const cpx<R> *roots, int tid) {
+template <class R, int L, int NL, int NT = 32, class Team = WarpTeam,
+          class RT = const cpx<R> *>
+__device__ __forceinline__ R fft_static(cpx<R> *x, RT roots, int tid) {
     constexpr bool F = sizeof(R) == 4;
     R e;
     if constexpr (L == 256 && F && FPSSFT_R16_256) {
-        e = stage_static<R, L, NL, 16, 1, false, NT, Team>(x, roots, tid);
-        stage_static<R, L, NL, 16, 16, true, NT, Team>(x, roots, tid);
+        e = stage_static<R, L, NL, 16, 1, false, NT, Team, RT>(x, roots, tid);
+        stage_static<R, L, NL, 16, 16, true, NT, Team, RT>(x, roots, tid);
     } else if constexpr (L == 256) {
-        e = stage_static<R, L, NL, 8, 1, false, NT, Team>(x, roots, tid);
-        stage_static<R, L, NL, 8, 8, false, NT, Team>(x, roots, tid);
-        stage_static<R, L, NL, 4, 64, true, NT, Team>(x, roots, tid);
+        e = stage_static<R, L, NL, 8, 1, false, NT, Team, RT>(x, roots, tid);
+        stage_static<R, L, NL, 8, 8, false, NT, Team, RT>(x, roots, tid);
+        stage_static<R, L, NL, 4, 64, true, NT, Team, RT>(x, roots, tid);
     } else if constexpr (L == 512) {
-        e = stage_static<R, L, NL, 8, 1, false, NT, Team>(x, roots, tid);
-        stage_static<R, L, NL, 8, 8, false, NT, Team>(x, roots, tid);
-        stage_static<R, L, NL, 8, 64, true, NT, Team>(x, roots, tid);
+        e = stage_static<R, L, NL, 8, 1, false, NT, Team, RT>(x, roots, tid);
+        stage_static<R, L, NL, 8, 8, false, NT, Team, RT>(x, roots, tid);
+        stage_static<R, L, NL, 8, 64, true, NT, Team, RT>(x, roots, tid);
     } else if constexpr (L == 64) {
-        e = stage_static<R, L, NL, 8, 1, false, NT, Team>(x, roots, tid);
-        stage_static<R, L, NL, 8, 8, true, NT, Team>(x, roots, tid);
+        e = stage_static<R, L, NL, 8, 1, false, NT, Team, RT>(x, roots, tid);
+        stage_static<R, L, NL, 8, 8, true, NT, Team, RT>(x, roots, tid);
     } else if constexpr (L == 2048 && F) {
-        e = stage_static<R, L, NL, 16, 1, false, NT, Team>(x, roots, tid);
-        stage_static<R, L, NL, 16, 16, false, NT, Team>(x, roots, tid);
-        stage_static<R, L, NL, 8, 256, true, NT, Team>(x, roots, tid);
+        e = stage_static<R, L, NL, 16, 1, false, NT, Team, RT>(x, roots, tid);
+        stage_static<R, L, NL, 16, 16, false, NT, Team, RT>(x, roots, tid);
+        stage_static<R, L, NL, 8, 256, true, NT, Team, RT>(x, roots, tid);
     } else if constexpr (L == 2048) {
-        e = stage_static<R, L, NL, 8, 1, false, NT, Team>(x, roots, tid);
-        stage_static<R, L, NL, 8, 8, false, NT, Team>(x, roots, tid);
-        stage_static<R, L, NL, 8, 64, false, NT, Team>(x, roots, tid);
-        stage_static<R, L, NL, 4, 512, true, NT, Team>(x, roots, tid);
+        e = stage_static<R, L, NL, 8, 1, false, NT, Team, RT>(x, roots, tid);
+        stage_static<R, L, NL, 8, 8, false, NT, Team, RT>(x, roots, tid);
+        stage_static<R, L, NL, 8, 64, false, NT, Team, RT>(x, roots, tid);
+        stage_static<R, L, NL, 4, 512, true, NT, Team, RT>(x, roots, tid);
     } else {
         static_assert(HasStaticPlan<L>::value, "no static plan for this L");
     }
@@ -998,26 +1022,20 @@ __device__ __forceinline__ R bin_residual(const cpx<R> *spec, const Geo &g, int 
 
 // ---------------------------------------------------------- classifier
 // decode_spectra for one bin b (decoder.py:127-169) with the driver's guard
-// (driver.py:166-176).  Returns 0 (not a candidate), 1 (candidate,
-// rejected), 2 (accepted), 3 (decoded and verified but guard failed).
-template <class R>
-__device__ __forceinline__ int classify_bin(const cpx<R> *spec, const Geo &g, int b,
-                                            const int *al, const int *ta, const cpx<R> *roots,
-                                            R mag_tol, R round_tol, R verify_tol, R floor,
-                                            int *m, cpx<R> *amp_out) {
-    const int L = g.L, D = g.D;
-    cpx<R> s[MAXD + 1];
+// (driver.py:166-176), on the bin's D+1 values s[0..D].  Returns 0 (not a
+// candidate), 1 (candidate, rejected), 2 (accepted), 3 (decoded and verified
+// but guard failed).  `roots` is any exact-phase table e^{+2 pi i j / L}.
+template <class R, class RT = const cpx<R> *>
+__device__ __forceinline__ int classify_values(const cpx<R> *s, const Geo &g, int b,
+                                               const int *al, const int *ta,
+                                               RT roots, R mag_tol, R round_tol,
+                                               R verify_tol, R floor, int *m, cpx<R> *amp_out) {
+    const int D = g.D;
     R mag[MAXD + 1];
-    R top, low;
 #pragma unroll
-    for (int i = 0; i < MAXD + 1; ++i) {
-        if (i <= D) {
-            s[i] = spec[i * L + b];
-            mag[i] = cabs(s[i]);
-        }
-    }
-    top = mag[0];
-    low = mag[0];
+    for (int i = 0; i < MAXD + 1; ++i)
+        if (i <= D) mag[i] = cabs(s[i]);
+    R top = mag[0], low = mag[0];
 #pragma unroll
     for (int i = 1; i < MAXD + 1; ++i) {
         if (i <= D) {
@@ -1055,6 +1073,18 @@ __device__ __forceinline__ int classify_bin(const cpx<R> *spec, const Geo &g, in
     *amp_out = amp;
     if (al != nullptr && bin_of(m, g, al) != b) return 3;
     return 2;
+}
+template <class R>
+__device__ __forceinline__ int classify_bin(const cpx<R> *spec, const Geo &g, int b,
+                                            const int *al, const int *ta, const cpx<R> *roots,
+                                            R mag_tol, R round_tol, R verify_tol, R floor,
+                                            int *m, cpx<R> *amp_out) {
+    cpx<R> s[MAXD + 1];
+#pragma unroll
+    for (int i = 0; i < MAXD + 1; ++i)
+        if (i <= g.D) s[i] = spec[i * g.L + b];
+    return classify_values(s, g, b, al, ta, roots, mag_tol, round_tol, verify_tol, floor, m,
+                           amp_out);
 }
 
 // As classify_bin for a bin already known to pass the magnitude test.

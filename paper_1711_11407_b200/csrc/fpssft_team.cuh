@@ -5,10 +5,14 @@
 // many warps resident (config 5: L = 512, k_cap = 1024): NT threads own one
 // instance and synchronise with block barriers.  Per iteration:
 //   cp.async gather -> compile-time FFT (padded layout) -> projection of the
-//   recovered set (counting sort by bin, 16-bit scratch) -> magnitude test on
-//   every bin with block-scan compaction of candidates -> dense decode of the
-//   candidates -> merge in candidate (= ascending bin) order -> residual and
-//   amp_sum reductions -> termination.
+//   recovered set (warp match_any groups, warps applied in order) -> magnitude
+//   test on every bin with block-scan compaction of candidates -> dense decode
+//   of the candidates -> merge in candidate (= ascending bin) order -> residual
+//   and amp_sum reductions -> termination.
+// GUARD (float32 only): the decisions of the float64 reference on the same
+// inputs (fpssft_guard.cuh) -- float64 slot amplitudes, a float64 transform
+// of line 0 (by the warp the register FFTs leave idle), guard-band flags on
+// every float32 decision statistic and exact re-evaluation of flagged bins.
 // Included by fpssft.cu after the warp kernel (shares its helpers).
 #pragma once
 // (included inside namespace fpssft)
@@ -19,22 +23,21 @@
 #define FPSSFT_TEAM_REGFFT 1  // 512-point lines: per-warp register FFTs (regfft::)
 #endif
 #ifndef FPSSFT_TEAM_PROJ_Q
-#define FPSSFT_TEAM_PROJ_Q 2  // projection sub-rounds per ordered apply (match_any path)
-#endif
-#ifndef FPSSFT_TEAM_PROJ
-#define FPSSFT_TEAM_PROJ 1  // projection: 1 = warp match_any + ordered apply, 0 = counting sort
+#define FPSSFT_TEAM_PROJ_Q 2  // projection sub-rounds per ordered apply
 #endif
 
 struct TeamLayout {
     size_t spec, roots, slot_amp, slot_key, hash, slot_live;
-    size_t bin_start, bin_fill, seg, slot_bin, slot_u0;  // projection scratch (union A)
-    size_t cand;                                         // classifier scratch (union B)
+    size_t x0d, roots64, pabs;                 // GUARD only
+    size_t proj, cand, res_st, res_key, flist;  // union: projection / classifier scratch
     size_t red, total;
     int H;
 };
 
-__host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, int cs, int nt) {
+__host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, int cs, int nt,
+                                                       bool guard = false) {
     TeamLayout y;
+    const int acs = guard ? 16 : cs;  // slot amplitude bytes (complex128 when guarded)
     size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // padi() layout
     if (stage16_ok(D, L, cs, nt) && spec_bytes < (size_t)(D + 1) * L * 16)
         spec_bytes = (size_t)(D + 1) * L * 16;  // 16-byte staging slots (gather_lines_cg16)
@@ -43,59 +46,73 @@ __host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, 
     y.H = 2 * k_cap;
     y.spec = o;      o = align16(o + (spec_bytes > sort_bytes ? spec_bytes : sort_bytes));
     y.roots = o;     o = align16(o + (size_t)L * cs);
-    y.slot_amp = o;  o = align16(o + (size_t)k_cap * cs);
+    y.slot_amp = o;  o = align16(o + (size_t)k_cap * acs);
     y.slot_key = o;  o = align16(o + (size_t)k_cap * 4);
     y.hash = o;      o = align16(o + (size_t)y.H * 2);
     y.slot_live = o; o = align16(o + (size_t)k_cap);
+    y.x0d = y.roots64 = y.pabs = o;
+    if (guard) {
+        y.x0d = o;     o = align16(o + (size_t)(L + L / 16 + 1) * 16);
+        y.roots64 = o; o = align16(o + (size_t)L * 8);  // lo half of Roots64Split
+        y.pabs = o;    o = align16(o + (size_t)L * 4);
+    }
+    // union: the projection's per-warp scratch (phases + amplitudes of 32
+    // slots) / the classifier's candidate list and the guard's per-round
+    // exact-evaluation results
     const size_t u = o;
-    y.bin_start = u; size_t a = align16(u + (size_t)(L + 1) * 2);
-    y.bin_fill = a;  a = align16(a + (size_t)L * 4);
-    y.seg = a;       a = align16(a + (size_t)k_cap * 2);
-    y.slot_bin = a;  a = align16(a + (size_t)k_cap * 2);
-    y.slot_u0 = a;   a = align16(a + (size_t)k_cap * 2);
+    y.proj = u;
+    const size_t a = align16(u + (size_t)(nt / 32) * 32 * ((MAXD + 1) * 4 + acs));
     y.cand = u;      size_t b = align16(u + (size_t)L * 2);
-    // the match_any projection's per-warp scratch also lives in this union
-    const size_t c = align16(u + (size_t)(nt / 32) * 32 * ((MAXD + 1) * 4 + cs));
-    o = b > c ? b : c;
-    if (!FPSSFT_TEAM_PROJ) o = o > a ? o : a;  // the counting-sort projection's scratch
-    y.red = o;       o = align16(o + 64 * 8);
+    y.res_st = b;    b = align16(b + (size_t)nt * 4);
+    y.res_key = b;   b = align16(b + (size_t)nt * 4);
+    y.flist = b;     b = align16(b + (size_t)nt * 2);
+    if (!guard) b = align16(u + (size_t)L * 2);
+    o = a > b ? a : b;
+    // reductions: 256 B of int scratch, then NW floats/doubles (and the
+    // guard's NW x 4 MAXD doubles of exact-evaluation partial sums)
+    const size_t dr = (size_t)(nt / 32) * 4 * MAXD * 8;
+    y.red = o;       o = align16(o + 256 + (guard && dr > 256 ? dr : 256));
     y.total = o;
     return y;
 }
 
 constexpr unsigned short U16_NONE = 0xFFFF;
 
-template <class R, int LC, int DC, int NT>
-__global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_team_kernel(const float2 *__restrict__ cubes,
-                                                             long long batch_stride, Geo g_in,
-                                                             Knobs kn,
-                                                             const int *__restrict__ schedule,
-                                                             const int *__restrict__ sched_index,
-                                                             int n_sched, OutPtrs out) {
+template <class R, int LC, int DC, int NT, bool GUARD = false>
+__global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
+                                            : (512 / NT > 1 ? 512 / NT : 1))
+    recover_team_kernel(const float2 *__restrict__ cubes, long long batch_stride, Geo g_in,
+                        Knobs kn, const int *__restrict__ schedule,
+                        const int *__restrict__ sched_index, int n_sched, OutPtrs out) {
+    static_assert(!GUARD || (sizeof(R) == 4 && NT <= 512), "guarded mode: float32, NT <= 512");
     extern __shared__ __align__(16) unsigned char sm[];
     constexpr bool PAD = true;
+    using A = typename std::conditional<GUARD, double, R>::type;  // slot amplitude type
     Geo g = g_in;
     g.L = LC;
     g.D = DC;
     g.nlines = DC + 1;
-    constexpr int L = LC, D = DC, nl = DC + 1;
-    const TeamLayout lay = make_team_layout(D, L, kn.k_cap, (int)sizeof(cpx<R>), NT);
+    constexpr int L = LC, D = DC, nl = DC + 1, NW = NT / 32;
+    const TeamLayout lay = make_team_layout(D, L, kn.k_cap, (int)sizeof(cpx<R>), NT, GUARD);
     cpx<R> *spec = (cpx<R> *)(sm + lay.spec);
     cpx<R> *roots = (cpx<R> *)(sm + lay.roots);
-    cpx<R> *slot_amp = (cpx<R> *)(sm + lay.slot_amp);
+    cpx<A> *slot_amp = (cpx<A> *)(sm + lay.slot_amp);
     int *slot_key = (int *)(sm + lay.slot_key);
     unsigned short *hash = (unsigned short *)(sm + lay.hash);
     unsigned char *slot_live = sm + lay.slot_live;
-    [[maybe_unused]] unsigned short *bin_start = (unsigned short *)(sm + lay.bin_start);
-    [[maybe_unused]] unsigned short *bin_fill = (unsigned short *)(sm + lay.bin_fill);
-    [[maybe_unused]] unsigned short *seg = (unsigned short *)(sm + lay.seg);
-    [[maybe_unused]] unsigned short *slot_bin = (unsigned short *)(sm + lay.slot_bin);
-    [[maybe_unused]] unsigned short *slot_u0 = (unsigned short *)(sm + lay.slot_u0);
+    [[maybe_unused]] cpx<double> *x0d = (cpx<double> *)(sm + lay.x0d);
+    [[maybe_unused]] cpx<float> *roots_lo = (cpx<float> *)(sm + lay.roots64);
+    [[maybe_unused]] const Roots64Split roots64{(const cpx<float> *)roots, roots_lo};
+    [[maybe_unused]] float *pabs = (float *)(sm + lay.pabs);
     unsigned short *cand = (unsigned short *)(sm + lay.cand);
+    [[maybe_unused]] int *res_st = (int *)(sm + lay.res_st);
+    [[maybe_unused]] int *res_key = (int *)(sm + lay.res_key);
+    [[maybe_unused]] unsigned short *flist = (unsigned short *)(sm + lay.flist);
     int *ired = (int *)(sm + lay.red);
     R *rred = (R *)(sm + lay.red + 256);
+    [[maybe_unused]] double *dred = (double *)(sm + lay.red + 256);
 
-    const int tid = threadIdx.x, H = lay.H;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, H = lay.H;
     const long long inst = blockIdx.x;
     const float2 *cube = cube_base(cubes, (long long)inst, batch_stride, kn.group);
     int sidx = sched_index ? sched_index[inst] : 0;
@@ -103,15 +120,15 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
     if (!sched_ok) sidx = 0;
     const int *sched = schedule + (long long)sidx * kn.t_max * 2 * D;
     const R mag_tol = (R)kn.mag_tol, round_tol = (R)kn.round_tol, verify_tol = (R)kn.verify_tol;
-    const R prune = (R)kn.amp_prune_tol;
 
     build_roots(roots, L);
+    if constexpr (GUARD) build_roots_lo(roots_lo, L);
     for (int h = tid; h < H; h += NT) hash[h] = U16_NONE;
     __syncthreads();
 
     int n_slots = 0, stall = 0, it_run = 0;
     int term = sched_ok ? FPSSFT_TERM_MAX_ITERATIONS : -1;
-    R amp_sum = (R)0;
+    A amp_sum = (A)0;
     int nal[MAXD], nta[MAXD];
 #pragma unroll
     for (int k = 0; k < MAXD; ++k) {
@@ -157,41 +174,66 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
             }
             // (no L2 prefetch here: measured slower on config 5, 42.3 vs 38.2 ms)
         }
+        if constexpr (GUARD)
+            for (int b = tid; b < L; b += NT) pabs[b] = 0.f;
         if constexpr (sizeof(R) == 4) cp_async_wait_all();
         if constexpr (stage16_ok(DC, LC, (int)sizeof(cpx<R>), NT)) {
-            if (staged) compact_stage16<LC, nl, NT, BlockTeam>((cpx<float> *)spec, par, dup, tid);
+            if (staged)
+                compact_stage16<LC, nl, NT, BlockTeam>((cpx<float> *)spec, par, dup, tid,
+                                                       GUARD ? x0d : nullptr);
         }
         __syncthreads();
+        if constexpr (GUARD) {
+            if (!staged) {  // line 0's samples into the float64 buffer
+                for (int l = tid; l < L; l += NT) {
+                    const cpx<R> v = spec[padi<PAD>(l)];
+                    x0d[padi<PAD>(l)] = {(double)v.re, (double)v.im};
+                }
+                __syncthreads();
+            }
+        }
         R my_energy;
-        if constexpr (FPSSFT_TEAM_REGFFT && LC == 512 && sizeof(R) == 4 && NT / 32 >= nl) {
+        constexpr bool REG512 = FPSSFT_TEAM_REGFFT && LC == 512 && sizeof(R) == 4 && NW >= nl;
+        if constexpr (REG512) {
             // one warp per line, in registers (regfft::): no block barrier inside
             my_energy = regfft::fft512_lines_warp<NT>((cpx<float> *)spec, nl,
                                                       (const cpx<float> *)roots, tid);
+            if constexpr (GUARD) {  // line 0 in float64 by the warp left idle, else after
+                if (NW > nl && warp == NW - 1)
+                    fft_static<double, LC, 1, 32, WarpTeam, Roots64Split>(x0d, roots64, lane);
+            }
             __syncthreads();
+            if constexpr (GUARD) {
+                if (NW == nl) fft_static<double, LC, 1, NT, BlockTeam, Roots64Split>(x0d, roots64, tid);
+            }
         } else if constexpr (FPSSFT_TEAM_REGFFT && LC == 2048 && sizeof(R) == 4 &&
                              NT >= 128 * nl && nl < 16) {
             // four warps per line, in registers, named barriers per line
             my_energy = regfft::fft2048_lines_team<NT>((cpx<float> *)spec, nl,
                                                        (const cpx<float> *)roots, tid);
             __syncthreads();
+            if constexpr (GUARD) fft_static<double, LC, 1, NT, BlockTeam, Roots64Split>(x0d, roots64, tid);
         } else {
             my_energy = fft_static<R, LC, nl, NT, BlockTeam>(spec, roots, tid);
+            if constexpr (GUARD) fft_static<double, LC, 1, NT, BlockTeam, Roots64Split>(x0d, roots64, tid);
         }
         R noise_floor = (R)0;
-        if (sizeof(R) == 4 && kn.noise_coef > 0)
+        [[maybe_unused]] float Ef = 0.f;  // GUARD: transform part of the error bound
+        if constexpr (GUARD) {
+            Ef = (float)(kn.guard_coef * sqrt((double)block_sum(my_energy, rred)));
+        } else if (sizeof(R) == 4 && kn.noise_coef > 0) {
             noise_floor = (R)kn.noise_coef * sqrt(block_sum(my_energy, rred));
+        }
 
-        // (3) construction-subtraction
-#if FPSSFT_TEAM_PROJ == 1
-        //     NT slots per round, 32 per warp; slots sharing a bin inside a
-        //     warp are summed by their lowest lane (match_any), and the warps
-        //     apply their partial sums one after another -- a fixed order, so
-        //     the result is deterministic without a sort
+        // (3) construction-subtraction: NT slots per round, 32 per warp;
+        //     slots sharing a bin inside a warp are summed by their lowest
+        //     lane (match_any), and the warps apply their partial sums one
+        //     after another -- a fixed order, so the result is deterministic
+        //     without a sort.  GUARD: also the float64 line-0 projection and
+        //     the bins' sum |a| (the projection's share of the error bound).
         if (n_slots > 0) {
-            constexpr int NW = NT / 32;
-            const int warp = tid >> 5, lane = tid & 31;
-            int *scr_u = (int *)(sm + lay.bin_start) + warp * 32 * (MAXD + 1);
-            cpx<R> *scr_amp = (cpx<R> *)((int *)(sm + lay.bin_start) + NW * 32 * (MAXD + 1)) +
+            int *scr_u = (int *)(sm + lay.proj) + warp * 32 * (MAXD + 1);
+            cpx<A> *scr_amp = (cpx<A> *)((int *)(sm + lay.proj) + NW * 32 * (MAXD + 1)) +
                               warp * 32;
             // Q sub-rounds of NT slots per round: the warps' ordered apply (NW-1
             // barriers) is paid once per Q * NT slots
@@ -199,6 +241,8 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
 #pragma unroll 1
             for (int c0 = 0; c0 < n_slots; c0 += Q * NT) {
                 cpx<R> P[Q][MAXD + 1];
+                [[maybe_unused]] cpx<double> P0[Q];
+                [[maybe_unused]] float pa[Q];
                 int bq[Q];
                 bool leader[Q];
 #pragma unroll
@@ -223,13 +267,23 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
                     bq[q] = b;
 #pragma unroll
                     for (int i = 0; i < MAXD + 1; ++i) P[q][i] = {(R)0, (R)0};
+                    if constexpr (GUARD) {
+                        P0[q] = {0.0, 0.0};
+                        pa[q] = 0.f;
+                    }
                     if (leader[q]) {
                         for (unsigned rest = grp; rest; rest &= rest - 1) {
                             const int j = __ffs(rest) - 1;
-                            const cpx<R> aj = scr_amp[j];
+                            const cpx<A> aj = scr_amp[j];
+                            const cpx<R> ar = {(R)aj.re, (R)aj.im};
 #pragma unroll
                             for (int i = 0; i < MAXD + 1; ++i)
-                                if (i < nl) P[q][i] = P[q][i] + aj * roots[scr_u[i * 32 + j]];
+                                if (i < nl) P[q][i] = P[q][i] + ar * roots[scr_u[i * 32 + j]];
+                            if constexpr (GUARD) {
+                                const cpx<double> ad = {(double)aj.re, (double)aj.im};
+                                P0[q] = P0[q] + ad * roots64[scr_u[j]];
+                                pa[q] += cabs(ar);
+                            }
                         }
                     }
                 }
@@ -245,151 +299,192 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
                                     if (i < nl)
                                         spec[padi<PAD>(i * L + bq[q])] =
                                             spec[padi<PAD>(i * L + bq[q])] - P[q][i];
+                                if constexpr (GUARD) {
+                                    x0d[padi<PAD>(bq[q])] = x0d[padi<PAD>(bq[q])] - P0[q];
+                                    pabs[bq[q]] += pa[q];
+                                }
                             }
                     }
                 }
                 __syncthreads();
             }
         }
-#else
-        //     counting sort of the live slots by
-        //     bin, per-bin sums in slot order (deterministic, no float atomics)
-        if (n_slots > 0) {
-            int *fill = (int *)bin_fill;
-            for (int b = tid; b < L; b += NT) fill[b] = 0;
-            __syncthreads();
-            for (int s = tid; s < n_slots; s += NT) {
-                unsigned short bb = U16_NONE;
-                if (slot_live[s]) {
-                    int m[MAXD];
-                    unpack_key(slot_key[s], g, m);
-                    const int b = bin_of(m, g, al);
-                    bb = (unsigned short)b;
-                    slot_u0[s] = (unsigned short)phase_of(m, g, ta);
-                    atomicAdd(&fill[b], 1);
-                }
-                slot_bin[s] = bb;
-            }
-            __syncthreads();
-            int carry = 0;
-#pragma unroll 1
-            for (int j0 = 0; j0 < L; j0 += NT) {
-                const int b = j0 + tid;
-                const int c = b < L ? fill[b] : 0;
-                int tot;
-                const int pre = block_exscan(c, ired, &tot);
-                if (b < L) {
-                    bin_start[b] = (unsigned short)(carry + pre);
-                    fill[b] = 0;
-                }
-                carry += tot;
-            }
-            if (tid == 0) bin_start[L] = (unsigned short)carry;
-            __syncthreads();
-            for (int s = tid; s < n_slots; s += NT) {
-                const unsigned short bb = slot_bin[s];
-                if (bb != U16_NONE) seg[bin_start[bb] + atomicAdd(&fill[bb], 1)] = (unsigned short)s;
-            }
-            __syncthreads();
-            for (int b = tid; b < L; b += NT) {
-                const int st = bin_start[b], en = bin_start[b + 1];
-                if (en == st) continue;
-                for (int i = st + 1; i < en; ++i) {  // short segments: insertion sort
-                    const unsigned short v = seg[i];
-                    int j = i - 1;
-                    while (j >= st && seg[j] > v) {
-                        seg[j + 1] = seg[j];
-                        --j;
-                    }
-                    seg[j + 1] = v;
-                }
-                cpx<R> P[MAXD + 1];
-#pragma unroll
-                for (int i = 0; i < MAXD + 1; ++i) P[i] = {(R)0, (R)0};
-                for (int p = st; p < en; ++p) {
-                    const int s = seg[p];
-                    int m[MAXD];
-                    unpack_key(slot_key[s], g, m);
-                    const cpx<R> as = slot_amp[s];
-                    const int u0 = slot_u0[s];
-#pragma unroll
-                    for (int i = 0; i < MAXD + 1; ++i)
-                        if (i < nl) P[i] = P[i] + as * roots[phase_step(u0, i, m, g)];
-                }
-#pragma unroll
-                for (int i = 0; i < MAXD + 1; ++i)
-                    if (i < nl) spec[padi<PAD>(i * L + b)] = spec[padi<PAD>(i * L + b)] - P[i];
-            }
-            __syncthreads();
-        }
-
-#endif
 
         // (4) magnitude test on every bin, candidates compacted in ascending
-        //     order; the residual of non-candidate bins is folded in
-        const R floor =
-            max(max((R)kn.energy_floor_abs, (R)kn.energy_floor * amp_sum), noise_floor);
+        //     order; the residual of non-candidate bins is folded in.  GUARD:
+        //     bins inside the guard band join the list, flagged
+        const A floor_a = max(max((A)kn.energy_floor_abs, (A)kn.energy_floor * amp_sum),
+                              (A)noise_floor);
+        const R floor = (R)floor_a;
         R resid = (R)0;
         int n_cand = 0;
         {
             // thread t tests the BPT consecutive bins [t BPT, (t+1) BPT): one
             // block scan of the per-thread counts keeps ascending order
             constexpr int BPT = (LC + NT - 1) / NT;
-            unsigned okm = 0;
+            unsigned okm = 0, flm = 0;
 #pragma unroll
             for (int j = 0; j < BPT; ++j) {
                 const int b = tid * BPT + j;
                 R top = (R)0;
-                const bool ok = b < L && bin_is_candidate<R, PAD>(spec, g, b, mag_tol, floor, &top);
-                if (!ok) resid = max(resid, top);
-                okm |= (unsigned)ok << j;
+                bool ok = false, fl = false;
+                if (b < L) {
+                    if constexpr (GUARD)
+                        ok = bin_is_candidate_guarded<PAD>((const cpx<float> *)spec, g, b,
+                                                           (float)mag_tol, (float)floor,
+                                                           Ef + GUARD_KP * pabs[b], (float *)&top,
+                                                           &fl);
+                    else
+                        ok = bin_is_candidate<R, PAD>(spec, g, b, mag_tol, floor, &top);
+                }
+                if (!ok && !fl) resid = max(resid, top);
+                okm |= (unsigned)(ok || fl) << j;
+                flm |= (unsigned)fl << j;
             }
             int pos = block_exscan(__popc(okm), ired, &n_cand);
 #pragma unroll
             for (int j = 0; j < BPT; ++j)
-                if (okm >> j & 1) cand[pos++] = (unsigned short)(tid * BPT + j);
+                if (okm >> j & 1)
+                    cand[pos++] = (unsigned short)(tid * BPT + j) |
+                                  (unsigned short)((flm >> j & 1) ? CAND_FLAG : 0);
         }
         __syncthreads();
 
         // (5) decode + merge-by-sum, NT candidates per round in ascending bin
         //     order (driver.py:103-108); decode results stay in registers
-        int n_acc = 0;
+        int n_acc = 0, n_cand_x = 0;
         bool overflow = false;
 #pragma unroll 1
         for (int c0 = 0; c0 < n_cand; c0 += NT) {
             const int idx = c0 + tid;
-            const int b = idx < n_cand ? cand[idx] : -1;
+            const int ce = idx < n_cand ? cand[idx] : -1;
+            const int b = ce >= 0 ? (ce & ~(int)CAND_FLAG) : -1;
             int m[MAXD];
             cpx<R> a;
             int st = 0;
-            if (b >= 0)
-                st = decode_candidate<R, PAD>(spec, g, b, al, ta, roots, round_tol, verify_tol, m, &a);
+            if constexpr (GUARD) {
+                const bool mflag = ce >= 0 && ((ce & CAND_FLAG) || FPSSFT_GUARD_CALIB == 1);
+                if (b >= 0 && !mflag)
+                    st = decode_candidate_guarded<PAD>((const cpx<float> *)spec, g, b, al, ta,
+                                                       (const cpx<float> *)roots,
+                                                       (float)round_tol, (float)verify_tol,
+                                                       Ef + GUARD_KP * pabs[b], m);
+                const bool need = b >= 0 && (mflag || st == ST_FLAG);
+                int nf;
+                const int fpos = block_exscan((int)need, ired, &nf);
+#if FPSSFT_GUARD_CALIB == 2
+                if (tid == 0 && nf) atomicAdd(&g_guard_calib_count, (unsigned long long)nf);
+#endif
+                if (nf > 0) {  // exact float64 re-evaluation of the flagged bins
+                    if (need) flist[fpos] = (unsigned short)tid;
+                    __syncthreads();
+#pragma unroll 1
+                    for (int f = 0; f < nf; ++f) {
+                        const int owner = flist[f];
+                        const int bf = cand[c0 + owner] & ~(int)CAND_FLAG;
+                        cpx<double> dft[MAXD], prj[MAXD];
+                        exact_bin_partials<A>(bf, cube, g, al, ta, roots64, n_slots, slot_key,
+                                              slot_live, slot_amp, tid, NT, dft, prj);
+                        double v[4 * MAXD];
+#pragma unroll
+                        for (int i = 0; i < MAXD; ++i) {
+                            v[4 * i] = warp_sum(dft[i].re);
+                            v[4 * i + 1] = warp_sum(dft[i].im);
+                            v[4 * i + 2] = warp_sum(prj[i].re);
+                            v[4 * i + 3] = warp_sum(prj[i].im);
+                        }
+                        if (lane == 0)
+#pragma unroll
+                            for (int i = 0; i < 4 * D; ++i) dred[warp * 4 * MAXD + i] = v[i];
+                        __syncthreads();
+                        if (tid == 0) {
+                            cpx<double> S[MAXD + 1];
+                            S[0] = x0d[padi<PAD>(bf)];
+                            for (int i = 0; i < D; ++i) {
+                                double t[4] = {0.0, 0.0, 0.0, 0.0};
+                                for (int w2 = 0; w2 < NW; ++w2)
+                                    for (int c = 0; c < 4; ++c) t[c] += dred[w2 * 4 * MAXD + 4 * i + c];
+                                S[i + 1] = {t[0] / (double)L - t[2], t[1] / (double)L - t[3]};
+                            }
+                            int mx[MAXD];
+                            cpx<double> ax;
+                            const int sx = classify_values<double, Roots64Split>(
+                                S, g, bf, al, ta, roots64, kn.mag_tol, kn.round_tol,
+                                kn.verify_tol, (double)floor_a, mx, &ax);
+                            res_st[owner] = sx;
+                            res_key[owner] = sx >= 2 ? pack_key(mx, g) : 0;
+#if FPSSFT_GUARD_CALIB == 1
+                            {   // float32 value error against the exact values, in units
+                                // of the bound at kappa = 1
+                                const double unit = (double)Ef / GUARD_KF + U32 * pabs[bf];
+                                double worst = 0.0;
+                                for (int i = 0; i <= D; ++i) {
+                                    const cpx<R> v = spec[padi<PAD>(i * L + bf)];
+                                    worst = fmax(worst, hypot((double)v.re - S[i].re,
+                                                              (double)v.im - S[i].im));
+                                }
+                                atomicMax(&g_guard_calib_max, __float_as_uint((float)(worst / unit)));
+                                atomicAdd(&g_guard_calib_count, 1ull);
+                            }
+#endif
+                        }
+                        __syncthreads();
+                    }
+                    if (need) {
+                        st = res_st[tid];
+                        unpack_key(res_key[tid], g, m);
+                    }
+                }
+            } else {
+                if (b >= 0)
+                    st = decode_candidate<R, PAD>(spec, g, b, al, ta, roots, round_tol,
+                                                  verify_tol, m, &a);
+            }
             int found = -1, key = 0;
             if (st == 2) {
                 key = pack_key(m, g);
                 found = hash16_find(hash, slot_key, H, key);
             }
             const int fresh = st == 2 && found < 0;
-            int tot;  // low 16 bits: new slots, high: accepted
-            const int pre = block_exscan(fresh | ((st == 2) << 16), ired, &tot);
-            const int tot_new = tot & 0xFFFF;
+            int tot;  // packed counts: new slots, accepted (, candidates when guarded)
+            int pre, tot_new, tot_acc;
+            if constexpr (GUARD) {
+                pre = block_exscan(fresh | ((st == 2) << 10) | ((st >= 1) << 20), ired, &tot);
+                tot_new = tot & 0x3FF;
+                tot_acc = (tot >> 10) & 0x3FF;
+                n_cand_x += (tot >> 20) & 0x3FF;
+                pre &= 0x3FF;
+            } else {
+                pre = block_exscan(fresh | ((st == 2) << 16), ired, &tot);
+                tot_new = tot & 0xFFFF;
+                tot_acc = tot >> 16;
+                pre &= 0xFFFF;
+            }
             if (n_slots + tot_new > kn.k_cap) {
                 overflow = true;
                 break;
             }
             if (st == 2) {
-                cpx<R> v = a;
+                cpx<A> av;
+                if constexpr (GUARD) {  // the float64 amplitude (decoder.py:160)
+                    const int u0 = phase_of(m, g, ta);
+                    av = mulc(x0d[padi<PAD>(b)], roots64[u0]);
+                    a = {(R)av.re, (R)av.im};
+                } else {
+                    av = a;
+                }
+                cpx<A> v = av;
                 int s;
                 if (fresh) {
-                    s = n_slots + (pre & 0xFFFF);
+                    s = n_slots + pre;
                     slot_key[s] = key;
                     hash16_insert(hash, H, key, s);
                 } else {
                     s = found;
-                    v = slot_amp[s] + a;  // a pruned slot holds 0: entries.get(f, 0) + a
+                    v = slot_amp[s] + av;  // a pruned slot holds 0: entries.get(f, 0) + a
                 }
-                const bool keep = !(cabs(v) <= prune);
-                slot_amp[s] = keep ? v : cpx<R>{(R)0, (R)0};
+                const bool keep = !(cabs(v) <= (A)kn.amp_prune_tol);
+                slot_amp[s] = keep ? v : cpx<A>{(A)0, (A)0};
                 slot_live[s] = keep;
                 const int u0 = phase_of(m, g, ta);  // driver.py:189-194
 #pragma unroll
@@ -400,9 +495,10 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
             }
             if (b >= 0) resid = max(resid, bin_residual<R, PAD>(spec, g, b));
             n_slots += tot_new;
-            n_acc += tot >> 16;
+            n_acc += tot_acc;
             __syncthreads();  // inserts visible to the next round's lookups
         }
+        if constexpr (GUARD) n_cand = n_cand_x;
         if (overflow) {
             term = FPSSFT_TERM_K_CAP_OVERFLOW;
             if (tid == 0 && out.iter_stats) {
@@ -415,13 +511,16 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
         }
 
         // (6) amp_sum and (7) termination                   driver.py:108,196-204
-        R my = (R)0;
+        A my = (A)0;
         for (int s = tid; s < n_slots; s += NT)
             if (slot_live[s]) my += cabs(slot_amp[s]);
-        amp_sum = block_sum(my, rred);
+        if constexpr (GUARD)
+            amp_sum = block_sum(my, dred);
+        else
+            amp_sum = block_sum(my, rred);
         const R worst = block_max(resid, rred);  // |S|^2 (float) or |S| (double)
         stall = n_acc > 0 ? 0 : stall + 1;
-        const R clean = max((R)kn.energy_floor_abs, (R)kn.residual_stop * amp_sum);
+        const R clean = (R)max((A)kn.energy_floor_abs, (A)kn.residual_stop * amp_sum);
         const bool is_clean = sizeof(R) == 8 ? worst <= clean : worst <= clean * clean;
         if (tid == 0 && out.iter_stats) {
             int *st = out.iter_stats + (inst * kn.t_max + it) * 3;
@@ -507,4 +606,3 @@ __global__ void __launch_bounds__(NT, (512 / NT > 1 ? 512 / NT : 1)) recover_tea
         out.terminated_by[inst] = term;
     }
 }
-

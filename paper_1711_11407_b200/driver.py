@@ -15,8 +15,12 @@ Deliberate differences:
 * The schedule (alpha_t, tau_t) is explicit.  ``fps_sft`` derives it from
   ``config.seed`` exactly as the reference draws it (``schedule.py``), so the
   same seed follows the same lines.
-* Arithmetic is float32 by default (``precision="fp32"``, the north-star
-  configuration); ``precision="fp64"`` runs the same kernels in float64.
+* Arithmetic is float32 (the north-star configuration): plain
+  (``precision="fp32"``) for tight noiseless profiles, guarded
+  (``"fp32-guarded"``: float64 amplitudes, every decision inside its float32
+  error bound of the threshold re-evaluated in float64) for the loose noisy
+  profiles -- ``"auto"`` (default) picks by the profile; ``"fp64"`` runs the
+  kernels in float64.
 * ``time_domain_subtraction`` is accepted for signature compatibility; the
   device path always subtracts in the frequency domain (the reference states
   both give identical results up to roundoff, driver.py:37-41).
@@ -106,11 +110,20 @@ def default_max_iterations(shape: CubeShape) -> int:
     return max(1, shape.n_total // ((shape.ndim + 1) * shape.line_len))
 
 
-def _precision_code(precision: str) -> int:
+def _precision_code(precision: str, config=None) -> int:
+    """``fp32`` | ``fp64`` | ``fp32-guarded`` (float32 arithmetic with the
+    float64 reference's decisions, csrc/fpssft_guard.cuh) | ``auto``:
+    guarded for loose (noisy-data) tolerance profiles, where decision
+    statistics land near their thresholds, plain float32 otherwise."""
+    if precision == "auto":
+        loose = config is not None and max(config.mag_tol, config.verify_tol) >= 1e-3
+        return N.F32_GUARDED if loose else N.F32
     if precision in ("fp32", "float32", "f32"):
         return N.F32
     if precision in ("fp64", "float64", "f64"):
         return N.F64
+    if precision in ("fp32-guarded", "fp32g", "guarded"):
+        return N.F32_GUARDED
     raise ValueError(f"unknown precision {precision!r}")
 
 
@@ -137,13 +150,14 @@ def _pow2_ceil(x: int) -> int:
     return 1 << max(0, int(x - 1).bit_length())
 
 
-def max_k_cap(shape: CubeShape, precision: str = "fp32", mode: str = "auto") -> int:
+def max_k_cap(shape: CubeShape, precision: str = "fp32", mode: str = "auto",
+              config=None) -> int:
     """Largest power-of-two capacity whose on-chip state fits (in ``mode``)."""
     sh = N.make_shape(shape.dims)
     best = 0
     k = 1
     while k <= (1 << 20):
-        p = _params(FpsSftConfig(), 1, k, _precision_code(precision), mode)
+        p = _params(FpsSftConfig(), 1, k, _precision_code(precision, config), mode)
         if N.lib().fpssft_smem_bytes(C_ref(sh), C_ref(p)) == 0:  # no plan fits
             break
         best = k
@@ -259,7 +273,7 @@ class BatchRunner:
     device, outputs allocated once, one ``fpssft_run_batch`` per ``run``."""
 
     def __init__(self, shape: CubeShape, config: FpsSftConfig, batch: int, *, schedule=None,
-                 sched_index=None, k_cap: int = 256, precision: str = "fp32",
+                 sched_index=None, k_cap: int = 256, precision: str = "auto",
                  iter_stats: bool = False, device=None, mode: str = "auto", group: int = 1):
         import torch
 
@@ -288,7 +302,7 @@ class BatchRunner:
         if k_cap < 1 or k_cap & (k_cap - 1):
             raise ValueError("k_cap must be a positive power of two")
         self.k_cap = int(k_cap)
-        self.prec = _precision_code(precision)
+        self.prec = _precision_code(precision, config)
         self._shape_c = N.make_shape(shape.dims)
         self._params_c = _params(config, self.t_max, self.k_cap, self.prec, mode)
         self.plan = launch_plan(shape, self._params_c)
@@ -376,7 +390,7 @@ def launch_plan(shape: CubeShape, params: N.Params) -> dict:
 
 
 def fps_sft_batch(cubes, config: FpsSftConfig = FpsSftConfig(), *, schedule=None,
-                  sched_index=None, k_cap: int = 256, precision: str = "fp32",
+                  sched_index=None, k_cap: int = 256, precision: str = "auto",
                   iter_stats: bool = False, mode: str = "auto") -> BatchResult:
     """Recover every instance of ``cubes`` (complex64 CUDA tensor [B, *dims]).
 
@@ -430,7 +444,7 @@ def materialize(source, device=None) -> tuple[CubeShape, "np.ndarray | object"]:
 
 
 def fps_sft(source: SignalSource, config: FpsSftConfig = FpsSftConfig(), *,
-            precision: str = "fp32", k_cap: int | None = None, device=None,
+            precision: str = "auto", k_cap: int | None = None, device=None,
             mode: str = "auto") -> RecoveryReport:
     """Recover the sparse spectrum of ``source`` on the GPU (driver.py:121-212).
 
@@ -448,7 +462,7 @@ def fps_sft(source: SignalSource, config: FpsSftConfig = FpsSftConfig(), *,
         t = torch.as_tensor(np.ascontiguousarray(cube, dtype=np.complex64)).to(dev)
     t = t.reshape((1, *shape.dims))
     if k_cap is None:
-        k_cap = min(_pow2_ceil(shape.n_total), max_k_cap(shape, precision, mode))
+        k_cap = min(_pow2_ceil(shape.n_total), max_k_cap(shape, precision, mode, config))
         if k_cap < 1:
             raise N.UnsupportedError(f"shape {shape.dims} does not fit one CTA")
     res = fps_sft_batch(t, config, k_cap=k_cap, precision=precision, iter_stats=True, mode=mode)

@@ -68,7 +68,7 @@ class HostBatchRunner:
     """
 
     def __init__(self, shape: CubeShape, config: FpsSftConfig, batch: int, *,
-                 k_cap: int = 256, precision: str = "fp32", device=None, mode: str = "auto",
+                 k_cap: int = 256, precision: str = "auto", device=None, mode: str = "auto",
                  zero_copy_fraction: float | None = None, chunk: int | None = None,
                  chunk_bytes: int = 256 << 20, schedule=None, sched_index=None,
                  graphs: bool = True):
