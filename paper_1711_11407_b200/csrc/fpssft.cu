@@ -784,6 +784,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         __syncwarp();
         bool overflow = false;
         int n_cand_x = 0;
+        [[maybe_unused]] A d_amp = (A)0;  // GUARD: this lane's change of amp_sum
         for (int c0 = 0; c0 < n_cand; c0 += 32) {
             const int ce = c0 + lane < n_cand ? cand[c0 + lane] : -1;
             const int b = ce >= 0 ? (ce & ~(int)CAND_FLAG) : -1;
@@ -875,7 +876,10 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
                     s = found;
                     v = slot_amp[s] + av;  // a pruned slot holds 0: entries.get(f, 0) + a
                 }
-                const bool keep = !(cabs(v) <= (A)kn.amp_prune_tol);
+                const A av_new = cabs(v);
+                const bool keep = !(av_new <= (A)kn.amp_prune_tol);
+                if constexpr (GUARD)  // amp_sum kept incrementally (float64)
+                    d_amp += (keep ? av_new : (A)0) - (found < 0 ? (A)0 : cabs(slot_amp[s]));
                 slot_amp[s] = keep ? v : cpx<A>{(A)0, (A)0};
                 slot_live[s] = keep;
                 const int u0 = phase_of(m, g, ta);  // driver.py:189-194
@@ -901,10 +905,14 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         __syncwarp();
 
         // (6) amp_sum = sum |a| over the recovered set        driver.py:108
-        A my = (A)0;
-        for (int s = lane; s < n_slots; s += 32)
-            if (slot_live[s]) my += cabs(slot_amp[s]);
-        amp_sum = __shfl_sync(FULL, warp_sum(my), 0);
+        if constexpr (GUARD) {
+            amp_sum += __shfl_sync(FULL, warp_sum(d_amp), 0);
+        } else {
+            A my = (A)0;
+            for (int s = lane; s < n_slots; s += 32)
+                if (slot_live[s]) my += cabs(slot_amp[s]);
+            amp_sum = __shfl_sync(FULL, warp_sum(my), 0);
+        }
         stall = n_acc > 0 ? 0 : stall + 1;
 
         // (7) termination                                     driver.py:196-204

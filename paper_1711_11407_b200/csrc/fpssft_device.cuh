@@ -528,6 +528,70 @@ __device__ __forceinline__ void compact_stage16(cpx<float> *spec, unsigned par, 
             for (int j = 0; j < J; ++j) x0d[padi<true>(NTC * j + tid)] = {(double)v[j].x, (double)v[j].y};
     }
 }
+// Group gather (interleaved batch layout [B/G, *dims, G]): the WG warps of a
+// CTA own WG consecutive members of one interleave group, which share the
+// schedule, so at every sample position their WG samples are contiguous
+// (WG * 8 bytes) and are fetched once for all of them -- as 16-byte chunks,
+// one thread per chunk, with L1-bypassing register loads -- and scattered
+// into the owners' padded spectra.  Thread tid takes chunk c = tid % CH
+// (members 2c, 2c + 1) of positions q = tid / CH + QS j (q = line * LC + l).
+// The index arithmetic of a position is done once per group, not once per
+// instance, and no 16-byte staging area is needed.
+__device__ __forceinline__ float4 ld_nc16(const float2 *p) {
+    float4 v;
+    asm("ld.global.nc.L1::no_allocate.L2::64B.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+template <int LC, int DC, int WG>
+struct GroupGather {
+    static constexpr int NL = DC + 1, CH = WG / 2, NTH = WG * 32, QS = NTH / CH;
+    static constexpr int PPT = NL * LC * CH / NTH;  // chunks per thread
+    static constexpr int LQ = LC / QS;              // distinct l per thread
+    static_assert(WG % 2 == 0 && LC % QS == 0 && PPT * NTH == NL * LC * CH,
+                  "group gather: whole lines per thread");
+    float4 v[PPT];
+    // gbase: the CTA's first member's sample 0 (group block + member0);
+    // strides include the factor G of the interleaved layout
+    __device__ __forceinline__ void load(const float2 *__restrict__ gbase, const Geo &g,
+                                         const int *al, const int *ta, int tid) {
+        const int c = tid % CH, q0 = tid / CH;
+        int n[LQ][DC];
+#pragma unroll
+        for (int j = 0; j < LQ; ++j)
+#pragma unroll
+            for (int k = 0; k < DC; ++k)
+                n[j][k] = (int)fastmod((unsigned)al[k] * (unsigned)(q0 + QS * j) + (unsigned)ta[k],
+                                       g.magic[k], (unsigned)g.N[k]);
+#pragma unroll
+        for (int i = 0; i < NL; ++i) {
+#pragma unroll
+            for (int j = 0; j < LQ; ++j) {
+                int off = 0;
+#pragma unroll
+                for (int k = 0; k < DC; ++k) {
+                    int nk = n[j][k];
+                    if (k == i - 1) nk = nk + 1 == g.N[k] ? 0 : nk + 1;  // tau + e_k
+                    off += nk * g.stride32[k];
+                }
+                v[i * LQ + j] = ld_nc16(gbase + off + 2 * c);
+            }
+        }
+    }
+    // owner spectra: warp w's at spec0 + w * warp_stride (complex units)
+    __device__ __forceinline__ void store(cpx<float> *spec0, int warp_stride, int tid) const {
+        const int c = tid % CH, q0 = tid / CH;
+        cpx<float> *a = spec0 + (2 * c) * warp_stride, *b = a + warp_stride;
+#pragma unroll
+        for (int t = 0; t < PPT; ++t) {
+            const int q = q0 + QS * t;  // position t: line t / LQ, l = q0 + QS (t % LQ)
+            const int e = padi<true>(q);
+            a[e] = {v[t].x, v[t].y};
+            b[e] = {v[t].z, v[t].w};
+        }
+    }
+};
+
 // L2 prefetch of a future iteration's line samples (compile-time line
 // length, one warp): the same addresses as gather_lines_async, no data moved
 // on chip.

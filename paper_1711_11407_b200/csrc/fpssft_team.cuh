@@ -29,7 +29,7 @@
 struct TeamLayout {
     size_t spec, roots, slot_amp, slot_key, hash, slot_live;
     size_t x0d, roots64, pabs;                 // GUARD only
-    size_t proj, cand, res_st, res_key, flist;  // union: projection / classifier scratch
+    size_t proj, cand;  // union: projection / classifier scratch
     size_t red, total;
     int H;
 };
@@ -57,21 +57,13 @@ __host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, 
         y.pabs = o;    o = align16(o + (size_t)L * 4);
     }
     // union: the projection's per-warp scratch (phases + amplitudes of 32
-    // slots) / the classifier's candidate list and the guard's per-round
-    // exact-evaluation results
+    // slots) / the classifier's candidate list
     const size_t u = o;
     y.proj = u;
     const size_t a = align16(u + (size_t)(nt / 32) * 32 * ((MAXD + 1) * 4 + acs));
-    y.cand = u;      size_t b = align16(u + (size_t)L * 2);
-    y.res_st = b;    b = align16(b + (size_t)nt * 4);
-    y.res_key = b;   b = align16(b + (size_t)nt * 4);
-    y.flist = b;     b = align16(b + (size_t)nt * 2);
-    if (!guard) b = align16(u + (size_t)L * 2);
+    y.cand = u;      const size_t b = align16(u + (size_t)L * 2);
     o = a > b ? a : b;
-    // reductions: 256 B of int scratch, then NW floats/doubles (and the
-    // guard's NW x 4 MAXD doubles of exact-evaluation partial sums)
-    const size_t dr = (size_t)(nt / 32) * 4 * MAXD * 8;
-    y.red = o;       o = align16(o + 256 + (guard && dr > 256 ? dr : 256));
+    y.red = o;       o = align16(o + 64 * 8);  // 256 B of ints, then NW floats/doubles
     y.total = o;
     return y;
 }
@@ -105,9 +97,6 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
     [[maybe_unused]] const Roots64Split roots64{(const cpx<float> *)roots, roots_lo};
     [[maybe_unused]] float *pabs = (float *)(sm + lay.pabs);
     unsigned short *cand = (unsigned short *)(sm + lay.cand);
-    [[maybe_unused]] int *res_st = (int *)(sm + lay.res_st);
-    [[maybe_unused]] int *res_key = (int *)(sm + lay.res_key);
-    [[maybe_unused]] unsigned short *flist = (unsigned short *)(sm + lay.flist);
     int *ired = (int *)(sm + lay.red);
     R *rred = (R *)(sm + lay.red + 256);
     [[maybe_unused]] double *dred = (double *)(sm + lay.red + 256);
@@ -353,6 +342,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
         // (5) decode + merge-by-sum, NT candidates per round in ascending bin
         //     order (driver.py:103-108); decode results stay in registers
         int n_acc = 0, n_cand_x = 0;
+        [[maybe_unused]] A d_amp = (A)0;  // GUARD: this thread's change of amp_sum
         bool overflow = false;
 #pragma unroll 1
         for (int c0 = 0; c0 < n_cand; c0 += NT) {
@@ -369,70 +359,46 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
                                                        (const cpx<float> *)roots,
                                                        (float)round_tol, (float)verify_tol,
                                                        Ef + GUARD_KP * pabs[b], m);
-                const bool need = b >= 0 && (mflag || st == ST_FLAG);
-                int nf;
-                const int fpos = block_exscan((int)need, ired, &nf);
+                const unsigned need = __ballot_sync(FULL, b >= 0 && (mflag || st == ST_FLAG));
 #if FPSSFT_GUARD_CALIB == 2
-                if (tid == 0 && nf) atomicAdd(&g_guard_calib_count, (unsigned long long)nf);
+                if (lane == 0 && need) atomicAdd(&g_guard_calib_count, (unsigned long long)__popc(need));
 #endif
-                if (nf > 0) {  // exact float64 re-evaluation of the flagged bins
-                    if (need) flist[fpos] = (unsigned short)tid;
-                    __syncthreads();
-#pragma unroll 1
-                    for (int f = 0; f < nf; ++f) {
-                        const int owner = flist[f];
-                        const int bf = cand[c0 + owner] & ~(int)CAND_FLAG;
-                        cpx<double> dft[MAXD], prj[MAXD];
-                        exact_bin_partials<A>(bf, cube, g, al, ta, roots64, n_slots, slot_key,
-                                              slot_live, slot_amp, tid, NT, dft, prj);
-                        double v[4 * MAXD];
+                // exact float64 re-evaluation of this warp's flagged bins, one
+                // at a time by the whole warp (no block barrier)
+                for (unsigned rest = need; rest; rest &= rest - 1) {
+                    const int owner = __ffs(rest) - 1;
+                    const int bf = __shfl_sync(FULL, b, owner);
+                    cpx<double> dft[MAXD], prj[MAXD];
+                    exact_bin_partials<A>(bf, cube, g, al, ta, roots64, n_slots, slot_key,
+                                          slot_live, slot_amp, lane, 32, dft, prj);
+                    cpx<double> S[MAXD + 1];
+                    S[0] = x0d[padi<PAD>(bf)];
 #pragma unroll
-                        for (int i = 0; i < MAXD; ++i) {
-                            v[4 * i] = warp_sum(dft[i].re);
-                            v[4 * i + 1] = warp_sum(dft[i].im);
-                            v[4 * i + 2] = warp_sum(prj[i].re);
-                            v[4 * i + 3] = warp_sum(prj[i].im);
-                        }
-                        if (lane == 0)
+                    for (int i = 0; i < MAXD; ++i)
+                        if (i < D)
+                            S[i + 1] = {warp_sum(dft[i].re) / (double)L - warp_sum(prj[i].re),
+                                        warp_sum(dft[i].im) / (double)L - warp_sum(prj[i].im)};
+                    int mx[MAXD];
+                    cpx<double> ax;
+                    // every lane holds the same sums: each decides, the owner keeps it
+                    const int sx = classify_values<double, Roots64Split>(
+                        S, g, bf, al, ta, roots64, kn.mag_tol, kn.round_tol, kn.verify_tol,
+                        (double)floor_a, mx, &ax);
+                    if (lane == owner) {
+                        st = sx;
 #pragma unroll
-                            for (int i = 0; i < 4 * D; ++i) dred[warp * 4 * MAXD + i] = v[i];
-                        __syncthreads();
-                        if (tid == 0) {
-                            cpx<double> S[MAXD + 1];
-                            S[0] = x0d[padi<PAD>(bf)];
-                            for (int i = 0; i < D; ++i) {
-                                double t[4] = {0.0, 0.0, 0.0, 0.0};
-                                for (int w2 = 0; w2 < NW; ++w2)
-                                    for (int c = 0; c < 4; ++c) t[c] += dred[w2 * 4 * MAXD + 4 * i + c];
-                                S[i + 1] = {t[0] / (double)L - t[2], t[1] / (double)L - t[3]};
-                            }
-                            int mx[MAXD];
-                            cpx<double> ax;
-                            const int sx = classify_values<double, Roots64Split>(
-                                S, g, bf, al, ta, roots64, kn.mag_tol, kn.round_tol,
-                                kn.verify_tol, (double)floor_a, mx, &ax);
-                            res_st[owner] = sx;
-                            res_key[owner] = sx >= 2 ? pack_key(mx, g) : 0;
+                        for (int k = 0; k < MAXD; ++k) m[k] = mx[k];
 #if FPSSFT_GUARD_CALIB == 1
-                            {   // float32 value error against the exact values, in units
-                                // of the bound at kappa = 1
-                                const double unit = (double)Ef / GUARD_KF + U32 * pabs[bf];
-                                double worst = 0.0;
-                                for (int i = 0; i <= D; ++i) {
-                                    const cpx<R> v = spec[padi<PAD>(i * L + bf)];
-                                    worst = fmax(worst, hypot((double)v.re - S[i].re,
-                                                              (double)v.im - S[i].im));
-                                }
-                                atomicMax(&g_guard_calib_max, __float_as_uint((float)(worst / unit)));
-                                atomicAdd(&g_guard_calib_count, 1ull);
-                            }
-#endif
+                        const double unit = (double)Ef / GUARD_KF + U32 * pabs[bf];
+                        double worst = 0.0;
+                        for (int i = 0; i <= D; ++i) {
+                            const cpx<R> v = spec[padi<PAD>(i * L + bf)];
+                            worst = fmax(worst, hypot((double)v.re - S[i].re,
+                                                      (double)v.im - S[i].im));
                         }
-                        __syncthreads();
-                    }
-                    if (need) {
-                        st = res_st[tid];
-                        unpack_key(res_key[tid], g, m);
+                        atomicMax(&g_guard_calib_max, __float_as_uint((float)(worst / unit)));
+                        atomicAdd(&g_guard_calib_count, 1ull);
+#endif
                     }
                 }
             } else {
@@ -483,7 +449,10 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
                     s = found;
                     v = slot_amp[s] + av;  // a pruned slot holds 0: entries.get(f, 0) + a
                 }
-                const bool keep = !(cabs(v) <= (A)kn.amp_prune_tol);
+                const A av_new = cabs(v);
+                const bool keep = !(av_new <= (A)kn.amp_prune_tol);
+                if constexpr (GUARD)  // amp_sum kept incrementally (float64)
+                    d_amp += (keep ? av_new : (A)0) - (fresh ? (A)0 : cabs(slot_amp[s]));
                 slot_amp[s] = keep ? v : cpx<A>{(A)0, (A)0};
                 slot_live[s] = keep;
                 const int u0 = phase_of(m, g, ta);  // driver.py:189-194
@@ -511,13 +480,14 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
         }
 
         // (6) amp_sum and (7) termination                   driver.py:108,196-204
-        A my = (A)0;
-        for (int s = tid; s < n_slots; s += NT)
-            if (slot_live[s]) my += cabs(slot_amp[s]);
-        if constexpr (GUARD)
-            amp_sum = block_sum(my, dred);
-        else
+        if constexpr (GUARD) {
+            amp_sum += block_sum(d_amp, dred);
+        } else {
+            A my = (A)0;
+            for (int s = tid; s < n_slots; s += NT)
+                if (slot_live[s]) my += cabs(slot_amp[s]);
             amp_sum = block_sum(my, rred);
+        }
         const R worst = block_max(resid, rred);  // |S|^2 (float) or |S| (double)
         stall = n_acc > 0 ? 0 : stall + 1;
         const R clean = (R)max((A)kn.energy_floor_abs, (A)kn.residual_stop * amp_sum);

@@ -12,7 +12,8 @@ import ncu_lines as T  # noqa: E402
 
 SRC = {n: open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                             "paper_1711_11407_b200", "csrc", n)).read().split("\n")
-       for n in ("fpssft.cu", "fpssft_device.cuh", "fpssft_team.cuh", "fpssft_large.cuh")}
+       for n in ("fpssft.cu", "fpssft_device.cuh", "fpssft_team.cuh", "fpssft_large.cuh",
+                                "fpssft_guard.cuh", "fpssft_regfft.cuh", "fpssft_synth.cuh")}
 
 
 def region(f, ln):
