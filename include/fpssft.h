@@ -65,7 +65,7 @@ typedef struct fpssft_params {
     int32_t t_max;       /* iteration cap (driver.py:132, default :88-91)  */
     int32_t stall_limit; /* driver.py:44                                    */
     int32_t k_cap;       /* recovered-set capacity per instance (power of 2)*/
-    int32_t precision;   /* FPSSFT_F32 | FPSSFT_F64                         */
+    int32_t precision;   /* FPSSFT_F32 | FPSSFT_F64 | FPSSFT_F32_GUARDED    */
     int32_t mode;        /* FPSSFT_MODE_*: which kernel owns an instance    */
     double mag_tol, verify_tol, round_tol, amp_prune_tol;
     double energy_floor, energy_floor_abs, residual_stop;
@@ -198,6 +198,14 @@ int fpssft_block_threads(const fpssft_shape *shape, int32_t precision);
  * Returns 0, or an error code if the shape/params cannot run. */
 int fpssft_plan(const fpssft_shape *shape, const fpssft_params *params, int32_t *mode,
                 int32_t *threads_per_cta, int32_t *instances_per_cta, size_t *smem_bytes);
+
+/* The plan of fpssft_run_batch_grouped for a batch stored `group` instances
+ * interleaved, with (per_instance_schedules != 0) or without a sched_index:
+ * a shared schedule over an interleaved batch lets the CTA's warps gather
+ * their group's lines together (instances per CTA then divides `group`). */
+int fpssft_plan_batch(const fpssft_shape *shape, const fpssft_params *params, int32_t group,
+                      int32_t per_instance_schedules, int32_t *mode, int32_t *threads_per_cta,
+                      int32_t *instances_per_cta, size_t *smem_bytes);
 
 /* Number of kernel launches fpssft_run_batch issues per call (for accounting). */
 int fpssft_launches_per_batch(void);

@@ -23,7 +23,7 @@ TERM_NAMES = {0: "residual_clean", 1: "stall", 2: "max_iterations", 3: "k_cap_ov
 EXPORTS = ("fpssft_run_batch", "fpssft_run_batch_grouped", "fpssft_line_spectra", "fpssft_gather_lines", "fpssft_dft_forward",
            "fpssft_synthesize",
            "fpssft_decode_spectra", "fpssft_project_onto_bins", "fpssft_smem_bytes",
-           "fpssft_block_threads", "fpssft_plan", "fpssft_launches_per_batch",
+           "fpssft_block_threads", "fpssft_plan", "fpssft_plan_batch", "fpssft_launches_per_batch",
            "fpssft_set_l2_fetch_granularity", "fpssft_get_l2_fetch_granularity", "fpssft_last_error",
            "fpssft_abi_version")
 
@@ -83,6 +83,9 @@ def lib() -> C.CDLL:
         h.fpssft_block_threads.argtypes = [C.POINTER(Shape), I32]
         h.fpssft_plan.argtypes = [C.POINTER(Shape), C.POINTER(Params), C.POINTER(I32),
                                   C.POINTER(I32), C.POINTER(I32), C.POINTER(C.c_size_t)]
+        h.fpssft_plan_batch.argtypes = [C.POINTER(Shape), C.POINTER(Params), I32, I32,
+                                        C.POINTER(I32), C.POINTER(I32), C.POINTER(I32),
+                                        C.POINTER(C.c_size_t)]
         h.fpssft_set_l2_fetch_granularity.argtypes = [I32]
         h.fpssft_get_l2_fetch_granularity.argtypes = []
         h.fpssft_last_error.restype = C.c_char_p

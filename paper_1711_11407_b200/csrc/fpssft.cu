@@ -479,11 +479,11 @@ struct WarpLayout {
 };
 
 __host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, int cs,
-                                                       bool guard = false) {
+                                                       bool guard = false, bool grouped = false) {
     WarpLayout y;
     const int acs = guard ? 16 : cs;  // slot amplitude bytes (complex128 when guarded)
     size_t spec_bytes = (size_t)(D + 1) * (L + L / 16 + 1) * cs;  // room for padi()
-    if (stage16_ok(D, L, cs, 32) && spec_bytes < (size_t)(D + 1) * L * 16)
+    if (!grouped && stage16_ok(D, L, cs, 32) && spec_bytes < (size_t)(D + 1) * L * 16)
         spec_bytes = (size_t)(D + 1) * L * 16;  // 16-byte staging slots (gather_lines_cg16)
     const size_t sort_bytes = 1024 + (size_t)k_cap * 4;
     size_t o = 0;
@@ -544,7 +544,7 @@ __device__ __forceinline__ void hash16_insert(unsigned short *hash, int H, int k
 // (fpssft_guard.cuh) -- float64 slot amplitudes and line-0 transform, guard
 // flags on every float32 decision statistic, flagged bins re-evaluated in
 // float64 by the whole warp.
-template <class R, int LC, int DC, bool GUARD = false>
+template <class R, int LC, int DC, bool GUARD = false, int WG = 0, int KC = 0>
 __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp_kernel(const float2 *__restrict__ cubes,
                                                            long long batch, long long batch_stride,
                                                            Geo g_in, Knobs kn,
@@ -553,6 +553,8 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
                                                            int n_sched, OutPtrs out) {
     static_assert(!GUARD || (sizeof(R) == 4 && LC != 0 && DC != 0),
                   "guarded mode: float32 with a compile-time shape");
+    static_assert(!WG || (sizeof(R) == 4 && LC != 0 && DC != 0 && !GUARD),
+                  "group gather: float32 with a compile-time shape");
     extern __shared__ __align__(16) unsigned char sm[];
     constexpr bool PAD = LC != 0;  // padded spectra layout (see padi)
     using A = typename std::conditional<GUARD, double, R>::type;  // slot amplitude type
@@ -562,7 +564,9 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         g.D = DC;
         g.nlines = DC + 1;
     }
-    const WarpLayout lay = make_warp_layout(g.D, g.L, kn.k_cap, (int)sizeof(cpx<R>), GUARD);
+    // KC: compile-time capacity, so the per-warp layout is constant-folded
+    const int k_cap = KC ? KC : kn.k_cap;
+    const WarpLayout lay = make_warp_layout(g.D, g.L, k_cap, (int)sizeof(cpx<R>), GUARD, WG != 0);
     cpx<R> *roots = (cpx<R> *)sm;
     [[maybe_unused]] cpx<float> *roots_lo = (cpx<float> *)(sm + lay.roots64);
     [[maybe_unused]] const Roots64Split roots64{(const cpx<float> *)roots, roots_lo};
@@ -571,8 +575,12 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     __syncthreads();  // the only block-wide barrier: warps run independently below
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long inst = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
-    if (inst >= batch) return;
+    const long long inst0 = (long long)blockIdx.x * (blockDim.x >> 5);
+    const long long inst = inst0 + warp;
+    // WG: the CTA's warps gather together every iteration, so a warp without
+    // an instance (the batch's last group) stays to the end, inactive
+    if (!WG && inst >= batch) return;
+    const bool has_inst = inst < batch;
     unsigned char *base = sm + lay.roots + (size_t)warp * lay.per_warp;
     cpx<R> *spec = (cpx<R> *)(base + lay.spec);
     cpx<A> *slot_amp = (cpx<A> *)(base + lay.slot_amp);
@@ -587,12 +595,16 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
 
     const int L = g.L, D = g.D, nl = g.nlines, H = lay.H;
     const float2 *cube = cube_base(cubes, (long long)inst, batch_stride, kn.group);
-    int sidx = sched_index ? sched_index[inst] : 0;
+    // WG: the group shares schedule 0 (the launcher passes no sched_index)
+    int sidx = (sched_index && !WG && has_inst) ? sched_index[inst] : 0;
     const bool sched_ok = sidx >= 0 && sidx < n_sched;
     if (!sched_ok) sidx = 0;
     const int *sched = schedule + (long long)sidx * kn.t_max * 2 * D;
     const R mag_tol = (R)kn.mag_tol, round_tol = (R)kn.round_tol, verify_tol = (R)kn.verify_tol;
     const unsigned lt_mask = (1u << lane) - 1u;
+    [[maybe_unused]] const float2 *gbase =
+        cube_base(cubes, inst0, batch_stride, kn.group);  // the CTA's first member
+    [[maybe_unused]] cpx<float> *spec0 = (cpx<float> *)(sm + lay.roots + lay.spec);
 
     for (int h = lane; h < H; h += 32) hash[h] = HASH_EMPTY;
     __syncwarp();
@@ -609,24 +621,52 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         nal[k] = k < D ? sched[k] : 0;
         nta[k] = k < D ? sched[D + k] : 0;
     }
-    for (int it = 0; it < kn.t_max && term != -1; ++it) {
+    bool active = sched_ok && has_inst;
+    for (int it = 0; it < kn.t_max; ++it) {
         int al[MAXD], ta[MAXD];
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) {
             al[k] = nal[k];
             ta[k] = nta[k];
         }
+        if constexpr (WG != 0) {
+            // (1) group gather: loads in flight across the barrier that waits
+            // for every warp to finish the previous iteration with its spectra
+            const bool lines_ok = line_params_ok(g, al, ta);
+            GroupGather<LC, DC, WG> gg;
+            if (lines_ok) gg.load(gbase, g, al, ta, threadIdx.x);
+            if (!__syncthreads_or(active && lines_ok)) {
+                if (active) term = -1;  // invalid schedule: the whole group stops
+                break;
+            }
+            gg.store(spec0, (int)(lay.per_warp / sizeof(cpx<float>)), threadIdx.x);
+            if (it + 1 < kn.t_max) {
+#pragma unroll
+                for (int k = 0; k < MAXD; ++k) {
+                    nal[k] = k < D ? sched[(long long)(it + 1) * 2 * D + k] : 0;
+                    nta[k] = k < D ? sched[(long long)(it + 1) * 2 * D + D + k] : 0;
+                }
+            }
+            __syncthreads();
+        } else if (!active) {
+            break;
+        }
+        do {  // one iteration of this warp's instance; `break` ends its recovery
+        if (!active) break;
         if (!line_params_ok(g, al, ta)) {
             term = -1;
+            active = false;
             break;
         }
         it_run = it + 1;
 
         // (1) gather + (2) DFT of the D+1 lines           driver.py:146-154
-        R my_energy;
+        R my_energy = (R)0;
         bool staged = false;
         unsigned par = 0, dup = 0;
-        if constexpr (sizeof(R) == 4) {
+        if constexpr (WG != 0) {
+            // the group gather above filled the spectra
+        } else if constexpr (sizeof(R) == 4) {
             bool reg_gather = false;
             // register gather for short lines (config 3: 1.2% faster), cp.async
             // for L >= 256 (config 2: 1% faster) -- measured, profiles/README.md
@@ -784,7 +824,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         __syncwarp();
         bool overflow = false;
         int n_cand_x = 0;
-        [[maybe_unused]] A d_amp = (A)0;  // GUARD: this lane's change of amp_sum
+        A d_amp = (A)0;  // this lane's change of amp_sum
         for (int c0 = 0; c0 < n_cand; c0 += 32) {
             const int ce = c0 + lane < n_cand ? cand[c0 + lane] : -1;
             const int b = ce >= 0 ? (ce & ~(int)CAND_FLAG) : -1;
@@ -853,7 +893,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
                 found = hash16_find(hash, slot_key, H, key);
             }
             const unsigned fresh = __ballot_sync(FULL, st == 2 && found < 0);
-            if (n_slots + __popc(fresh) > kn.k_cap) {
+            if (n_slots + __popc(fresh) > k_cap) {
                 overflow = true;
                 break;
             }
@@ -878,8 +918,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
                 }
                 const A av_new = cabs(v);
                 const bool keep = !(av_new <= (A)kn.amp_prune_tol);
-                if constexpr (GUARD)  // amp_sum kept incrementally (float64)
-                    d_amp += (keep ? av_new : (A)0) - (found < 0 ? (A)0 : cabs(slot_amp[s]));
+                d_amp += (keep ? av_new : (A)0) - (found < 0 ? (A)0 : cabs(slot_amp[s]));
                 slot_amp[s] = keep ? v : cpx<A>{(A)0, (A)0};
                 slot_live[s] = keep;
                 const int u0 = phase_of(m, g, ta);  // driver.py:189-194
@@ -900,19 +939,14 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
                 st[1] = 0;
                 st[2] = n_cand;
             }
+            active = false;
             break;
         }
         __syncwarp();
 
         // (6) amp_sum = sum |a| over the recovered set        driver.py:108
-        if constexpr (GUARD) {
-            amp_sum += __shfl_sync(FULL, warp_sum(d_amp), 0);
-        } else {
-            A my = (A)0;
-            for (int s = lane; s < n_slots; s += 32)
-                if (slot_live[s]) my += cabs(slot_amp[s]);
-            amp_sum = __shfl_sync(FULL, warp_sum(my), 0);
-        }
+        //     kept incrementally: every merge adds |new| - |old| of its slot
+        amp_sum += __shfl_sync(FULL, warp_sum(d_amp), 0);
         stall = n_acc > 0 ? 0 : stall + 1;
 
         // (7) termination                                     driver.py:196-204
@@ -928,13 +962,17 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         __syncwarp();
         if (is_clean) {
             term = FPSSFT_TERM_RESIDUAL_CLEAN;
+            active = false;
             break;
         }
         if (stall >= kn.stall_limit) {
             term = FPSSFT_TERM_STALL;
+            active = false;
             break;
         }
+        } while (0);
     }
+    if (!has_inst) return;  // (WG: a padding warp of the batch's last group)
 
     // ---- RecoveryReport: live entries sorted by packed key (= lexicographic).
     // Counting sort on the key's top 8 bits (shared-memory histogram, warp
@@ -997,11 +1035,11 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         const int s = sslot[r];
         int m[MAXD];
         unpack_key(slot_key[s], g, m);
-        int *fo = out.freqs + (inst * kn.k_cap + r) * D;
+        int *fo = out.freqs + (inst * k_cap + r) * D;
 #pragma unroll
         for (int k = 0; k < MAXD; ++k)
             if (k < D) fo[k] = m[k];
-        double *ao = out.amps + (inst * kn.k_cap + r) * 2;
+        double *ao = out.amps + (inst * k_cap + r) * 2;
         ao[0] = (double)slot_amp[s].re;
         ao[1] = (double)slot_amp[s].im;
     }
@@ -1641,18 +1679,21 @@ int check_launch(const char *where) {
 // The warp kernel instance for a shape: compile-time specialisations for the
 // benchmark shapes, else the runtime-shape version.
 template <class R>
-const void *warp_kernel_for_t(const Geo &g) {
+const void *warp_kernel_for_t(const Geo &g, int k_cap) {
+    if (g.off32 && g.D == 2 && g.L == 256 && k_cap == 128 && sizeof(R) == 4)  // config 2
+        return (const void *)recover_warp_kernel<R, 256, 2, false, 0, 128>;
     if (g.off32 && g.D == 2 && g.L == 256) return (const void *)recover_warp_kernel<R, 256, 2>;
     if (g.off32 && g.D == 2 && g.L == 512) return (const void *)recover_warp_kernel<R, 512, 2>;
     if (g.off32 && g.D == 3 && g.L == 64) return (const void *)recover_warp_kernel<R, 64, 3>;
     return (const void *)recover_warp_kernel<R, 0, 0>;
 }
-const void *warp_kernel_for(const Geo &g, int precision) {
+const void *warp_kernel_for(const Geo &g, int precision, int k_cap) {
     if (precision == FPSSFT_F32_GUARDED)  // guarded float32: the noisy config-3 shape
         return g.off32 && g.D == 3 && g.L == 64
                    ? (const void *)recover_warp_kernel<float, 64, 3, true>
                    : nullptr;
-    return precision == FPSSFT_F64 ? warp_kernel_for_t<double>(g) : warp_kernel_for_t<float>(g);
+    return precision == FPSSFT_F64 ? warp_kernel_for_t<double>(g, k_cap)
+                                   : warp_kernel_for_t<float>(g, k_cap);
 }
 
 // The compile-time team kernel for a shape (one CTA of *nt threads per
@@ -1720,17 +1761,38 @@ struct LaunchPlan {
 // CTA per instance.  `g` receives the FFT plan of the chosen mode.
 // Registers per thread of the warp kernel chosen for (precision, L, D): the
 // compiled value when a device is present, else the launch-bounds cap.
-const void *warp_kernel_for(const Geo &g, int precision);
+const void *warp_kernel_for(const Geo &g, int precision, int k_cap);
 
-int warp_kernel_regs(const Geo &g, int precision) {
+int warp_kernel_regs(const Geo &g, int precision, int k_cap) {
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, warp_kernel_for(g, precision)) == cudaSuccess && fa.numRegs > 0)
+    if (cudaFuncGetAttributes(&fa, warp_kernel_for(g, precision, k_cap)) == cudaSuccess &&
+        fa.numRegs > 0)
         return fa.numRegs;
     cudaGetLastError();  // no device: clear the error, assume the cap
     return precision == FPSSFT_F64 ? 128 : 80;
 }
 
-int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) {
+// The group-gather warp kernel (GroupGather: WG warps of one CTA own WG
+// consecutive members of an interleave group and gather their shared lines
+// once): float32, a compile-time shape, a batch stored interleaved with
+// kn.group a multiple of WG, and one schedule for the whole batch.
+#ifndef FPSSFT_GROUP_WG
+#define FPSSFT_GROUP_WG 8  // warps (= interleaved instances) per group-gather CTA; 0 = off
+#endif
+const void *group_kernel_for(const Geo &g, int precision, int group, int k_cap) {
+    if (!FPSSFT_GROUP_WG || precision != FPSSFT_F32 || !g.off32 || group < FPSSFT_GROUP_WG ||
+        group % FPSSFT_GROUP_WG)
+        return nullptr;
+#if FPSSFT_GROUP_WG
+    if (g.D == 2 && g.L == 256)
+        return k_cap == 128 ? (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_WG, 128>
+                            : (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_WG>;
+#endif
+    return nullptr;
+}
+
+int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp,
+              bool shared_sched = false) {
     const int cs = precision == FPSSFT_F64 ? 16 : 8;
     const bool guard = precision == FPSSFT_F32_GUARDED;
     // candidate 1: warp per instance
@@ -1740,10 +1802,10 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
     if (want != FPSSFT_MODE_CTA) {
         bool ok = g.key_bits_ <= 31 && kn.k_cap <= 32768 && (long long)g.nlines * g.L <= 2048 &&
                   (g.L & (g.L - 1)) == 0 && plan_fft(&gw, g.nlines, precision, 32) > 0 &&
-                  (!guard || warp_kernel_for(g, precision) != nullptr);
+                  (!guard || warp_kernel_for(g, precision, kn.k_cap) != nullptr);
         if (ok) {
             const WarpLayout wl = make_warp_layout(g.D, g.L, kn.k_cap, cs, guard);
-            const int regs = (warp_kernel_regs(gw, precision) + 7) / 8 * 8;
+            const int regs = (warp_kernel_regs(gw, precision, kn.k_cap) + 7) / 8 * 8;
             const long long reg_warps = 65536 / (regs * 32);
             int best_w = 0;
             for (int w : {8, 7, 6, 5, 4, 3, 2, 1}) {
@@ -1761,7 +1823,15 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp) 
             if (best_w)
                 wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * best_w, best_w,
                                 wl.roots + (size_t)best_w * wl.per_warp,
-                                warp_kernel_for(gw, precision)};
+                                warp_kernel_for(gw, precision, kn.k_cap)};
+            const void *gk =
+                shared_sched ? group_kernel_for(gw, precision, kn.group, kn.k_cap) : nullptr;
+            if (best_w && gk) {
+                const WarpLayout gl = make_warp_layout(g.D, g.L, kn.k_cap, cs, false, true);
+                const size_t smem = gl.roots + (size_t)FPSSFT_GROUP_WG * gl.per_warp;
+                if ((long long)smem <= SMEM_PER_CTA)
+                    wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * FPSSFT_GROUP_WG, FPSSFT_GROUP_WG, smem, gk};
+            }
         }
         if (want == FPSSFT_MODE_WARP) {
             if (!warp_warps)
@@ -1862,7 +1932,7 @@ int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
     LaunchPlan lp;
     const int prec = sizeof(R) == 8 ? FPSSFT_F64
                                     : (kn.guard_coef > 0 ? FPSSFT_F32_GUARDED : FPSSFT_F32);
-    int rc = make_plan(g, kn, prec, want_mode, &lp);
+    int rc = make_plan(g, kn, prec, want_mode, &lp, sched_index == nullptr);
     if (rc != FPSSFT_OK) return rc;
     cudaError_t e;
     if (lp.mode == FPSSFT_MODE_CTA && lp.kernel) {  // compile-time team kernel
@@ -2102,14 +2172,24 @@ int fpssft_synthesize(const int32_t *freqs, const double *amps, const int32_t *c
 
 int fpssft_plan(const fpssft_shape *shape, const fpssft_params *params, int32_t *mode,
                 int32_t *threads_per_cta, int32_t *instances_per_cta, size_t *smem_bytes) {
+    return fpssft_plan_batch(shape, params, 1, 0, mode, threads_per_cta, instances_per_cta,
+                             smem_bytes);
+}
+
+int fpssft_plan_batch(const fpssft_shape *shape, const fpssft_params *params, int32_t group,
+                      int32_t per_instance_schedules, int32_t *mode, int32_t *threads_per_cta,
+                      int32_t *instances_per_cta, size_t *smem_bytes) {
     Geo g;
     Knobs kn;
     int rc;
     if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
     if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
+    if (group < 1 || group > 64) return fail(FPSSFT_EINVAL, "group must be in [1, 64]");
+    kn.group = group;
     LaunchPlan lp;
     const int prec = effective_precision(g, kn, params->precision, params->mode);
-    if ((rc = make_plan(g, kn, prec, params->mode, &lp)) != FPSSFT_OK) return rc;
+    if ((rc = make_plan(g, kn, prec, params->mode, &lp, !per_instance_schedules)) != FPSSFT_OK)
+        return rc;
     if (mode) *mode = lp.mode;
     if (threads_per_cta) *threads_per_cta = lp.threads;
     if (instances_per_cta) *instances_per_cta = lp.per_cta;

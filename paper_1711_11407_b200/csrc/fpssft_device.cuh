@@ -111,6 +111,13 @@ __device__ __forceinline__ const T *cube_base(const T *cubes, long long inst,
     return cubes + (inst / group) * group_stride + (inst % group);
 }
 
+// v mod n for v in [-n, 2n) without division: the rounded phase ratio
+// rint(N angle / 2 pi) lies in [-N/2, N/2] (decoder.py:153-158).
+__device__ __forceinline__ int wrap_index(int v, int n) {
+    v = v < 0 ? v + n : v;
+    return v >= n ? v - n : v;
+}
+
 // a mod d without division (Lemire): valid for any 32-bit a, d >= 1.
 __device__ __forceinline__ unsigned fastmod(unsigned a, unsigned long long M, unsigned d) {
     return (unsigned)__umul64hi(M * (unsigned long long)a, (unsigned long long)d);
@@ -1118,8 +1125,7 @@ __device__ __forceinline__ int classify_values(const cpx<R> *s, const Geo &g, in
             R raw = (R)g.N[k] * theta / two_pi;
             R near = rint(raw);
             ok = ok && (fabs(raw - near) <= round_tol);
-            int mk = ((int)near) % g.N[k];
-            m[k] = mk < 0 ? mk + g.N[k] : mk;
+            m[k] = wrap_index((int)near, g.N[k]);
         }
     }
     if (!ok) return 1;
@@ -1176,8 +1182,7 @@ __device__ __forceinline__ int decode_candidate(const cpx<R> *spec, const Geo &g
                                    : (R)g.N[k] * theta * (R)0.15915494309189533577;
             R near = rint(raw);
             ok = ok && (fabs(raw - near) <= round_tol);
-            int mk = ((int)near) % g.N[k];
-            m[k] = mk < 0 ? mk + g.N[k] : mk;
+            m[k] = wrap_index((int)near, g.N[k]);
         }
     }
     if (!ok) return 1;

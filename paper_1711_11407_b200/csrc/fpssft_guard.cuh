@@ -108,8 +108,7 @@ __device__ __forceinline__ int decode_candidate_guarded(const cpx<float> *spec, 
             const float raw = (float)g.N[k] * theta * inv2pi;
             const float near = rintf(raw);
             const float d = fabsf(raw - near);
-            const int mk = ((int)near) % g.N[k];
-            m[k] = mk < 0 ? mk + g.N[k] : mk;
+            m[k] = wrap_index((int)near, g.N[k]);
             // angle error <= asin(E/|S_k+1|) + asin(E/|S_0|) (+ atan2f's own);
             // asin(x) <= 1.02 x for x <= 1/4, else no useful bound
             const float dth = (mg[k + 1] > 4.f * Eb && mg[0] > 4.f * Eb)
@@ -123,8 +122,7 @@ __device__ __forceinline__ int decode_candidate_guarded(const cpx<float> *spec, 
                 m_unsure |= 0x80u;  // phase too uncertain to bound m
             } else if (d >= 0.5f - draw) {
                 m_unsure |= 1u << k;
-                const int ak = ((int)near + (raw > near ? 1 : -1)) % g.N[k];
-                m_alt[k] = ak < 0 ? ak + g.N[k] : ak;
+                m_alt[k] = wrap_index((int)near + (raw > near ? 1 : -1), g.N[k]);
             }
         }
     }

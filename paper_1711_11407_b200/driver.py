@@ -305,7 +305,7 @@ class BatchRunner:
         self.prec = _precision_code(precision, config)
         self._shape_c = N.make_shape(shape.dims)
         self._params_c = _params(config, self.t_max, self.k_cap, self.prec, mode)
-        self.plan = launch_plan(shape, self._params_c)
+        self.plan = launch_plan(shape, self._params_c, self.group, self.sched_index is not None)
         self.out = allocate_outputs(self.batch, shape, self.k_cap, self.t_max, self.device,
                                     iter_stats)
         o = self.out
@@ -375,15 +375,17 @@ def interleave(cubes, group: int = 8):
     return out
 
 
-def launch_plan(shape: CubeShape, params: N.Params) -> dict:
-    """The kernel/launch shape ``fpssft_run_batch`` will use (raises if the
-    shape cannot run)."""
+def launch_plan(shape: CubeShape, params: N.Params, group: int = 1,
+                per_instance_schedules: bool = False) -> dict:
+    """The kernel/launch shape ``fpssft_run_batch_grouped`` will use for a
+    batch interleaved by ``group`` (raises if the shape cannot run)."""
     import ctypes
 
     mode, thr, per = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
     smem = ctypes.c_size_t()
-    N.check(N.lib().fpssft_plan(C_ref(N.make_shape(shape.dims)), C_ref(params), C_ref(mode),
-                                C_ref(thr), C_ref(per), C_ref(smem)))
+    N.check(N.lib().fpssft_plan_batch(C_ref(N.make_shape(shape.dims)), C_ref(params), int(group),
+                                      int(bool(per_instance_schedules)), C_ref(mode), C_ref(thr),
+                                      C_ref(per), C_ref(smem)))
     return {"mode": {N.MODE_CTA: "cta", N.MODE_WARP: "warp"}[mode.value],
             "threads_per_cta": thr.value, "instances_per_cta": per.value,
             "smem_bytes": smem.value}
