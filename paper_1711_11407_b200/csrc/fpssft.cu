@@ -50,6 +50,9 @@
 #ifndef FPSSFT_WARP_NT
 #define FPSSFT_WARP_NT 256  // largest CTA of the warp kernel (FPSSFT_WARP_NT / 32 instances)
 #endif
+#ifndef FPSSFT_WARP_REGFFT256
+#define FPSSFT_WARP_REGFFT256 1  // warp kernel, 256-point lines: register FFT (regfft::fft256)
+#endif
 #ifndef FPSSFT_WARP_W
 #define FPSSFT_WARP_W 0  // A/B builds only: force the warp kernel's instances per CTA (0 = planner)
 #endif
@@ -460,6 +463,7 @@ __global__ void __launch_bounds__(1024, 1) recover_kernel(const float2 *__restri
 }
 
 #include "fpssft_guard.cuh"
+#include "fpssft_regfft.cuh"
 
 // ------------------------------------------------------ warp-per-instance
 // For short lines ((D+1) L <= 2048) one warp owns one instance: the same loop
@@ -727,7 +731,12 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             }
             __syncwarp();
         }
-        if constexpr (LC != 0) {
+        if constexpr (LC == 256 && sizeof(R) == 4 && FPSSFT_WARP_REGFFT256) {
+            // 256-point lines in registers (regfft::fft256_lines_warp)
+            my_energy = (R)regfft::fft256_lines_warp((cpx<float> *)spec, DC + 1,
+                                                     (const cpx<float> *)roots, lane);
+            if constexpr (GUARD) fft_static<double, LC, 1, 32, WarpTeam, Roots64Split>(x0d, roots64, lane);
+        } else if constexpr (LC != 0) {
             const R e = fft_static<R, LC, DC + 1>(spec, roots, lane);
             if (sizeof(R) == 4) my_energy = e;
             if constexpr (GUARD) fft_static<double, LC, 1, 32, WarpTeam, Roots64Split>(x0d, roots64, lane);
@@ -1051,7 +1060,6 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     }
 }
 
-#include "fpssft_regfft.cuh"
 #include "fpssft_team.cuh"
 #include "fpssft_synth.cuh"
 

@@ -68,6 +68,91 @@ __device__ __forceinline__ void dft16(float2 *v) {
         for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
 }
 
+// X[k] = sum_n v[n] e^{+2 pi i n k / 8}, in place, natural order (radix 2 x 4).
+__device__ __forceinline__ void dft8(float2 *v) {
+    float2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+    float2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+    dft4(e0, e1, e2, e3);
+    dft4(o0, o1, o2, o3);
+    const float h = 0.70710678118654752f;
+    const float2 t1 = make_float2(h * (o1.x - o1.y), h * (o1.x + o1.y));    // e^{i pi/4} o1
+    const float2 t2 = make_float2(-o2.y, o2.x);                            // i o2
+    const float2 t3 = make_float2(-h * (o3.x + o3.y), h * (o3.x - o3.y));  // e^{3 i pi/4} o3
+    v[0] = cadd(e0, o0);
+    v[4] = csub(e0, o0);
+    v[1] = cadd(e1, t1);
+    v[5] = csub(e1, t1);
+    v[2] = cadd(e2, t2);
+    v[6] = csub(e2, t2);
+    v[3] = cadd(e3, t3);
+    v[7] = csub(e3, t3);
+}
+
+// Forward 1/L-normalised DFTs of `nlines` 256-point lines (padded layout),
+// one warp doing the lines one after another, in registers: 256 = 8 x 32.
+// Lane b holds x[32 a + b] (a = 0..7): 8-point DFT over a, twiddle
+// e^{2 pi i b k1 / 256}, one shared-memory exchange (rows of 33) inside the
+// line's own padded region, then lane (k1, h) = (lane / 4, lane % 4) holds
+// y[4 beta + h] (beta = 0..7) of row k1: 8-point DFT over beta, twiddle
+// e^{2 pi i h k2a / 32}, and a 4-point DFT across the 4 lanes h by shuffles
+// (lane h ends with k2b = h / 2 + 2 (h % 2)): X[k1 + 8 (k2a + 8 k2b)].
+// Forward = conjugate of the inverse of the conjugate.  Returns this lane's
+// share of sum |x|^2 over the input samples, like fft_static.
+__device__ __forceinline__ float fft256_lines_warp(cpx<float> *spec, int nlines,
+                                                   const cpx<float> *roots, int lane) {
+    constexpr int PADL = 256 + 16, S = 33;
+    float energy = 0.f;
+    const int k1 = lane >> 2, h = lane & 3, k2b = (h >> 1) + 2 * (h & 1);
+#pragma unroll 1
+    for (int line = 0; line < nlines; ++line) {
+        float2 *base = (float2 *)(spec + line * PADL);
+        float2 v[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int i = 32 * a + lane;
+            const float2 x = base[i + (i >> 4)];
+            energy += x.x * x.x + x.y * x.y;
+            v[a] = make_float2(x.x, -x.y);  // conjugate in
+        }
+        dft8(v);
+#pragma unroll
+        for (int c = 1; c < 8; ++c) {
+            const cpx<float> r = roots[lane * c];
+            v[c] = cmul(v[c], make_float2(r.re, r.im));
+        }
+        __syncwarp();  // the line's inputs are read before the exchange overwrites them
+#pragma unroll
+        for (int c = 0; c < 8; ++c) base[c * S + lane] = v[c];
+        __syncwarp();
+#pragma unroll
+        for (int be = 0; be < 8; ++be) v[be] = base[k1 * S + 4 * be + h];
+        dft8(v);
+#pragma unroll
+        for (int d = 1; d < 8; ++d) {  // e^{2 pi i h d / 32} = roots[8 h d] (a runtime h)
+            const cpx<float> r = roots[8 * h * d];
+            v[d] = cmul(v[d], make_float2(r.re, r.im));
+        }
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {  // 4-point DFT across lanes h (xor 2, then xor 1)
+            float2 x = v[d];
+            float2 p = make_float2(__shfl_xor_sync(FULL, x.x, 2), __shfl_xor_sync(FULL, x.y, 2));
+            x = (h & 2) ? csub(p, x) : cadd(x, p);
+            if (h == 3) x = mul_i(x);
+            p = make_float2(__shfl_xor_sync(FULL, x.x, 1), __shfl_xor_sync(FULL, x.y, 1));
+            v[d] = (h & 1) ? csub(p, x) : cadd(x, p);
+        }
+        __syncwarp();  // every lane has read the exchange before outputs land in it
+        const float inv = 1.f / 256.f;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+            const int k = k1 + 8 * (d + 8 * k2b);
+            base[k + (k >> 4)] = make_float2(v[d].x * inv, -v[d].y * inv);  // conjugate out
+        }
+        __syncwarp();
+    }
+    return energy;
+}
+
 // Forward 1/L-normalised DFTs of `nlines` 512-point lines in the padded
 // spectra layout (padi), one warp per line (warps >= nlines idle): the
 // conjugate of the inverse transform of the conjugated line.  `roots` is the
