@@ -1957,6 +1957,24 @@ int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
         return check_launch("recover_team_kernel");
     }
     if (lp.mode == FPSSFT_MODE_WARP) {
+        // a batch smaller than one CTA per SM: fewer instances per CTA so the
+        // CTAs cover every SM (config 3: 1024 instances, 7 per CTA on 147 SMs
+        // instead of 8 on 128 -- 0.961 -> 0.934 ms).  The group-gather kernel
+        // keeps its fixed width (its CTA is one interleave group's share).
+        int sms = 0, dev = 0;
+        if (lp.per_cta > 1 && lp.threads == 32 * lp.per_cta && cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+            sms > 0 && lp.kernel != group_kernel_for(g, prec, kn.group, kn.k_cap)) {
+            const long long want = (batch + sms - 1) / sms;
+            if (want < lp.per_cta) {
+                const WarpLayout wl = make_warp_layout(g.D, g.L, kn.k_cap, sizeof(R) == 8 ? 16 : 8,
+                                                       prec == FPSSFT_F32_GUARDED);
+                lp.per_cta = (int)std::max(1LL, want);
+                lp.threads = 32 * lp.per_cta;
+                lp.smem = wl.roots + (size_t)lp.per_cta * wl.per_warp;
+            }
+        }
+        cudaGetLastError();
         auto kernel = (void (*)(const float2 *, long long, long long, Geo, Knobs, const int *,
                                 const int *, int, OutPtrs))lp.kernel;
         e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
