@@ -47,6 +47,12 @@
 #ifndef SYNTH_NT
 #define SYNTH_NT 256
 #endif
+#ifndef FPSSFT_WARP_FFT_JOINT
+#define FPSSFT_WARP_FFT_JOINT 0  // A/B: warp kernel, 256-point lines transformed together (measured slower: spills)
+#endif
+#ifndef FPSSFT_GROUP_PF
+#define FPSSFT_GROUP_PF 0  // group kernel: L2-prefetch iteration t+1 during t for t + 1 < this
+#endif
 #ifndef FPSSFT_WARP_NT
 #define FPSSFT_WARP_NT 256  // largest CTA of the warp kernel (FPSSFT_WARP_NT / 32 instances)
 #endif
@@ -542,6 +548,35 @@ __device__ __forceinline__ void hash16_insert(unsigned short *hash, int H, int k
         h = (h + 1) & (unsigned)(H - 1);
 }
 
+// FPSSFT_PHASE_CLOCK builds: per-phase clock cycles of the warp kernel
+// (lane 0 of every warp), summed over the launch (fpssft_debug_phase_cycles)
+#ifndef FPSSFT_PHASE_CLOCK
+#define FPSSFT_PHASE_CLOCK 0
+#endif
+#if FPSSFT_PHASE_CLOCK
+__device__ unsigned long long g_phase_cycles[16];
+#define PCLK_DECL() long long pclk_t = clock64(); long long pclk_acc[9] = {0}; int pclk_last = 8
+#define PCLK(n) do { const long long t_ = clock64(); pclk_acc[pclk_last] += t_ - pclk_t; pclk_t = t_; pclk_last = (n); } while (0)
+#define PCLK_FLUSH() do { if (lane == 0) for (int i_ = 0; i_ < 9; ++i_) atomicAdd(&g_phase_cycles[i_], (unsigned long long)pclk_acc[i_]); } while (0)
+#else
+#define PCLK_DECL() do {} while (0)
+#define PCLK(n) do {} while (0)
+#define PCLK_FLUSH() do {} while (0)
+#endif
+
+// Named barrier `id` over `n` threads (a gather team), plain and OR-reducing.
+__device__ __forceinline__ void team_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ bool team_bar_or(int id, int n, bool p) {
+    int r;
+    asm volatile(
+        "{\n\t.reg .pred pi, po;\n\tsetp.ne.s32 pi, %1, 0;\n\t"
+        "bar.red.or.pred po, %2, %3, pi;\n\tselp.s32 %0, 1, 0, po;\n\t}"
+        : "=r"(r) : "r"((int)p), "r"(id), "r"(n) : "memory");
+    return r != 0;
+}
+
 // LC / DC: compile-time line length and dimensionality (0 = runtime), so the
 // benchmark shapes get fully unrolled gathers, FFTs and bin loops.  GUARD
 // (float32, compile-time shapes): the float64 reference's decisions
@@ -579,8 +614,15 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     __syncthreads();  // the only block-wide barrier: warps run independently below
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long inst0 = (long long)blockIdx.x * (blockDim.x >> 5);
-    const long long inst = inst0 + warp;
+    // WG: the CTA's warps form teams of WG consecutive instances (members of
+    // one interleave group); a team gathers its members' shared line samples
+    // together and meets at its own barrier (the CTA-wide one when the team is
+    // the whole CTA, else named barrier 1 + team)
+    [[maybe_unused]] const int team = WG ? warp / WG : 0;
+    [[maybe_unused]] const int team_tid = WG ? (int)threadIdx.x - team * WG * 32 : 0;
+    [[maybe_unused]] const bool team_is_cta = WG && (int)blockDim.x == WG * 32;
+    const long long inst0 = (long long)blockIdx.x * (blockDim.x >> 5) + (WG ? team * WG : 0);
+    const long long inst = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
     // WG: the CTA's warps gather together every iteration, so a warp without
     // an instance (the batch's last group) stays to the end, inactive
     if (!WG && inst >= batch) return;
@@ -608,7 +650,8 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     const unsigned lt_mask = (1u << lane) - 1u;
     [[maybe_unused]] const float2 *gbase =
         cube_base(cubes, inst0, batch_stride, kn.group);  // the CTA's first member
-    [[maybe_unused]] cpx<float> *spec0 = (cpx<float> *)(sm + lay.roots + lay.spec);
+    [[maybe_unused]] cpx<float> *spec0 =
+        (cpx<float> *)(sm + lay.roots + (WG ? (size_t)team * WG : 0) * lay.per_warp + lay.spec);
 
     for (int h = lane; h < H; h += 32) hash[h] = HASH_EMPTY;
     __syncwarp();
@@ -626,6 +669,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         nta[k] = k < D ? sched[D + k] : 0;
     }
     bool active = sched_ok && has_inst;
+    PCLK_DECL();
     for (int it = 0; it < kn.t_max; ++it) {
         int al[MAXD], ta[MAXD];
 #pragma unroll
@@ -637,13 +681,17 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             // (1) group gather: loads in flight across the barrier that waits
             // for every warp to finish the previous iteration with its spectra
             const bool lines_ok = line_params_ok(g, al, ta);
+            PCLK(0);
             GroupGather<LC, DC, WG> gg;
-            if (lines_ok) gg.load(gbase, g, al, ta, threadIdx.x);
-            if (!__syncthreads_or(active && lines_ok)) {
-                if (active) term = -1;  // invalid schedule: the whole group stops
+            if (lines_ok) gg.load(gbase, g, al, ta, team_tid);
+            const bool any = team_is_cta ? __syncthreads_or(active && lines_ok)
+                                         : team_bar_or(1 + team, WG * 32, active && lines_ok);
+            if (!any) {
+                if (active) term = -1;  // invalid schedule: the whole team stops
                 break;
             }
-            gg.store(spec0, (int)(lay.per_warp / sizeof(cpx<float>)), threadIdx.x);
+            PCLK(1);
+            gg.store(spec0, (int)(lay.per_warp / sizeof(cpx<float>)), team_tid);
             if (it + 1 < kn.t_max) {
 #pragma unroll
                 for (int k = 0; k < MAXD; ++k) {
@@ -651,7 +699,14 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
                     nta[k] = k < D ? sched[(long long)(it + 1) * 2 * D + D + k] : 0;
                 }
             }
-            __syncthreads();
+            if (team_is_cta) __syncthreads();
+            else team_bar(1 + team, WG * 32);
+            // L2 prefetch of the next iteration's segments (one request per
+            // segment) while this one computes: only for the leading
+            // iterations nearly every instance runs (FPSSFT_GROUP_PF)
+            if (FPSSFT_GROUP_PF && it + 1 < FPSSFT_GROUP_PF && it + 1 < kn.t_max &&
+                line_params_ok(g, nal, nta))
+                gg.prefetch_l2(gbase, g, nal, nta, team_tid);
         } else if (!active) {
             break;
         }
@@ -731,10 +786,15 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             }
             __syncwarp();
         }
+        PCLK(2);
         if constexpr (LC == 256 && sizeof(R) == 4 && FPSSFT_WARP_REGFFT256) {
             // 256-point lines in registers (regfft::fft256_lines_warp)
-            my_energy = (R)regfft::fft256_lines_warp((cpx<float> *)spec, DC + 1,
-                                                     (const cpx<float> *)roots, lane);
+            if constexpr (FPSSFT_WARP_FFT_JOINT && DC + 1 <= 3)
+                my_energy = (R)regfft::fft256_lines_joint<DC + 1>((cpx<float> *)spec,
+                                                                  (const cpx<float> *)roots, lane);
+            else
+                my_energy = (R)regfft::fft256_lines_warp((cpx<float> *)spec, DC + 1,
+                                                         (const cpx<float> *)roots, lane);
             if constexpr (GUARD) fft_static<double, LC, 1, 32, WarpTeam, Roots64Split>(x0d, roots64, lane);
         } else if constexpr (LC != 0) {
             const R e = fft_static<R, LC, DC + 1>(spec, roots, lane);
@@ -742,6 +802,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             if constexpr (GUARD) fft_static<double, LC, 1, 32, WarpTeam, Roots64Split>(x0d, roots64, lane);
         } else
             fft_lines_warp<R>(spec, nl, g, roots, lane);
+        PCLK(3);
         R noise_floor = (R)0;
         [[maybe_unused]] float Ef = 0.f;  // GUARD: transform part of the error bound
         if constexpr (GUARD) {
@@ -800,6 +861,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             __syncwarp();
         }
 
+        PCLK(4);
         // (4) classify + (5) merge, 32 bins at a time in ascending order
         const A floor_a = max(max((A)kn.energy_floor_abs, (A)kn.energy_floor * amp_sum),
                               (A)noise_floor);
@@ -831,6 +893,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             n_cand += __popc(msk);
         }
         __syncwarp();
+        PCLK(5);
         bool overflow = false;
         int n_cand_x = 0;
         A d_amp = (A)0;  // this lane's change of amp_sum
@@ -953,6 +1016,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         }
         __syncwarp();
 
+        PCLK(6);
         // (6) amp_sum = sum |a| over the recovered set        driver.py:108
         //     kept incrementally: every merge adds |new| - |old| of its slot
         amp_sum += __shfl_sync(FULL, warp_sum(d_amp), 0);
@@ -983,6 +1047,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     }
     if (!has_inst) return;  // (WG: a padding warp of the batch's last group)
 
+    PCLK(7);
     // ---- RecoveryReport: live entries sorted by packed key (= lexicographic).
     // Counting sort on the key's top 8 bits (shared-memory histogram, warp
     // scan, scatter), then insertion sort inside the (short) buckets.
@@ -1058,6 +1123,8 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         out.samples_used[inst] = (long long)it_run * nl * L;
         out.terminated_by[inst] = term;
     }
+    PCLK(8);
+    PCLK_FLUSH();
 }
 
 #include "fpssft_team.cuh"
@@ -1787,14 +1854,17 @@ int warp_kernel_regs(const Geo &g, int precision, int k_cap) {
 #ifndef FPSSFT_GROUP_WG
 #define FPSSFT_GROUP_WG 8  // warps (= interleaved instances) per group-gather CTA; 0 = off
 #endif
+#ifndef FPSSFT_GROUP_TEAM
+#define FPSSFT_GROUP_TEAM FPSSFT_GROUP_WG  // warps per gather team (a divisor of the CTA width)
+#endif
 const void *group_kernel_for(const Geo &g, int precision, int group, int k_cap) {
     if (!FPSSFT_GROUP_WG || precision != FPSSFT_F32 || !g.off32 || group < FPSSFT_GROUP_WG ||
         group % FPSSFT_GROUP_WG)
         return nullptr;
 #if FPSSFT_GROUP_WG
     if (g.D == 2 && g.L == 256)
-        return k_cap == 128 ? (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_WG, 128>
-                            : (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_WG>;
+        return k_cap == 128 ? (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_TEAM, 128>
+                            : (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_TEAM>;
 #endif
     return nullptr;
 }
@@ -2008,6 +2078,17 @@ size_t spec_smem(const Geo &g, int nlines, int cs) {
 using namespace fpssft;
 
 extern "C" {
+#if FPSSFT_PHASE_CLOCK
+int fpssft_debug_phase_cycles(unsigned long long *out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
+    if (reset) {
+        static const unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 const char *fpssft_last_error(void) { return g_err.c_str(); }
 int fpssft_abi_version(void) { return 1; }

@@ -585,6 +585,34 @@ struct GroupGather {
             }
         }
     }
+    // the same segments into L2 only (one request per 64-byte segment: the
+    // thread that loads the segment's first chunk)
+    __device__ __forceinline__ void prefetch_l2(const float2 *__restrict__ gbase, const Geo &g,
+                                                const int *al, const int *ta, int tid) const {
+        const int c = tid % CH, q0 = tid / CH;
+        if (c != 0) return;
+        int n[LQ][DC];
+#pragma unroll
+        for (int j = 0; j < LQ; ++j)
+#pragma unroll
+            for (int k = 0; k < DC; ++k)
+                n[j][k] = (int)fastmod((unsigned)al[k] * (unsigned)(q0 + QS * j) + (unsigned)ta[k],
+                                       g.magic[k], (unsigned)g.N[k]);
+#pragma unroll
+        for (int i = 0; i < NL; ++i) {
+#pragma unroll
+            for (int j = 0; j < LQ; ++j) {
+                int off = 0;
+#pragma unroll
+                for (int k = 0; k < DC; ++k) {
+                    int nk = n[j][k];
+                    if (k == i - 1) nk = nk + 1 == g.N[k] ? 0 : nk + 1;
+                    off += nk * g.stride32[k];
+                }
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(gbase + off));
+            }
+        }
+    }
     // owner spectra: warp w's at spec0 + w * warp_stride (complex units)
     __device__ __forceinline__ void store(cpx<float> *spec0, int warp_stride, int tid) const {
         const int c = tid % CH, q0 = tid / CH;

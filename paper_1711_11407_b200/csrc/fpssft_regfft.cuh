@@ -153,6 +153,89 @@ __device__ __forceinline__ float fft256_lines_warp(cpx<float> *spec, int nlines,
     return energy;
 }
 
+// As fft256_lines_warp for a compile-time number of lines NL, all lines
+// transformed together phase by phase: NL independent chains per phase for
+// the scheduler to interleave, and each twiddle loaded once for every line.
+template <int NL>
+__device__ __forceinline__ float fft256_lines_joint(cpx<float> *spec, const cpx<float> *roots,
+                                                    int lane) {
+    constexpr int PADL = 256 + 16, S = 33;
+    float energy = 0.f;
+    const int k1 = lane >> 2, h = lane & 3, k2b = (h >> 1) + 2 * (h & 1);
+    float2 *base = (float2 *)spec;
+    float2 v[NL][8];
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int i = 32 * a + lane;
+            const float2 x = base[l * PADL + i + (i >> 4)];
+            energy += x.x * x.x + x.y * x.y;
+            v[l][a] = make_float2(x.x, -x.y);  // conjugate in
+        }
+    float2 tw[8];
+#pragma unroll
+    for (int c = 1; c < 8; ++c) {
+        const cpx<float> r = roots[lane * c];
+        tw[c] = make_float2(r.re, r.im);
+    }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        dft8(v[l]);
+#pragma unroll
+        for (int c = 1; c < 8; ++c) v[l][c] = cmul(v[l][c], tw[c]);
+    }
+    __syncwarp();  // the lines' inputs are read before the exchange overwrites them
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) base[l * PADL + c * S + lane] = v[l][c];
+    __syncwarp();
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+#pragma unroll
+        for (int be = 0; be < 8; ++be) v[l][be] = base[l * PADL + k1 * S + 4 * be + h];
+#pragma unroll
+    for (int d = 1; d < 8; ++d) {  // e^{2 pi i h d / 32} = roots[8 h d] (a runtime h)
+        const cpx<float> r = roots[8 * h * d];
+        tw[d] = make_float2(r.re, r.im);
+    }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        dft8(v[l]);
+#pragma unroll
+        for (int d = 1; d < 8; ++d) v[l][d] = cmul(v[l][d], tw[d]);
+    }
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {  // 4-point DFTs across lanes h (xor 2, then xor 1)
+        float2 x[NL], p[NL];
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+            x[l] = v[l][d];
+            p[l] = make_float2(__shfl_xor_sync(FULL, x[l].x, 2), __shfl_xor_sync(FULL, x[l].y, 2));
+        }
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+            x[l] = (h & 2) ? csub(p[l], x[l]) : cadd(x[l], p[l]);
+            if (h == 3) x[l] = mul_i(x[l]);
+            p[l] = make_float2(__shfl_xor_sync(FULL, x[l].x, 1), __shfl_xor_sync(FULL, x[l].y, 1));
+        }
+#pragma unroll
+        for (int l = 0; l < NL; ++l) v[l][d] = (h & 1) ? csub(p[l], x[l]) : cadd(x[l], p[l]);
+    }
+    __syncwarp();  // every lane has read the exchange before outputs land in it
+    const float inv = 1.f / 256.f;
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+            const int k = k1 + 8 * (d + 8 * k2b);
+            base[l * PADL + k + (k >> 4)] = make_float2(v[l][d].x * inv, -v[l][d].y * inv);
+        }
+    __syncwarp();
+    return energy;
+}
+
 // Forward 1/L-normalised DFTs of `nlines` 512-point lines in the padded
 // spectra layout (padi), one warp per line (warps >= nlines idle): the
 // conjugate of the inverse transform of the conjugated line.  `roots` is the
