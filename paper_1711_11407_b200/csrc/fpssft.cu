@@ -50,6 +50,12 @@
 #ifndef FPSSFT_WARP_FFT_JOINT
 #define FPSSFT_WARP_FFT_JOINT 0  // A/B: warp kernel, 256-point lines transformed together (measured slower: spills)
 #endif
+#ifndef FPSSFT_GUARD_FFT64
+#define FPSSFT_GUARD_FFT64 1  // guarded warp kernel, 64-point lines: register/shuffle float64 FFT
+#endif
+#ifndef FPSSFT_GUARD_R64
+#define FPSSFT_GUARD_R64 1  // guarded warp kernel: float64 root table (not a float32 hi/lo pair)
+#endif
 #ifndef FPSSFT_GROUP_PF
 #define FPSSFT_GROUP_PF 0  // group kernel: L2-prefetch iteration t+1 during t for t + 1 < this
 #endif
@@ -504,8 +510,11 @@ __host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, 
     y.hash = o;      o = align16(o + (size_t)y.H * 2);
     y.slot_live = o; o = align16(o + (size_t)k_cap);
     y.cand = o;      o = align16(o + (size_t)L * 2);
-    y.scr_u = o;     o = align16(o + 32 * 4 * (size_t)(D + 1));
-    y.scr_amp = o;   o = align16(o + 32 * (size_t)acs);
+    // projection staging: per lane, its slot's contribution on every line
+    // (and, guarded, the float64 line-0 one and |a|)
+    // (float64: the slots' phases and amplitudes instead)
+    y.scr_u = o;     o = align16(o + 32 * (size_t)(cs == 16 ? 4 : cs) * (size_t)(D + 1));
+    y.scr_amp = o;   o = align16(o + (guard ? 32 * (16 + 4) : (cs == 16 ? 32 * 16 : 0)));
     y.x0d = y.pabs = o;
     if (guard) {
         y.x0d = o;   o = align16(o + (size_t)(L + L / 16 + 1) * 16);
@@ -514,7 +523,7 @@ __host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, 
     y.per_warp = o;
     // per CTA: the float32 root table, then (guarded) the float64 one
     y.roots64 = align16((size_t)L * cs);  // lo half of Roots64Split (guarded)
-    y.roots = y.roots64 + (guard ? align16((size_t)L * 8) : 0);
+    y.roots = y.roots64 + (guard ? align16((size_t)L * (FPSSFT_GUARD_R64 ? 16 : 8)) : 0);
     return y;
 }
 
@@ -555,9 +564,9 @@ __device__ __forceinline__ void hash16_insert(unsigned short *hash, int H, int k
 #endif
 #if FPSSFT_PHASE_CLOCK
 __device__ unsigned long long g_phase_cycles[16];
-#define PCLK_DECL() long long pclk_t = clock64(); long long pclk_acc[9] = {0}; int pclk_last = 8
+#define PCLK_DECL() long long pclk_t = clock64(); long long pclk_acc[12] = {0}; int pclk_last = 8
 #define PCLK(n) do { const long long t_ = clock64(); pclk_acc[pclk_last] += t_ - pclk_t; pclk_t = t_; pclk_last = (n); } while (0)
-#define PCLK_FLUSH() do { if (lane == 0) for (int i_ = 0; i_ < 9; ++i_) atomicAdd(&g_phase_cycles[i_], (unsigned long long)pclk_acc[i_]); } while (0)
+#define PCLK_FLUSH() do { if (lane == 0) for (int i_ = 0; i_ < 12; ++i_) atomicAdd(&g_phase_cycles[i_], (unsigned long long)pclk_acc[i_]); } while (0)
 #else
 #define PCLK_DECL() do {} while (0)
 #define PCLK(n) do {} while (0)
@@ -608,9 +617,18 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     const WarpLayout lay = make_warp_layout(g.D, g.L, k_cap, (int)sizeof(cpx<R>), GUARD, WG != 0);
     cpx<R> *roots = (cpx<R> *)sm;
     [[maybe_unused]] cpx<float> *roots_lo = (cpx<float> *)(sm + lay.roots64);
-    [[maybe_unused]] const Roots64Split roots64{(const cpx<float> *)roots, roots_lo};
+#if FPSSFT_GUARD_R64
+    using Roots64 = Roots64Full;  // guarded: a float64 root table
+    [[maybe_unused]] const Roots64 roots64{(const cpx<double> *)(sm + lay.roots64)};
+#else
+    using Roots64 = Roots64Split;
+    [[maybe_unused]] const Roots64 roots64{(const cpx<float> *)roots, roots_lo};
+#endif
     build_roots(roots, g.L);
-    if constexpr (GUARD) build_roots_lo(roots_lo, g.L);
+    if constexpr (GUARD) {
+        if (FPSSFT_GUARD_R64) build_roots64((cpx<double> *)(sm + lay.roots64), g.L);
+        else build_roots_lo(roots_lo, g.L);
+    }
     __syncthreads();  // the only block-wide barrier: warps run independently below
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -634,8 +652,9 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     unsigned short *hash = (unsigned short *)(base + lay.hash);
     unsigned char *slot_live = base + lay.slot_live;
     unsigned short *cand = (unsigned short *)(base + lay.cand);
-    int *scr_u = (int *)(base + lay.scr_u);
-    cpx<A> *scr_amp = (cpx<A> *)(base + lay.scr_amp);
+    cpx<R> *scr_c = (cpx<R> *)(base + lay.scr_u);
+    [[maybe_unused]] cpx<double> *scr_c0 = (cpx<double> *)(base + lay.scr_amp);
+    [[maybe_unused]] float *scr_ca = (float *)(base + lay.scr_amp + 32 * 16);
     [[maybe_unused]] cpx<double> *x0d = (cpx<double> *)(base + lay.x0d);
     [[maybe_unused]] float *pabs = (float *)(base + lay.pabs);
 
@@ -795,11 +814,14 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             else
                 my_energy = (R)regfft::fft256_lines_warp((cpx<float> *)spec, DC + 1,
                                                          (const cpx<float> *)roots, lane);
-            if constexpr (GUARD) fft_static<double, LC, 1, 32, WarpTeam, Roots64Split>(x0d, roots64, lane);
+            if constexpr (GUARD) fft_static<double, LC, 1, 32, WarpTeam, Roots64>(x0d, roots64, lane);
         } else if constexpr (LC != 0) {
             const R e = fft_static<R, LC, DC + 1>(spec, roots, lane);
             if (sizeof(R) == 4) my_energy = e;
-            if constexpr (GUARD) fft_static<double, LC, 1, 32, WarpTeam, Roots64Split>(x0d, roots64, lane);
+            if constexpr (GUARD && LC == 64 && FPSSFT_GUARD_FFT64)
+                regfft::fft64_line_f64(x0d, roots64, lane);
+            else if constexpr (GUARD)
+                fft_static<double, LC, 1, 32, WarpTeam, Roots64>(x0d, roots64, lane);
         } else
             fft_lines_warp<R>(spec, nl, g, roots, lane);
         PCLK(3);
@@ -812,56 +834,115 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             noise_floor = (R)kn.noise_coef * sqrt(__shfl_sync(FULL, warp_sum(my_energy), 0));
         }
 
-        // (3) construction-subtraction, 32 slots at a time in slot order;
-        //     each lane stages its slot's phase on every line, slots sharing
-        //     a bin are summed by their lowest lane in lane (= slot) order.
+        // (3) construction-subtraction, 32 slots at a time in slot order:
+        //     each lane computes its slot's contribution on every line; slots
+        //     sharing a bin are summed by their lowest lane in lane (= slot)
+        //     order, through shared memory only when a bin is hit twice.
         //     GUARD: also the float64 line-0 projection and the bins' sum |a|
+        if constexpr (sizeof(R) == 8) {
+            // float64: slot phases staged, the group's lowest lane forms the
+            // sums (fewer live registers than per-lane contributions:
+            // measured 1.75 vs 2.12 ms on config 3)
+            int *scr_u = (int *)scr_c;
+            cpx<R> *scr_amp = (cpx<R> *)(base + lay.scr_amp);
+            for (int c0 = 0; c0 < n_slots; c0 += 32) {
+                const int s = c0 + lane;
+                const bool valid = s < n_slots && slot_live[s];
+                int b = -1 - lane;
+                if (valid) {
+                    int m[MAXD];
+                    unpack_key(slot_key[s], g, m);
+                    b = bin_of(m, g, al);
+                    const int u0 = phase_of(m, g, ta);
+#pragma unroll
+                    for (int i = 0; i < MAXD + 1; ++i)
+                        if (i < nl) scr_u[i * 32 + lane] = phase_step(u0, i, m, g);
+                    scr_amp[lane] = {(R)slot_amp[s].re, (R)slot_amp[s].im};
+                }
+                __syncwarp();
+                const unsigned grp = __match_any_sync(FULL, b);
+                if (valid && lane == __ffs(grp) - 1) {
+                    cpx<R> P[MAXD + 1];
+#pragma unroll
+                    for (int i = 0; i < MAXD + 1; ++i) P[i] = {(R)0, (R)0};
+                    for (unsigned rest = grp; rest; rest &= rest - 1) {
+                        const int j = __ffs(rest) - 1;
+                        const cpx<R> ar = scr_amp[j];
+#pragma unroll
+                        for (int i = 0; i < MAXD + 1; ++i)
+                            if (i < nl) P[i] = P[i] + ar * roots[scr_u[i * 32 + j]];
+                    }
+#pragma unroll
+                    for (int i = 0; i < MAXD + 1; ++i)
+                        if (i < nl) spec[padi<PAD>(i * L + b)] = spec[padi<PAD>(i * L + b)] - P[i];
+                }
+                __syncwarp();
+            }
+        } else
         for (int c0 = 0; c0 < n_slots; c0 += 32) {
             const int s = c0 + lane;
             const bool valid = s < n_slots && slot_live[s];
             int b = -1 - lane;
+            // every lane: its slot's contribution a root[u_i] on each line
+            cpx<R> C[MAXD + 1];
+            [[maybe_unused]] cpx<double> C0 = {0.0, 0.0};
+            [[maybe_unused]] float ca = 0.f;
             if (valid) {
                 int m[MAXD];
                 unpack_key(slot_key[s], g, m);
                 b = bin_of(m, g, al);
                 const int u0 = phase_of(m, g, ta);
+                const cpx<A> aj = slot_amp[s];
+                const cpx<R> ar = {(R)aj.re, (R)aj.im};
 #pragma unroll
                 for (int i = 0; i < MAXD + 1; ++i)
-                    if (i < nl) scr_u[i * 32 + lane] = phase_step(u0, i, m, g);
-                scr_amp[lane] = slot_amp[s];
+                    if (i < nl) C[i] = ar * roots[phase_step(u0, i, m, g)];
+                if constexpr (GUARD) {
+                    C0 = cpx<double>{(double)aj.re, (double)aj.im} * roots64[u0];
+                    ca = cabs(ar);
+                }
             }
-            __syncwarp();
+            // slots sharing a bin are summed by their lowest lane in lane
+            // (= slot) order; a bin hit once is updated by its own lane
             const unsigned grp = __match_any_sync(FULL, b);
-            if (valid && lane == __ffs(grp) - 1) {
-                cpx<R> P[MAXD + 1];
-                [[maybe_unused]] cpx<double> P0 = {0.0, 0.0};
-                [[maybe_unused]] float pa = 0.f;
-#pragma unroll
-                for (int i = 0; i < MAXD + 1; ++i) P[i] = {(R)0, (R)0};
-                for (unsigned rest = grp; rest; rest &= rest - 1) {
-                    const int j = __ffs(rest) - 1;
-                    const cpx<A> aj = scr_amp[j];
-                    const cpx<R> ar = {(R)aj.re, (R)aj.im};
+            const bool multi = (grp & (grp - 1)) != 0;
+            const bool lead = valid && lane == __ffs(grp) - 1;
+            if (__any_sync(FULL, valid && multi)) {
+                if (valid && multi && !lead) {
 #pragma unroll
                     for (int i = 0; i < MAXD + 1; ++i)
-                        if (i < nl) P[i] = P[i] + ar * roots[scr_u[i * 32 + j]];
+                        if (i < nl) scr_c[i * 32 + lane] = C[i];
                     if constexpr (GUARD) {
-                        P0 = P0 + cpx<double>{(double)aj.re, (double)aj.im} * roots64[scr_u[j]];
-                        pa += cabs(ar);
+                        scr_c0[lane] = C0;
+                        scr_ca[lane] = ca;
                     }
                 }
+                __syncwarp();
+                if (lead && multi) {
+                    for (unsigned rest = grp & (grp - 1); rest; rest &= rest - 1) {
+                        const int j = __ffs(rest) - 1;
+#pragma unroll
+                        for (int i = 0; i < MAXD + 1; ++i)
+                            if (i < nl) C[i] = C[i] + scr_c[i * 32 + j];
+                        if constexpr (GUARD) {
+                            C0 = C0 + scr_c0[j];
+                            ca += scr_ca[j];
+                        }
+                    }
+                }
+            }
+            if (lead) {
 #pragma unroll
                 for (int i = 0; i < MAXD + 1; ++i)
-                    if (i < nl) spec[padi<PAD>(i * L + b)] = spec[padi<PAD>(i * L + b)] - P[i];
+                    if (i < nl) spec[padi<PAD>(i * L + b)] = spec[padi<PAD>(i * L + b)] - C[i];
                 if constexpr (GUARD) {
-                    x0d[padi<PAD>(b)] = x0d[padi<PAD>(b)] - P0;
-                    pabs[b] += pa;
+                    x0d[padi<PAD>(b)] = x0d[padi<PAD>(b)] - C0;
+                    pabs[b] += ca;
                 }
             }
             __syncwarp();
         }
 
-        PCLK(4);
         // (4) classify + (5) merge, 32 bins at a time in ascending order
         const A floor_a = max(max((A)kn.energy_floor_abs, (A)kn.energy_floor * amp_sum),
                               (A)noise_floor);
@@ -919,22 +1000,13 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
                 for (unsigned rest = need; rest; rest &= rest - 1) {
                     const int owner = __ffs(rest) - 1;
                     const int bf = __shfl_sync(FULL, b, owner);
-                    cpx<double> dft[MAXD], prj[MAXD];
-                    exact_bin_partials<A>(bf, cube, g, al, ta, roots64, n_slots, slot_key,
-                                          slot_live, slot_amp, lane, 32, dft, prj);
-                    cpx<double> S[MAXD + 1];
-                    S[0] = x0d[padi<PAD>(bf)];
-#pragma unroll
-                    for (int i = 0; i < MAXD; ++i)
-                        if (i < D)
-                            S[i + 1] = {warp_sum(dft[i].re) / (double)L - warp_sum(prj[i].re),
-                                        warp_sum(dft[i].im) / (double)L - warp_sum(prj[i].im)};
                     int mx[MAXD];
-                    cpx<double> ax;
-                    // every lane holds the same sums: each decides, the owner keeps it
-                    const int sx = classify_values<double, Roots64Split>(S, g, bf, al, ta, roots64, kn.mag_tol,
-                                                           kn.round_tol, kn.verify_tol,
-                                                           (double)floor_a, mx, &ax);
+                    [[maybe_unused]] cpx<double> S[MAXD + 1];
+                    // every lane gets the same decision, the owner keeps it
+                    const int sx = exact_reeval_warp<A, Roots64, LC, DC>(
+                        bf, cube, g, al, ta, roots64, n_slots, slot_key, slot_live, slot_amp,
+                        x0d[padi<PAD>(bf)], kn, (double)floor_a, lane, mx,
+                        FPSSFT_GUARD_CALIB == 1 ? S : nullptr);
                     if (lane == owner) {
                         st = sx;
 #pragma unroll
@@ -2111,6 +2183,15 @@ int fpssft_guard_calib(float *max_ratio, unsigned long long *count) {
     *count = c;
     return FPSSFT_OK;
 }
+#if FPSSFT_GUARD_CALIB == 2
+int fpssft_guard_reasons(unsigned long long *out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_guard_reason, sizeof(g_guard_reason));
+    static const unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_guard_reason, z, sizeof(z));
+    return 0;
+}
+#endif
 #endif
 
 int fpssft_set_l2_fetch_granularity(int32_t bytes) {

@@ -44,9 +44,16 @@ __device__ __forceinline__ cpx<R> mulc(cpx<R> a, cpx<R> b) {
     return {a.re * b.re + a.im * b.im, a.im * b.re - a.re * b.im};
 }
 // |z|: hypot in float64 (what np.abs computes); sqrt(x^2 + y^2) in float32,
-// whose inputs never approach overflow here.
+// whose inputs never approach overflow here.  (FPSSFT_CABS_HYPOT=0: the
+// float64 sqrt form, A/B only -- mixed, within +-4 %.)
+#ifndef FPSSFT_CABS_HYPOT
+#define FPSSFT_CABS_HYPOT 1
+#endif
 template <class R>
-__device__ __forceinline__ R cabs(cpx<R> a) { return hypot(a.re, a.im); }
+__device__ __forceinline__ R cabs(cpx<R> a) {
+    if constexpr (FPSSFT_CABS_HYPOT) return hypot(a.re, a.im);
+    else return sqrt(fma(a.re, a.re, a.im * a.im));
+}
 __device__ __forceinline__ float cabs(cpx<float> a) { return sqrtf(a.re * a.re + a.im * a.im); }
 template <class R>
 __device__ __forceinline__ R cabs2(cpx<R> a) { return a.re * a.re + a.im * a.im; }
@@ -205,6 +212,18 @@ struct Roots64Split {
         return {(double)h.re + (double)l.re, (double)h.im + (double)l.im};
     }
 };
+// A float64 table e^{+2 pi i j / L} (one 16-byte load per root).
+struct Roots64Full {
+    const cpx<double> *t;
+    __device__ __forceinline__ cpx<double> operator[](int j) const { return t[j]; }
+};
+__device__ __forceinline__ void build_roots64(cpx<double> *t, int L) {
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+        double s, c;
+        sincospi(2.0 * (double)j / (double)L, &s, &c);
+        t[j] = {c, s};
+    }
+}
 __device__ __forceinline__ void build_roots_lo(cpx<float> *lo, int L) {
     for (int j = threadIdx.x; j < L; j += blockDim.x) {
         double s, c;

@@ -37,6 +37,15 @@ constexpr float GUARD_KP = FPSSFT_GUARD_KP * U32;
 constexpr double GUARD_KF = FPSSFT_GUARD_KF;     // Knobs::guard_coef = GUARD_KF * unit
 constexpr int ST_FLAG = 4;                       // decision inside the guard band
 constexpr unsigned short CAND_FLAG = 0x8000;     // candidate-list entry flagged at the magnitude test
+#if FPSSFT_GUARD_CALIB == 2
+// why decisions were flagged: [0] magnitude test, [1] phase too uncertain,
+// [2] rint may round either way, [3] verify band, [4] round_tol band,
+// [5] decodes attempted, [6] certain rejections by the bin map
+__device__ unsigned long long g_guard_reason[8];
+#define GUARD_REASON(i) atomicAdd(&g_guard_reason[i], 1ull)
+#else
+#define GUARD_REASON(i) do {} while (0)
+#endif
 #if FPSSFT_GUARD_CALIB
 // largest |S_float32 - S_exact| / (unit bound) seen (float bits, positive)
 __device__ unsigned int g_guard_calib_max;
@@ -66,6 +75,7 @@ __device__ __forceinline__ bool bin_is_candidate_guarded(const cpx<float> *spec,
     const float t = sqrtf(top), lo = sqrtf(low), s0 = sqrtf(q0);
     const float Eb = Eb0 + 2.f * U32 * t;
     *flag = fabsf(s0 - floor) <= Eb || (mag_tol < 1.f && fabsf(lo - c * t) <= (1.f + c) * Eb);
+    if (*flag) GUARD_REASON(0);
     return ok;
 }
 
@@ -126,8 +136,12 @@ __device__ __forceinline__ int decode_candidate_guarded(const cpx<float> *spec, 
             }
         }
     }
+    GUARD_REASON(5);
     if (fail_sure) return 1;
-    if (m_unsure & 0x80u) return ST_FLAG;
+    if (m_unsure & 0x80u) {
+        GUARD_REASON(1);
+        return ST_FLAG;
+    }
     // the exact bin map: a frequency that does not map back onto b is
     // rejected (driver.py:166-176) -- for every m the rounding may give
     {
@@ -139,9 +153,15 @@ __device__ __forceinline__ int decode_candidate_guarded(const cpx<float> *spec, 
             for (int k = 0; k < MAXD; ++k) mc[k] = (c >> k & 1u) ? m_alt[k] : m[k];
             maps = maps || bin_of(mc, g, al) == b;
         }
-        if (!maps) return 3;
+        if (!maps) {
+            GUARD_REASON(6);
+            return 3;
+        }
     }
-    if (m_unsure) return ST_FLAG;
+    if (m_unsure) {
+        GUARD_REASON(2);
+        return ST_FLAG;
+    }
     const int u0 = phase_of(m, g, ta);
     const cpx<float> amp = mulc(s[0], roots[u0]);
     const float lim = verify_tol * mg[0];
@@ -157,6 +177,8 @@ __device__ __forceinline__ int decode_candidate_guarded(const cpx<float> *spec, 
         }
     }
     if (fail_sure) return 1;
+    if (verify_unsure) GUARD_REASON(3);
+    else if (round_unsure) GUARD_REASON(4);
     if (verify_unsure || round_unsure) return ST_FLAG;
     return 2;
 }
@@ -231,4 +253,47 @@ __device__ __forceinline__ void exact_bin_partials(int b, const float2 *__restri
         for (int i = 1; i < MAXD + 1; ++i)
             if (i <= D) prj[i - 1] = prj[i - 1] + a * roots64[phase_step(u0, i, m, g)];
     }
+}
+
+// The exact re-evaluation of one flagged bin bf by a whole warp: the float64
+// values of its D+1 lines (line 0 given, s0; lines 1..D from the samples and
+// the float64 projection) and the reference's decision on them.  Out of line
+// (FPSSFT_GUARD_NOINLINE): a rare path whose float64 atan2 / hypot code would
+// otherwise sit inside the hot loop and crowd the instruction cache.  Every
+// lane returns the same decision; *m gets the decoded frequency.
+#ifndef FPSSFT_GUARD_NOINLINE
+#define FPSSFT_GUARD_NOINLINE 0  // A/B: 1 measured slower (stack frame, spills)
+#endif
+#if FPSSFT_GUARD_NOINLINE
+#define GUARD_REEVAL_INLINE __noinline__
+#else
+#define GUARD_REEVAL_INLINE __forceinline__
+#endif
+template <class AmpT, class RT, int LC, int DC>
+__device__ GUARD_REEVAL_INLINE int exact_reeval_warp(int bf, const float2 *__restrict__ cube,
+                                                     const Geo &g, const int *al, const int *ta,
+                                                     RT roots64, int n_slots, const int *slot_key,
+                                                     const unsigned char *slot_live,
+                                                     const cpx<AmpT> *amp64, cpx<double> s0,
+                                                     const Knobs &kn, double floor, int lane,
+                                                     int *m, cpx<double> *S_out = nullptr) {
+    Geo gc = g;  // the compile-time shape, for the callee's loops
+    gc.L = LC;
+    gc.D = DC;
+    gc.nlines = DC + 1;
+    cpx<double> dft[MAXD], prj[MAXD];
+    exact_bin_partials<AmpT>(bf, cube, gc, al, ta, roots64, n_slots, slot_key, slot_live, amp64,
+                             lane, 32, dft, prj);
+    cpx<double> S[MAXD + 1];
+    S[0] = s0;
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i)
+        if (i < DC)
+            S[i + 1] = {warp_sum(dft[i].re) / (double)LC - warp_sum(prj[i].re),
+                        warp_sum(dft[i].im) / (double)LC - warp_sum(prj[i].im)};
+    if (S_out != nullptr)  // calibration builds: the exact values
+        for (int i = 0; i <= DC; ++i) S_out[i] = S[i];
+    cpx<double> ax;
+    return classify_values<double, RT>(S, gc, bf, al, ta, roots64, kn.mag_tol, kn.round_tol,
+                                       kn.verify_tol, floor, m, &ax);
 }

@@ -153,6 +153,47 @@ __device__ __forceinline__ float fft256_lines_warp(cpx<float> *spec, int nlines,
     return energy;
 }
 
+// Forward 1/64-normalised DFT of one 64-point float64 line (padded layout,
+// in place) by one warp, in registers: lane l holds x[l] and x[l + 32]; one
+// radix-2 step in the lane (a = x[l] + x[l+32], b = (x[l] - x[l+32]) w^l,
+// w = e^{-2 pi i / 64}), then the two 32-point DFTs (A -> X[2k], B -> X[2k+1])
+// across the lanes by five decimation-in-frequency shuffle stages; lane p
+// ends with A[bitrev5(p)], B[bitrev5(p)].  `roots` is any float64-exact
+// table e^{+2 pi i j / 64}.
+template <class RT>
+__device__ __forceinline__ void fft64_line_f64(cpx<double> *x, RT roots, int lane) {
+    const cpx<double> u = x[lane + (lane >> 4)], v = x[lane + 32 + ((lane + 32) >> 4)];
+    const cpx<double> r0 = roots[lane];
+    cpx<double> a = {u.re + v.re, u.im + v.im};
+    const cpx<double> d = {u.re - v.re, u.im - v.im};
+    cpx<double> b = mulc(d, r0);  // d e^{-2 pi i l / 64}
+    // stage twiddles (loaded up front): the lower half of each 2h block
+    // takes (x[p-h] - x[p]) W_{2h}^{p mod h}, the upper half x[p] + x[p+h];
+    // branch-free: t = x[partner] + sgn x[p], times w (1 in the upper half)
+    cpx<double> w[5];
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+        const int h = 16 >> st;
+        w[st] = (lane & h) ? roots[(lane & (h - 1)) * (32 / h)] : cpx<double>{1.0, 0.0};
+    }
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+        const int h = 16 >> st;
+        const double sg = (lane & h) ? -1.0 : 1.0;
+        const cpx<double> pa = {__shfl_xor_sync(FULL, a.re, h), __shfl_xor_sync(FULL, a.im, h)};
+        const cpx<double> pb = {__shfl_xor_sync(FULL, b.re, h), __shfl_xor_sync(FULL, b.im, h)};
+        a = mulc(cpx<double>{fma(sg, a.re, pa.re), fma(sg, a.im, pa.im)}, w[st]);
+        b = mulc(cpx<double>{fma(sg, b.re, pb.re), fma(sg, b.im, pb.im)}, w[st]);
+    }
+    const int k = (int)(__brev((unsigned)lane) >> 27);  // bitrev5
+    __syncwarp();  // every lane read its inputs before outputs land
+    const double inv = 1.0 / 64.0;
+    const int e0 = 2 * k, e1 = 2 * k + 1;
+    x[e0 + (e0 >> 4)] = {a.re * inv, a.im * inv};
+    x[e1 + (e1 >> 4)] = {b.re * inv, b.im * inv};
+    __syncwarp();
+}
+
 // As fft256_lines_warp for a compile-time number of lines NL, all lines
 // transformed together phase by phase: NL independent chains per phase for
 // the scheduler to interleave, and each twiddle loaded once for every line.

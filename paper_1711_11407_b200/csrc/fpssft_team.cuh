@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
         nta[k] = k < D ? sched[D + k] : 0;
     }
 
+    PCLK_DECL();
     for (int it = 0; it < kn.t_max && term != -1; ++it) {
         int al[MAXD], ta[MAXD];
 #pragma unroll
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
         }
         it_run = it + 1;
 
+        PCLK(0);
         // (1) gather + (2) DFT                                 driver.py:146-154
         bool staged = false;
         unsigned par = 0, dup = 0;
@@ -182,6 +184,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
             }
         }
         R my_energy;
+        PCLK(2);
         constexpr bool REG512 = FPSSFT_TEAM_REGFFT && LC == 512 && sizeof(R) == 4 && NW >= nl;
         if constexpr (REG512) {
             // one warp per line, in registers (regfft::): no block barrier inside
@@ -206,6 +209,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
             my_energy = fft_static<R, LC, nl, NT, BlockTeam>(spec, roots, tid);
             if constexpr (GUARD) fft_static<double, LC, 1, NT, BlockTeam, Roots64Split>(x0d, roots64, tid);
         }
+        PCLK(3);
         R noise_floor = (R)0;
         [[maybe_unused]] float Ef = 0.f;  // GUARD: transform part of the error bound
         if constexpr (GUARD) {
@@ -299,6 +303,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
             }
         }
 
+        PCLK(4);
         // (4) magnitude test on every bin, candidates compacted in ascending
         //     order; the residual of non-candidate bins is folded in.  GUARD:
         //     bins inside the guard band join the list, flagged
@@ -339,6 +344,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
         }
         __syncthreads();
 
+        PCLK(5);
         // (5) decode + merge-by-sum, NT candidates per round in ascending bin
         //     order (driver.py:103-108); decode results stay in registers
         int n_acc = 0, n_cand_x = 0;
@@ -346,6 +352,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
         bool overflow = false;
 #pragma unroll 1
         for (int c0 = 0; c0 < n_cand; c0 += NT) {
+            PCLK(5);
             const int idx = c0 + tid;
             const int ce = idx < n_cand ? cand[idx] : -1;
             const int b = ce >= 0 ? (ce & ~(int)CAND_FLAG) : -1;
@@ -359,6 +366,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
                                                        (const cpx<float> *)roots,
                                                        (float)round_tol, (float)verify_tol,
                                                        Ef + GUARD_KP * pabs[b], m);
+                PCLK(9);
                 const unsigned need = __ballot_sync(FULL, b >= 0 && (mflag || st == ST_FLAG));
 #if FPSSFT_GUARD_CALIB == 2
                 if (lane == 0 && need) atomicAdd(&g_guard_calib_count, (unsigned long long)__popc(need));
@@ -368,22 +376,13 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
                 for (unsigned rest = need; rest; rest &= rest - 1) {
                     const int owner = __ffs(rest) - 1;
                     const int bf = __shfl_sync(FULL, b, owner);
-                    cpx<double> dft[MAXD], prj[MAXD];
-                    exact_bin_partials<A>(bf, cube, g, al, ta, roots64, n_slots, slot_key,
-                                          slot_live, slot_amp, lane, 32, dft, prj);
-                    cpx<double> S[MAXD + 1];
-                    S[0] = x0d[padi<PAD>(bf)];
-#pragma unroll
-                    for (int i = 0; i < MAXD; ++i)
-                        if (i < D)
-                            S[i + 1] = {warp_sum(dft[i].re) / (double)L - warp_sum(prj[i].re),
-                                        warp_sum(dft[i].im) / (double)L - warp_sum(prj[i].im)};
                     int mx[MAXD];
-                    cpx<double> ax;
-                    // every lane holds the same sums: each decides, the owner keeps it
-                    const int sx = classify_values<double, Roots64Split>(
-                        S, g, bf, al, ta, roots64, kn.mag_tol, kn.round_tol, kn.verify_tol,
-                        (double)floor_a, mx, &ax);
+                    [[maybe_unused]] cpx<double> S[MAXD + 1];
+                    // every lane gets the same decision, the owner keeps it
+                    const int sx = exact_reeval_warp<A, Roots64Split, LC, DC>(
+                        bf, cube, g, al, ta, roots64, n_slots, slot_key, slot_live, slot_amp,
+                        x0d[padi<PAD>(bf)], kn, (double)floor_a, lane, mx,
+                        FPSSFT_GUARD_CALIB == 1 ? S : nullptr);
                     if (lane == owner) {
                         st = sx;
 #pragma unroll
@@ -406,6 +405,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
                     st = decode_candidate<R, PAD>(spec, g, b, al, ta, roots, round_tol,
                                                   verify_tol, m, &a);
             }
+            PCLK(10);
             int found = -1, key = 0;
             if (st == 2) {
                 key = pack_key(m, g);
@@ -479,6 +479,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
             break;
         }
 
+        PCLK(6);
         // (6) amp_sum and (7) termination                   driver.py:108,196-204
         if constexpr (GUARD) {
             amp_sum += block_sum(d_amp, dred);
@@ -509,6 +510,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
         }
     }
 
+    PCLK(7);
     // ---- RecoveryReport: counting sort of the live keys on their top
     //      TEAM_SORT_BITS bits, then insertion sort inside the (short)
     //      buckets.  Fine buckets matter: clustered spectra (config 4's blobs)
@@ -575,4 +577,6 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
         out.samples_used[inst] = (long long)it_run * nl * L;
         out.terminated_by[inst] = term;
     }
+    PCLK(8);
+    PCLK_FLUSH();
 }

@@ -9,9 +9,10 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-NAMES = ["gather issue + team barrier", "gather store + barrier", "FFT", "projection (3)",
+NAMES = ["gather (group: issue + barrier)", "gather store + barrier", "FFT", "projection (3)",
          "classify (4)", "decode + merge (5)", "amp_sum + termination", "output sort",
-         "kernel start (roots)"]
+         "kernel start (roots; warp kernel: + non-group gathers)",
+         "team guarded: flag re-evaluation", "team: exscan + merge", "-"]
 
 
 def main():
@@ -47,10 +48,10 @@ def main():
     r.run(run_cubes)
     torch.cuda.synchronize()
     f(buf, 1)
-    tot = sum(buf[:9])
+    tot = sum(buf[:12])
     print(f"config {args.config} {args.layout}: {tot / 1e9:.3f} G warp-cycles "
           f"({tot / w.batch / 1e3:.1f} k per instance)")
-    for n, v in zip(NAMES, buf[:9]):
+    for n, v in zip(NAMES, buf[:12]):
         print(f"  {n:30s} {100 * v / tot:5.1f} %  {v / w.batch:9.0f} cycles/instance")
 
 
