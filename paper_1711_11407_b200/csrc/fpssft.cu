@@ -56,6 +56,12 @@
 #ifndef FPSSFT_GUARD_R64
 #define FPSSFT_GUARD_R64 1  // guarded warp kernel: float64 root table (not a float32 hi/lo pair)
 #endif
+#ifndef FPSSFT_CLASSIFY_SPLIT
+#define FPSSFT_CLASSIFY_SPLIT 1  // warp kernel: all bins tested before the ballots (ILP)
+#endif
+#ifndef FPSSFT_DECODE_PIPE
+#define FPSSFT_DECODE_PIPE 0  // A/B: decode of chunk i+1 ahead of merge i (measured +2 %: off)
+#endif
 #ifndef FPSSFT_GROUP_PF
 #define FPSSFT_GROUP_PF 0  // group kernel: L2-prefetch iteration t+1 during t for t + 1 < this
 #endif
@@ -954,6 +960,40 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         // GUARD: bins inside the guard band join the list, flagged.
         int n_cand = 0, n_acc = 0;
         R resid = (R)0;
+        constexpr int NCH = (LC + 31) / 32;  // compile-time shapes: the chunks' tests
+        if constexpr (LC != 0 && NCH >= 4 && NCH <= 16 && FPSSFT_CLASSIFY_SPLIT) {
+            // first every chunk's test (loads and arithmetic only, independent
+            // chains), then the ballots and compaction
+            unsigned okb = 0, flb = 0;
+#pragma unroll
+            for (int j = 0; j < NCH; ++j) {
+                const int b = 32 * j + lane;
+                R top = (R)0;
+                bool ok = false, fl = false;
+                if (LC % 32 == 0 || b < L) {
+                    if constexpr (GUARD)
+                        ok = bin_is_candidate_guarded<PAD>((const cpx<float> *)spec, g, b,
+                                                           (float)mag_tol, (float)floor,
+                                                           Ef + GUARD_KP * pabs[b], (float *)&top,
+                                                           &fl);
+                    else
+                        ok = bin_is_candidate<R, PAD>(spec, g, b, mag_tol, floor, &top);
+                }
+                if (!ok && !fl) resid = max(resid, top);
+                okb |= (unsigned)ok << j;
+                flb |= (unsigned)fl << j;
+            }
+#pragma unroll
+            for (int j = 0; j < NCH; ++j) {
+                const bool c = ((okb | flb) >> j) & 1u;
+                const unsigned msk = __ballot_sync(FULL, c);
+                if (c)
+                    cand[n_cand + __popc(msk & lt_mask)] =
+                        (unsigned short)(32 * j + lane) |
+                        (unsigned short)(((flb >> j) & 1u) ? CAND_FLAG : 0);
+                n_cand += __popc(msk);
+            }
+        } else
         for (int c0 = 0; c0 < L; c0 += 32) {
             const int b = c0 + lane;
             R top = (R)0;
@@ -978,13 +1018,36 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         bool overflow = false;
         int n_cand_x = 0;
         A d_amp = (A)0;  // this lane's change of amp_sum
+        // unguarded: the next chunk is decoded before this one merges (its
+        // loads and arithmetic overlap the merge's dependent chain; distinct
+        // bins, so no hazard)
+        constexpr bool PIPE = !GUARD && FPSSFT_DECODE_PIPE;
+        [[maybe_unused]] int nx_b = -1, nx_st = 0, nx_m[MAXD];
+        [[maybe_unused]] cpx<R> nx_a;
+        if constexpr (PIPE) {
+            nx_b = lane < n_cand ? (int)(cand[lane] & ~CAND_FLAG) : -1;
+            if (nx_b >= 0)
+                nx_st = decode_candidate<R, PAD>(spec, g, nx_b, al, ta, roots, round_tol,
+                                                 verify_tol, nx_m, &nx_a);
+        }
         for (int c0 = 0; c0 < n_cand; c0 += 32) {
             const int ce = c0 + lane < n_cand ? cand[c0 + lane] : -1;
             const int b = ce >= 0 ? (ce & ~(int)CAND_FLAG) : -1;
             int m[MAXD];
             cpx<R> a;
             int st = 0;
-            if constexpr (GUARD) {
+            if constexpr (PIPE) {
+                st = nx_st;
+                a = nx_a;
+#pragma unroll
+                for (int k = 0; k < MAXD; ++k) m[k] = nx_m[k];
+                const int c1 = c0 + 32 + lane;
+                nx_b = c1 < n_cand ? (int)(cand[c1] & ~CAND_FLAG) : -1;
+                nx_st = 0;
+                if (nx_b >= 0)
+                    nx_st = decode_candidate<R, PAD>(spec, g, nx_b, al, ta, roots, round_tol,
+                                                     verify_tol, nx_m, &nx_a);
+            } else if constexpr (GUARD) {
                 const bool mflag = ce >= 0 && ((ce & CAND_FLAG) || FPSSFT_GUARD_CALIB == 1);
                 if (b >= 0 && !mflag)
                     st = decode_candidate_guarded<PAD>((const cpx<float> *)spec, g, b, al, ta,
