@@ -60,7 +60,11 @@ __host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, 
     // slots) / the classifier's candidate list
     const size_t u = o;
     y.proj = u;
-    const size_t a = align16(u + (size_t)(nt / 32) * 32 * ((MAXD + 1) * 4 + acs));
+    // (float32: per lane its contributions on the D+1 lines, guarded also a
+    // float64 line-0 one and |a|)
+    const size_t per_lane = cs == 16 ? (MAXD + 1) * 4 + acs
+                                     : (size_t)(D + 1) * cs + (guard ? 16 + 4 : 0);
+    const size_t a = align16(u + (size_t)(nt / 32) * 32 * per_lane);
     y.cand = u;      const size_t b = align16(u + (size_t)L * 2);
     o = a > b ? a : b;
     y.red = o;       o = align16(o + 64 * 8);  // 256 B of ints, then NW floats/doubles
@@ -244,6 +248,64 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
                     const bool valid = s < n_slots && slot_live[s];
                     int b = -1 - lane;
                     if (q) __syncwarp();  // the previous sub-round's scratch is read
+                    if constexpr (sizeof(R) == 4) {
+                        // float32: every lane its slot's contribution on each
+                        // line; shared memory only for bins hit twice
+                        cpx<R> *scr_c = (cpx<R> *)(sm + lay.proj) + warp * 32 * nl;
+                        [[maybe_unused]] cpx<double> *scr_c0 =
+                            (cpx<double> *)(sm + lay.proj + (size_t)NW * 32 * nl * 8) + warp * 32;
+                        [[maybe_unused]] float *scr_ca =
+                            (float *)(sm + lay.proj + (size_t)NW * 32 * (nl * 8 + 16)) + warp * 32;
+#pragma unroll
+                        for (int i = 0; i < MAXD + 1; ++i) P[q][i] = {(R)0, (R)0};
+                        if constexpr (GUARD) {
+                            P0[q] = {0.0, 0.0};
+                            pa[q] = 0.f;
+                        }
+                        if (valid) {
+                            int m[MAXD];
+                            unpack_key(slot_key[s], g, m);
+                            b = bin_of(m, g, al);
+                            const int u0 = phase_of(m, g, ta);
+                            const cpx<A> aj = slot_amp[s];
+                            const cpx<R> ar = {(R)aj.re, (R)aj.im};
+#pragma unroll
+                            for (int i = 0; i < MAXD + 1; ++i)
+                                if (i < nl) P[q][i] = ar * roots[phase_step(u0, i, m, g)];
+                            if constexpr (GUARD) {
+                                P0[q] = cpx<double>{(double)aj.re, (double)aj.im} * roots64[u0];
+                                pa[q] = cabs(ar);
+                            }
+                        }
+                        const unsigned grp = __match_any_sync(FULL, b);
+                        const bool multi = (grp & (grp - 1)) != 0;
+                        leader[q] = valid && lane == __ffs(grp) - 1;
+                        bq[q] = b;
+                        if (__any_sync(FULL, valid && multi)) {
+                            if (valid && multi && !leader[q]) {
+#pragma unroll
+                                for (int i = 0; i < MAXD + 1; ++i)
+                                    if (i < nl) scr_c[i * 32 + lane] = P[q][i];
+                                if constexpr (GUARD) {
+                                    scr_c0[lane] = P0[q];
+                                    scr_ca[lane] = pa[q];
+                                }
+                            }
+                            __syncwarp();
+                            if (leader[q] && multi)
+                                for (unsigned rest = grp & (grp - 1); rest; rest &= rest - 1) {
+                                    const int j = __ffs(rest) - 1;
+#pragma unroll
+                                    for (int i = 0; i < MAXD + 1; ++i)
+                                        if (i < nl) P[q][i] = P[q][i] + scr_c[i * 32 + j];
+                                    if constexpr (GUARD) {
+                                        P0[q] = P0[q] + scr_c0[j];
+                                        pa[q] += scr_ca[j];
+                                    }
+                                }
+                        }
+                        continue;
+                    }
                     if (valid) {
                         int m[MAXD];
                         unpack_key(slot_key[s], g, m);
