@@ -550,17 +550,24 @@ constexpr unsigned short HASH_EMPTY = 0xFFFF;
 __device__ __forceinline__ int hash16_find(const unsigned short *hash, const int *slot_key, int H,
                                            int key) {
     unsigned h = hash32(key) & (unsigned)(H - 1);
+    [[maybe_unused]] int probes = 0;
     while (true) {
         const unsigned short s = hash[h];
+        FPSSFT_CHECK(++probes <= H);
         if (s == HASH_EMPTY) return -1;
+        FPSSFT_CHECK((int)s < H / 2);  // H = 2 k_cap
         if (slot_key[s] == key) return s;
         h = (h + 1) & (unsigned)(H - 1);
     }
 }
 __device__ __forceinline__ void hash16_insert(unsigned short *hash, int H, int key, int slot) {
     unsigned h = hash32(key) & (unsigned)(H - 1);
-    while (atomicCAS(hash + h, HASH_EMPTY, (unsigned short)slot) != HASH_EMPTY)
+    FPSSFT_CHECK(slot >= 0 && slot < H / 2);
+    [[maybe_unused]] int probes = 0;
+    while (atomicCAS(hash + h, HASH_EMPTY, (unsigned short)slot) != HASH_EMPTY) {
+        FPSSFT_CHECK(++probes < H);
         h = (h + 1) & (unsigned)(H - 1);
+    }
 }
 
 // FPSSFT_PHASE_CLOCK builds: per-phase clock cycles of the warp kernel
@@ -987,6 +994,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             for (int j = 0; j < NCH; ++j) {
                 const bool c = ((okb | flb) >> j) & 1u;
                 const unsigned msk = __ballot_sync(FULL, c);
+                FPSSFT_CHECK(!c || n_cand + __popc(msk & lt_mask) < L);
                 if (c)
                     cand[n_cand + __popc(msk & lt_mask)] =
                         (unsigned short)(32 * j + lane) |
@@ -1008,6 +1016,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
             }
             if (!ok && !fl) resid = max(resid, top);
             const unsigned msk = __ballot_sync(FULL, ok || fl);
+            FPSSFT_CHECK(!(ok || fl) || n_cand + __popc(msk & lt_mask) < L);
             if (ok || fl)
                 cand[n_cand + __popc(msk & lt_mask)] =
                     (unsigned short)b | (unsigned short)(fl ? CAND_FLAG : 0);
@@ -1117,6 +1126,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
                 int s;
                 if (found < 0) {
                     s = n_slots + __popc(fresh & lt_mask);
+                    FPSSFT_CHECK(s < k_cap);
                     slot_key[s] = key;
                     hash16_insert(hash, H, key, s);
                 } else {
@@ -1224,7 +1234,11 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
     }
     __syncwarp();
     for (int s = lane; s < n_slots; s += 32)
-        if (slot_live[s]) sslot[atomicAdd(&hist[slot_key[s] >> shift], 1)] = s;
+        if (slot_live[s]) {
+            const int pos = atomicAdd(&hist[slot_key[s] >> shift], 1);
+            FPSSFT_CHECK(pos >= 0 && pos < count && (slot_key[s] >> shift) < 256);
+            sslot[pos] = s;
+        }
     __syncwarp();
     // buckets end at hist[b] (cursor after the scatter); sort each in place
     for (int bkt = lane; bkt < 256; bkt += 32) {

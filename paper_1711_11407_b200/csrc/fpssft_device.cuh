@@ -19,6 +19,25 @@
 namespace fpssft {
 
 constexpr int MAXD = 4;
+
+// Debug builds (-DFPSSFT_DEBUG_BOUNDS=1, tools/bounds_check.sh): every
+// shared-memory scatter / slot / hash index is checked and a violation traps
+// (the GPU pool has no compute-sanitizer).  Compiled out otherwise.
+#ifndef FPSSFT_DEBUG_BOUNDS
+#define FPSSFT_DEBUG_BOUNDS 0
+#endif
+#if FPSSFT_DEBUG_BOUNDS
+#define FPSSFT_CHECK(cond)                                                                    \
+    do {                                                                                      \
+        if (!(cond)) {                                                                        \
+            printf("FPSSFT_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #cond, (int)blockIdx.x, (int)threadIdx.x);                                \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define FPSSFT_CHECK(cond) do {} while (0)
+#endif
 #ifndef FPSSFT_R16_256
 #define FPSSFT_R16_256 1  // 256-point lines: radix 16x16 (1) or 8x8x4 (0)
 #endif

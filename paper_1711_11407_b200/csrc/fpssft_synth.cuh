@@ -81,7 +81,9 @@ __global__ void __launch_bounds__(NT, 2) synth512_kernel(const int *__restrict__
     // entries' m0 and amplitude into column-sorted arrays
     for (int e = tid; e < n; e += NT) {
         const int c = ecol[e];
-        sm0[atomicAdd(&col_fill[c], 1)] = e;  // sm0 holds entry ids for now
+        const int pos = atomicAdd(&col_fill[c], 1);
+        FPSSFT_CHECK(c >= 0 && c < NL && pos < n);
+        sm0[pos] = e;  // sm0 holds entry ids for now
     }
     __syncthreads();
     for (int c = tid; c < NL; c += NT) {

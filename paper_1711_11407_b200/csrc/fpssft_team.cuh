@@ -505,6 +505,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
                 int s;
                 if (fresh) {
                     s = n_slots + pre;
+                    FPSSFT_CHECK(s < kn.k_cap);
                     slot_key[s] = key;
                     hash16_insert(hash, H, key, s);
                 } else {
@@ -606,7 +607,11 @@ __global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
         }
     }
     for (int s = tid; s < n_slots; s += NT)
-        if (slot_live[s]) sslot[atomicAdd(&hist[slot_key[s] >> shift], 1)] = s;
+        if (slot_live[s]) {
+            const int pos = atomicAdd(&hist[slot_key[s] >> shift], 1);
+            FPSSFT_CHECK(pos >= 0 && pos < count);
+            sslot[pos] = s;
+        }
     __syncthreads();
     for (int bkt = tid; bkt < NB; bkt += NT) {
         const int en = hist[bkt], st = bkt ? hist[bkt - 1] : 0;

@@ -38,7 +38,37 @@ def run(dims, k, B=3, k_cap=None, modes=("auto", "cta"), prec=("fp32", "fp64")):
             print(dims, mode, p, res.count.tolist(), res.terminated_by.tolist(), img.shape)
 
 
+def run_group_and_guarded():
+    """The group-gather kernel (interleaved batch, shared schedule) and the
+    guarded float32 kernels (noisy profile: warp 64^3, team 512^2)."""
+    w = W.CONFIGS[2]
+    inst = [W.make_instance(w, r) for r in W.instance_rngs(w.seed, 8)]
+    cubes = torch.as_tensor(np.stack([c for _, _, c in inst])).cuda()
+    cfg = P.FpsSftConfig(seed=2, **PROF)
+    r = P.BatchRunner(P.CubeShape(w.dims), cfg, 8, k_cap=128, device="cuda", group=8)
+    res = r.run(P.interleave(cubes, 8))
+    torch.cuda.synchronize()
+    print("group kernel", r.plan, res.count.tolist())
+    pn = P.PROFILES["PN"]
+    for dims, k in (((64, 64, 64), 40), ((512, 512), 60)):
+        cubes = []
+        for b in range(2):
+            f, a = W.reference_generate(dims, k, 70 + b)
+            x = W.synthesize_np(dims, f, a)
+            x = x + 0.05 * (np.random.default_rng(b).standard_normal(x.shape)
+                            + 1j * np.random.default_rng(b + 9).standard_normal(x.shape))
+            cubes.append(x.astype(np.complex64))
+        t = torch.as_tensor(np.stack(cubes)).cuda()
+        cfg = P.FpsSftConfig(max_iterations=6, seed=5, **pn)
+        for mode in ("auto", "cta"):
+            res = P.fps_sft_batch(t, cfg, k_cap=256, precision="fp32-guarded", mode=mode,
+                                  iter_stats=True)
+            torch.cuda.synchronize()
+            print("guarded", dims, mode, res.count.tolist(), res.terminated_by.tolist())
+
+
 if __name__ == "__main__":
+    run_group_and_guarded()
     run((256, 256), 40)
     run((512, 512), 60, k_cap=128)
     run((1024, 2048), 50, B=2, k_cap=256)
