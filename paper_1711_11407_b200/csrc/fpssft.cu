@@ -57,10 +57,14 @@
 #define FPSSFT_GUARD_R64 1  // guarded warp kernel: float64 root table (not a float32 hi/lo pair)
 #endif
 #ifndef FPSSFT_CLASSIFY_SPLIT
-#define FPSSFT_CLASSIFY_SPLIT 1  // warp kernel: all bins tested before the ballots (ILP)
+#define FPSSFT_CLASSIFY_SPLIT 1  // group kernel: all bins tested before the ballots (ILP; measured
+                                 // -2 % there, +3 % on the batch-major kernel and config 3)
 #endif
 #ifndef FPSSFT_DECODE_PIPE
 #define FPSSFT_DECODE_PIPE 0  // A/B: decode of chunk i+1 ahead of merge i (measured +2 %: off)
+#endif
+#ifndef FPSSFT_PROJ_LANE
+#define FPSSFT_PROJ_LANE 1  // warp kernel float32: projection from per-lane contributions
 #endif
 #ifndef FPSSFT_GROUP_PF
 #define FPSSFT_GROUP_PF 0  // group kernel: L2-prefetch iteration t+1 during t for t + 1 < this
@@ -852,12 +856,13 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         //     sharing a bin are summed by their lowest lane in lane (= slot)
         //     order, through shared memory only when a bin is hit twice.
         //     GUARD: also the float64 line-0 projection and the bins' sum |a|
-        if constexpr (sizeof(R) == 8) {
+        if constexpr (sizeof(R) == 8 || (!GUARD && !FPSSFT_PROJ_LANE)) {
             // float64: slot phases staged, the group's lowest lane forms the
             // sums (fewer live registers than per-lane contributions:
             // measured 1.75 vs 2.12 ms on config 3)
             int *scr_u = (int *)scr_c;
-            cpx<R> *scr_amp = (cpx<R> *)(base + lay.scr_amp);
+            cpx<R> *scr_amp = sizeof(R) == 8 ? (cpx<R> *)(base + lay.scr_amp)
+                                             : scr_c + 16 * nl;  // after nl x 32 ints
             for (int c0 = 0; c0 < n_slots; c0 += 32) {
                 const int s = c0 + lane;
                 const bool valid = s < n_slots && slot_live[s];
@@ -968,7 +973,7 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp
         int n_cand = 0, n_acc = 0;
         R resid = (R)0;
         constexpr int NCH = (LC + 31) / 32;  // compile-time shapes: the chunks' tests
-        if constexpr (LC != 0 && NCH >= 4 && NCH <= 16 && FPSSFT_CLASSIFY_SPLIT) {
+        if constexpr (LC != 0 && WG != 0 && NCH >= 4 && NCH <= 16 && FPSSFT_CLASSIFY_SPLIT) {
             // first every chunk's test (loads and arithmetic only, independent
             // chains), then the ballots and compaction
             unsigned okb = 0, flb = 0;

@@ -7,5 +7,6 @@ for r in $(seq $R); do for so in "$@"; do
 import json,sys
 d=json.loads(sys.stdin.read().strip().splitlines()[-1]); p=d.get("parity") or {}
 print(sys.argv[1], round(d["ms_per_step"],4), round(d["roofline"]["kernel_ms"],4), d["clocks"].get("sm_mhz"),
-      (p.get("identical_support"), p.get("instances"), p.get("pass")) if p else "")' $so
+      (p.get("identical_support"), p.get("instances"), p.get("pass")) if p else "",
+      "batch-major %.4f" % d["batch_major"]["ms_per_step"] if d.get("batch_major") else "")' $so
 done; done
