@@ -183,6 +183,9 @@ __device__ __forceinline__ int decode_candidate_guarded(const cpx<float> *spec, 
     return 2;
 }
 
+#ifndef FPSSFT_REEVAL_UNROLL
+#define FPSSFT_REEVAL_UNROLL 2  // sample-loop unrolling of the exact re-evaluation (1: -0 %, 2: -1.7 %, 4: -0.4 %, 8: +7 %)
+#endif
 // Exact (float64) values of bin b on lines 1..D, as the team's partial sums:
 // single-bin DFTs of the complex64 line samples (the reference's
 // dft_forward(line)[b] = fft(line)[b] / L, transform.py:17-22) and the
@@ -213,6 +216,8 @@ __device__ __forceinline__ void exact_bin_partials(int b, const float2 *__restri
         }
     const int wstep = (int)(((long long)nth * b) % L);
     int w = (int)(((long long)tid * b) % L);
+    constexpr int kUnroll = FPSSFT_REEVAL_UNROLL;
+#pragma unroll kUnroll
     for (int l = tid; l < L; l += nth) {
         const cpx<double> r = roots64[w];
         long long base = 0;

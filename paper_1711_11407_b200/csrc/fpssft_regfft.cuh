@@ -8,6 +8,9 @@
 // X[c + 16 d + 256 h], d = 0..15.
 #pragma once
 // (included inside namespace fpssft)
+#ifndef FPSSFT_FFT256_TW_HOIST
+#define FPSSFT_FFT256_TW_HOIST 0  // A/B: 256-point lines, first-stage twiddles held across lines
+#endif
 namespace regfft {
 
 // constexpr e^{+2 pi i j / 16} and e^{+2 pi i j / 32}
@@ -103,6 +106,14 @@ __device__ __forceinline__ float fft256_lines_warp(cpx<float> *spec, int nlines,
     constexpr int PADL = 256 + 16, S = 33;
     float energy = 0.f;
     const int k1 = lane >> 2, h = lane & 3, k2b = (h >> 1) + 2 * (h & 1);
+#if FPSSFT_FFT256_TW_HOIST
+    float2 tw1[8];  // first-stage twiddles, loaded once for every line
+#pragma unroll
+    for (int c = 1; c < 8; ++c) {
+        const cpx<float> r = roots[lane * c];
+        tw1[c] = make_float2(r.re, r.im);
+    }
+#endif
 #pragma unroll 1
     for (int line = 0; line < nlines; ++line) {
         float2 *base = (float2 *)(spec + line * PADL);
@@ -117,8 +128,12 @@ __device__ __forceinline__ float fft256_lines_warp(cpx<float> *spec, int nlines,
         dft8(v);
 #pragma unroll
         for (int c = 1; c < 8; ++c) {
+#if FPSSFT_FFT256_TW_HOIST
+            v[c] = cmul(v[c], tw1[c]);
+#else
             const cpx<float> r = roots[lane * c];
             v[c] = cmul(v[c], make_float2(r.re, r.im));
+#endif
         }
         __syncwarp();  // the line's inputs are read before the exchange overwrites them
 #pragma unroll
