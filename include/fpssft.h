@@ -175,6 +175,32 @@ int fpssft_project_onto_bins(const int32_t *freqs, const double *amps, const int
                              int32_t precision, void *stream);
 
 /*
+ * The recovery loop of ONE large problem, device-resident (driver.py:121-212
+ * for recovered sets / lines beyond one CTA's shared memory: the imaging
+ * duality path, 512 x 576 cubes, L = 4608, ~20k entries; reference
+ * imaging.py:104-143 calls fps_sft on such a cube).  The whole loop is one
+ * CUDA graph launch: a conditional WHILE node whose body is one iteration
+ * (gather, DFT, peel, classify, merge, termination); the device sets the
+ * loop condition, the host waits once at the end.  float64 only
+ * (params->precision = FPSSFT_F64).
+ *   cube:      one complex64 (FPSSFT_F32) or complex128 (FPSSFT_F64) cube,
+ *              strides from shape->strides.
+ *   schedule:  [params->t_max, 2, D] int32 (alpha, tau) per iteration.
+ *   workspace: device buffer of fpssft_recover_large_workspace(shape, k_cap)
+ *              bytes (k_cap = params->k_cap).
+ *   freqs [k_cap, D] int32, amps [k_cap, 2] double: the live entries in
+ *   insertion order (the reference dict's); count, iterations,
+ *   samples_used, terminated_by: scalars; iter_stats [t_max, 3] or NULL.
+ * Blocks until the loop has finished (synchronises `stream`).
+ */
+int64_t fpssft_recover_large_workspace(const fpssft_shape *shape, int32_t k_cap);
+int fpssft_recover_large(const void *cube, int32_t cube_precision, const fpssft_shape *shape,
+                         const fpssft_params *params, const int32_t *schedule, void *workspace,
+                         int64_t workspace_bytes, int32_t *freqs, double *amps, int32_t *count,
+                         int32_t *iterations, int64_t *samples_used, int32_t *terminated_by,
+                         int32_t *iter_stats, void *stream);
+
+/*
  * Dense re-synthesis of recovered spectra on the full grid (config 5's
  * "inverse-synthesise each image"): for every instance b
  *   cube_b[n] = sum_{i < counts[b]} amps[b,i] * exp(+2 pi j sum_k n_k freqs[b,i,k] / N_k)

@@ -21,7 +21,7 @@ TERM_NAMES = {0: "residual_clean", 1: "stall", 2: "max_iterations", 3: "k_cap_ov
               -1: "invalid_schedule"}
 
 EXPORTS = ("fpssft_run_batch", "fpssft_run_batch_grouped", "fpssft_line_spectra", "fpssft_gather_lines", "fpssft_dft_forward",
-           "fpssft_synthesize",
+           "fpssft_synthesize", "fpssft_recover_large", "fpssft_recover_large_workspace",
            "fpssft_decode_spectra", "fpssft_project_onto_bins", "fpssft_smem_bytes",
            "fpssft_block_threads", "fpssft_plan", "fpssft_plan_batch", "fpssft_launches_per_batch",
            "fpssft_set_l2_fetch_granularity", "fpssft_get_l2_fetch_granularity", "fpssft_last_error",
@@ -78,6 +78,10 @@ def lib() -> C.CDLL:
         h.fpssft_project_onto_bins.argtypes = [P, P, P, I64, I32, C.POINTER(Shape), P, I32, P,
                                                I32, P]
         h.fpssft_synthesize.argtypes = [P, P, P, I64, I32, C.POINTER(Shape), P, I64, I32, P]
+        h.fpssft_recover_large_workspace.argtypes = [C.POINTER(Shape), I32]
+        h.fpssft_recover_large_workspace.restype = I64
+        h.fpssft_recover_large.argtypes = [P, I32, C.POINTER(Shape), C.POINTER(Params), P, P,
+                                           I64, P, P, P, P, P, P, P, P]
         h.fpssft_smem_bytes.argtypes = [C.POINTER(Shape), C.POINTER(Params)]
         h.fpssft_smem_bytes.restype = C.c_size_t
         h.fpssft_block_threads.argtypes = [C.POINTER(Shape), I32]
@@ -90,7 +94,8 @@ def lib() -> C.CDLL:
         h.fpssft_get_l2_fetch_granularity.argtypes = []
         h.fpssft_last_error.restype = C.c_char_p
         for name in EXPORTS:
-            if name not in ("fpssft_smem_bytes", "fpssft_last_error"):
+            if name not in ("fpssft_smem_bytes", "fpssft_last_error",
+                            "fpssft_recover_large_workspace"):
                 getattr(h, name).restype = C.c_int
         _lib = h
     return _lib

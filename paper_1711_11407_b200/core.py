@@ -103,10 +103,22 @@ class SparseSpectrum:
         self.shape = shape
         freqs = np.asarray(freqs, np.int64).reshape(-1, shape.ndim)
         amps = np.asarray(amps, np.complex128).reshape(-1)
-        self.entries = dict(zip(map(tuple, freqs.tolist()), amps.tolist()))
+        self.__dict__["_entries"] = None  # the dict is built on first use (large sets)
         self.__dict__["freq_array"] = freqs  # cached_property values, already at hand
         self.__dict__["amp_array"] = amps
         return self
+
+    @property
+    def entries(self) -> dict:
+        e = self.__dict__.get("_entries")
+        if e is None:
+            e = dict(zip(map(tuple, self.freq_array.tolist()), self.amp_array.tolist()))
+            self.__dict__["_entries"] = e
+        return e
+
+    @entries.setter
+    def entries(self, value) -> None:
+        self.__dict__["_entries"] = value
 
     @classmethod
     def from_sinusoids(cls, shape: CubeShape, sinusoids: Iterable[Sinusoid]) -> "SparseSpectrum":

@@ -16,6 +16,8 @@
 #include <functional>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <vector>
 #include <numeric>
 #include <string>
 #include <type_traits>
@@ -1587,7 +1589,8 @@ __global__ void __launch_bounds__(1024, 1) decode_kernel(const cpx<R> *__restric
                                                       const int *__restrict__ alpha_tau,
                                                       int per_instance, Knobs kn, double floor,
                                                       int *status, int *freqs, double *amps,
-                                                      int *n_candidates) {
+                                                      int *n_candidates,
+                                                      const double *floor_dev = nullptr) {
     extern __shared__ __align__(16) unsigned char sm[];
     cpx<R> *spec = GLOBAL ? nullptr : (cpx<R> *)sm;
     cpx<R> *roots = GLOBAL ? (cpx<R> *)sm : spec + (size_t)g.nlines * g.L;
@@ -1610,7 +1613,7 @@ __global__ void __launch_bounds__(1024, 1) decode_kernel(const cpx<R> *__restric
     }
     __syncthreads();
     const cpx<R> *sp = GLOBAL ? src : spec;
-    R fl = (R)floor;
+    R fl = (R)(floor_dev ? *floor_dev : floor);  // the device loop keeps its floor on chip
     if (sizeof(R) == 4 && kn.noise_coef > 0)  // sum |x|^2 = L sum |S|^2 (Parseval)
         fl = max(fl, (R)kn.noise_coef * sqrt((R)L * block_sum(my_e, (R *)(ired + 32))));
     int my = 0;
@@ -1671,6 +1674,7 @@ __global__ void __launch_bounds__(1024, 1) project_kernel(const int *__restrict_
 }
 
 #include "fpssft_large.cuh"
+#include "fpssft_loop.cuh"
 
 // ================================================================== host
 namespace {
@@ -2226,6 +2230,219 @@ size_t spec_smem(const Geo &g, int nlines, int cs) {
     return align16((size_t)(nlines + 1) * g.L * cs) + 64 * 8;
 }
 
+// The classifier launch shared by fpssft_decode_spectra and the device loop
+// (floor_dev: the energy floor read on the device, else `floor`).
+int launch_decode(const void *spectra, int64_t batch, Geo g, const Knobs &kn,
+                  int precision, const int32_t *alpha_tau, int per_instance, double floor,
+                  const double *floor_dev, int32_t *status, int32_t *freqs, double *amps,
+                  int32_t *n_candidates, cudaStream_t st) {
+    cudaError_t e;
+    const int cs = precision == FPSSFT_F64 ? 16 : 8;
+    const int nt = block_threads(g, g.nlines, precision);
+    if (nt < 0 || (long long)spec_smem(g, g.nlines, cs) > max_smem_optin()) {
+        // long lines: classify straight from global memory, roots on chip
+        const size_t sm = align16((size_t)g.L * cs) + 64 * 8;
+        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
+        if (precision == FPSSFT_F64) {
+            e = cudaFuncSetAttribute(decode_kernel<double, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+            decode_kernel<double, true><<<(unsigned)batch, 1024, sm, st>>>(
+                (const cpx<double> *)spectra, g, alpha_tau, per_instance, kn, floor, status,
+                freqs, amps, n_candidates, floor_dev);
+        } else {
+            e = cudaFuncSetAttribute(decode_kernel<float, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+            decode_kernel<float, true><<<(unsigned)batch, 1024, sm, st>>>(
+                (const cpx<float> *)spectra, g, alpha_tau, per_instance, kn, floor, status,
+                freqs, amps, n_candidates, floor_dev);
+        }
+        return check_launch("decode_kernel");
+    }
+    if (precision == FPSSFT_F64) {
+        const size_t sm = spec_smem(g, g.nlines, 16);
+        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
+        e = cudaFuncSetAttribute(decode_kernel<double>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        decode_kernel<double><<<(unsigned)batch, nt, sm, st>>>(
+            (const cpx<double> *)spectra, g, alpha_tau, per_instance, kn, floor, status, freqs,
+            amps, n_candidates, floor_dev);
+    } else {
+        const size_t sm = spec_smem(g, g.nlines, 8);
+        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
+        e = cudaFuncSetAttribute(decode_kernel<float>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        decode_kernel<float><<<(unsigned)batch, nt, sm, st>>>(
+            (const cpx<float> *)spectra, g, alpha_tau, per_instance, kn, floor, status, freqs,
+            amps, n_candidates, floor_dev);
+    }
+    return check_launch("decode_kernel");
+}
+
+
+// The device-resident large-problem loop (fpssft_loop.cuh): the
+// conditional-WHILE graph for one set of buffers is built and instantiated
+// once and kept (a small cache keyed by every pointer and parameter it bakes
+// in, guarded by a mutex: a repeated call -- the imaging path re-running the
+// same shape through the same buffers -- only re-launches it).  Each call:
+// init kernel, graph launch, compaction kernel, one wait.
+struct LargeGraph {
+    std::vector<unsigned char> key;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t cs = nullptr;
+};
+std::mutex g_large_mu;
+LargeGraph g_large_cache[4];
+int g_large_next = 0;
+
+void large_graph_free(LargeGraph &c) {
+    if (c.exec) cudaGraphExecDestroy(c.exec);
+    if (c.graph) cudaGraphDestroy(c.graph);
+    if (c.cs) cudaStreamDestroy(c.cs);
+    c = LargeGraph{};
+}
+
+int build_large_graph(const void *cube, int cube_precision, const fpssft_shape *shape,
+                      const Geo &g, const Knobs &kn, const int32_t *schedule, unsigned char *ws,
+                      const LargeWs &w, int32_t *iter_stats, LargeGraph &out) {
+    LargeState *stt = (LargeState *)(ws + w.state);
+    int *at_all = (int *)(ws + w.at_all);
+    cpx<double> *spec = (cpx<double> *)(ws + w.spec);
+    double *proj = (double *)(ws + w.proj);
+    int *status = (int *)(ws + w.status), *dfreqs = (int *)(ws + w.dfreqs);
+    double *damps = (double *)(ws + w.damps);
+    int *ncand = (int *)(ws + w.ncand), *slot_of = (int *)(ws + w.slot_of);
+    int *sfreqs = (int *)(ws + w.sfreqs);
+    double *samps = (double *)(ws + w.samps);
+    const int L = g.L, nl = g.nlines;
+    LargeGraph c;
+    cudaError_t e;
+#define LARGE_TRY(call, what)                   \
+    do {                                        \
+        e = (call);                             \
+        if (e != cudaSuccess) {                 \
+            large_graph_free(c);                \
+            return cuda_fail(e, what);          \
+        }                                       \
+    } while (0)
+    LARGE_TRY(cudaGraphCreate(&c.graph, 0), "cudaGraphCreate");
+    cudaGraphConditionalHandle cond;
+    LARGE_TRY(cudaGraphConditionalHandleCreate(&cond, c.graph, 1, cudaGraphCondAssignDefault),
+              "cudaGraphConditionalHandleCreate");
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    LARGE_TRY(cudaGraphAddNode(&cnode, c.graph, nullptr, 0, &cp), "cudaGraphAddNode(while)");
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    LARGE_TRY(cudaStreamCreateWithFlags(&c.cs, cudaStreamNonBlocking), "cudaStreamCreate");
+    LARGE_TRY(cudaStreamBeginCaptureToGraph(c.cs, body, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeThreadLocal),
+              "cudaStreamBeginCaptureToGraph");
+    // ---- one iteration
+    large_setup_kernel<<<1, 32, 0, c.cs>>>(schedule, g, kn, stt, at_all);
+    int rc = fpssft_gather_lines(cube, cube_precision, 1, 0, shape, at_all, 0, spec, FPSSFT_F64,
+                                 c.cs);
+    if (rc == FPSSFT_OK) rc = fpssft_dft_forward(spec, nl, L, spec, FPSSFT_F64, c.cs);
+    if (rc == FPSSFT_OK) {
+        constexpr int PBT = 64, PCAP = 512;
+        large_project_kernel<PBT, PCAP><<<(unsigned)((L + PBT - 1) / PBT), PBT, 0, c.cs>>>(
+            sfreqs, samps, stt, g, at_all, proj);
+        rc = check_launch("large_project_kernel");
+    }
+    if (rc == FPSSFT_OK) {
+        large_subtract_kernel<<<(unsigned)std::min(1184, (nl * L + 255) / 256), 256, 0, c.cs>>>(
+            spec, proj, nl * L, stt);
+        rc = launch_decode(spec, 1, g, kn, FPSSFT_F64, at_all, 0, 0.0, &stt->floor, status,
+                           dfreqs, damps, ncand, c.cs);
+    }
+    if (rc == FPSSFT_OK) {
+        large_merge_kernel<<<1, LARGE_NT, 0, c.cs>>>(spec, status, dfreqs, damps, ncand, at_all,
+                                                     g, kn, stt, slot_of, sfreqs, samps,
+                                                     iter_stats, cond);
+        rc = check_launch("large_merge_kernel");
+    }
+    cudaGraph_t captured = nullptr;
+    e = cudaStreamEndCapture(c.cs, &captured);
+    if (rc != FPSSFT_OK) {
+        large_graph_free(c);
+        return rc;
+    }
+    if (e != cudaSuccess) {
+        large_graph_free(c);
+        return cuda_fail(e, "cudaStreamEndCapture");
+    }
+    LARGE_TRY(cudaGraphInstantiate(&c.exec, c.graph, 0), "cudaGraphInstantiate");
+#undef LARGE_TRY
+    out = c;
+    return FPSSFT_OK;
+}
+
+int run_large(const void *cube, int cube_precision, const fpssft_shape *shape, const Geo &g,
+              const Knobs &kn, const int32_t *schedule, unsigned char *ws, const LargeWs &w,
+              int32_t *freqs, double *amps, int32_t *count, int32_t *iterations,
+              int64_t *samples_used, int32_t *terminated_by, int32_t *iter_stats,
+              cudaStream_t st) {
+    // everything the graph bakes in
+    std::vector<unsigned char> key;
+    auto put = [&key](const void *p, size_t n) {
+        key.insert(key.end(), (const unsigned char *)p, (const unsigned char *)p + n);
+    };
+    int dev = 0;
+    cudaGetDevice(&dev);
+    put(&dev, sizeof dev);
+    put(&cube, sizeof cube);
+    put(&cube_precision, sizeof cube_precision);
+    put(&shape->ndim, sizeof shape->ndim);
+    put(shape->dims, sizeof(shape->dims[0]) * shape->ndim);
+    put(shape->strides, sizeof(shape->strides[0]) * shape->ndim);
+    put(&kn, sizeof kn);
+    put(&schedule, sizeof schedule);
+    put(&ws, sizeof ws);
+    put(&iter_stats, sizeof iter_stats);
+    LargeState *stt = (LargeState *)(ws + w.state);
+    int *slot_of = (int *)(ws + w.slot_of);
+    long long n_total = 1;
+    for (int k = 0; k < g.D; ++k) n_total *= g.N[k];
+    std::lock_guard<std::mutex> lock(g_large_mu);
+    LargeGraph *c = nullptr;
+    for (auto &e : g_large_cache)
+        if (e.exec && e.key == key) c = &e;
+    if (!c) {
+        LargeGraph fresh;
+        const int rc = build_large_graph(cube, cube_precision, shape, g, kn, schedule, ws, w,
+                                         iter_stats, fresh);
+        if (rc != FPSSFT_OK) return rc;
+        fresh.key = key;
+        LargeGraph &slot = g_large_cache[g_large_next];
+        g_large_next = (g_large_next + 1) % 4;
+        cudaStreamSynchronize(slot.cs ? slot.cs : st);  // (never running: launches are waited)
+        large_graph_free(slot);
+        slot = fresh;
+        c = &slot;
+    }
+    large_init_kernel<<<(unsigned)std::min<long long>((n_total + 255) / 256, 1184), 256, 0, st>>>(
+        stt, slot_of, n_total, kn.t_max);
+    int rc = check_launch("large_init_kernel");
+    if (rc != FPSSFT_OK) return rc;
+    cudaError_t e = cudaGraphLaunch(c->exec, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
+    large_final_kernel<<<1, LARGE_NT, 0, st>>>(stt, slot_of, (const int *)(ws + w.sfreqs),
+                                               (const double *)(ws + w.samps), g, freqs, amps,
+                                               count, iterations, (long long *)samples_used,
+                                               terminated_by);
+    rc = check_launch("large_final_kernel");
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize(large loop)");
+    return rc;
+}
+
 }  // namespace
 }  // namespace fpssft
 
@@ -2275,6 +2492,39 @@ int fpssft_guard_reasons(unsigned long long *out) {
 }
 #endif
 #endif
+
+/* Device-resident loop for one large problem: see include/fpssft.h. */
+int64_t fpssft_recover_large_workspace(const fpssft_shape *shape, int32_t k_cap) {
+    Geo g;
+    if (make_geo(shape, &g) != FPSSFT_OK) return -1;
+    if (k_cap < 1) return -1;
+    return (int64_t)large_ws(g, k_cap).total;
+}
+
+int fpssft_recover_large(const void *cube, int32_t cube_precision, const fpssft_shape *shape,
+                         const fpssft_params *params, const int32_t *schedule, void *workspace,
+                         int64_t workspace_bytes, int32_t *freqs, double *amps, int32_t *count,
+                         int32_t *iterations, int64_t *samples_used, int32_t *terminated_by,
+                         int32_t *iter_stats, void *stream) {
+    Geo g;
+    Knobs kn;
+    int rc;
+    if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
+    if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
+    if (params->precision != FPSSFT_F64)
+        return fail(FPSSFT_EUNSUPPORTED, "the device-resident large loop runs in float64");
+    if (cube_precision != FPSSFT_F32 && cube_precision != FPSSFT_F64)
+        return fail(FPSSFT_EINVAL, "cube_precision must be FPSSFT_F32 or FPSSFT_F64");
+    if (!cube || !schedule || !workspace || !freqs || !amps || !count || !iterations ||
+        !samples_used || !terminated_by)
+        return fail(FPSSFT_EINVAL, "NULL buffer");
+    const LargeWs w = large_ws(g, kn.k_cap);
+    if (workspace_bytes < (int64_t)w.total)
+        return fail(FPSSFT_EINVAL, "workspace smaller than fpssft_recover_large_workspace()");
+    return run_large(cube, cube_precision, shape, g, kn, schedule, (unsigned char *)workspace, w,
+                     freqs, amps, count, iterations, samples_used, terminated_by, iter_stats,
+                     (cudaStream_t)stream);
+}
 
 int fpssft_set_l2_fetch_granularity(int32_t bytes) {
     if (bytes < 0 || bytes > 128 || (bytes & (bytes - 1)))
@@ -2589,51 +2839,8 @@ int fpssft_decode_spectra(const void *spectra, int64_t batch, const fpssft_shape
     if (batch == 0) return FPSSFT_OK;
     if (!spectra || !alpha_tau || !status || !freqs || !amps || !n_candidates)
         return fail(FPSSFT_EINVAL, "NULL buffer");
-    cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e;
-    const int cs = params->precision == FPSSFT_F64 ? 16 : 8;
-    const int nt = block_threads(g, g.nlines, params->precision);
-    if (nt < 0 || (long long)spec_smem(g, g.nlines, cs) > max_smem_optin()) {
-        // long lines: classify straight from global memory, roots on chip
-        const size_t sm = align16((size_t)g.L * cs) + 64 * 8;
-        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
-        if (params->precision == FPSSFT_F64) {
-            e = cudaFuncSetAttribute(decode_kernel<double, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-            decode_kernel<double, true><<<(unsigned)batch, 1024, sm, st>>>(
-                (const cpx<double> *)spectra, g, alpha_tau, per_instance, kn, floor, status,
-                freqs, amps, n_candidates);
-        } else {
-            e = cudaFuncSetAttribute(decode_kernel<float, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-            decode_kernel<float, true><<<(unsigned)batch, 1024, sm, st>>>(
-                (const cpx<float> *)spectra, g, alpha_tau, per_instance, kn, floor, status,
-                freqs, amps, n_candidates);
-        }
-        return check_launch("decode_kernel");
-    }
-    if (params->precision == FPSSFT_F64) {
-        const size_t sm = spec_smem(g, g.nlines, 16);
-        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
-        e = cudaFuncSetAttribute(decode_kernel<double>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-        decode_kernel<double><<<(unsigned)batch, nt, sm, st>>>(
-            (const cpx<double> *)spectra, g, alpha_tau, per_instance, kn, floor, status, freqs,
-            amps, n_candidates);
-    } else {
-        const size_t sm = spec_smem(g, g.nlines, 8);
-        if ((long long)sm > max_smem_optin()) return fail(FPSSFT_EUNSUPPORTED, "L too large");
-        e = cudaFuncSetAttribute(decode_kernel<float>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-        decode_kernel<float><<<(unsigned)batch, nt, sm, st>>>(
-            (const cpx<float> *)spectra, g, alpha_tau, per_instance, kn, floor, status, freqs,
-            amps, n_candidates);
-    }
-    return check_launch("decode_kernel");
+    return launch_decode(spectra, batch, g, kn, params->precision, alpha_tau, per_instance, floor,
+                         nullptr, status, freqs, amps, n_candidates, (cudaStream_t)stream);
 }
 
 int fpssft_project_onto_bins(const int32_t *freqs, const double *amps, const int32_t *counts,

@@ -112,7 +112,7 @@ def dense_dft(pixels: np.ndarray, device=None):
 
 
 def reconstruct_sparse_image(img_sparse: GrayImage, config: FpsSftConfig = FpsSftConfig(), *,
-                             device=None) -> tuple[GrayImage, RecoveryReport]:
+                             device=None, loop: str = "device") -> tuple[GrayImage, RecoveryReport]:
     """Recover a pixel-sparse image from samples of its frequency cube
     (imaging.py:104-143): absolute tolerances rescaled by 1/N, the iteration
     cap opened up from the pixel count when ``max_iterations`` is None, and
@@ -126,7 +126,7 @@ def reconstruct_sparse_image(img_sparse: GrayImage, config: FpsSftConfig = FpsSf
         cfg = replace(cfg, max_iterations=max(default_max_iterations(shape),
                                               math.ceil(4 * k / shape.line_len) + 20))
     xhat = dense_dft(img_sparse.pixels, device)
-    report = fps_sft_large(xhat, shape, cfg, precision="fp64")
+    report = fps_sft_large(xhat, shape, cfg, precision="fp64", loop=loop)
     out = np.zeros(shape.dims)
     freqs, values = report.recovered.freq_array, report.recovered.amp_array * n
     bad = np.flatnonzero(np.abs(values.imag) > IMAG_RESIDUE_TOL)

@@ -18,8 +18,11 @@ The loop is the reference's (``driver.py:121-212``, restated step for step in
   peel the new entries,     device projection + max|S| (driver.py:189-204)
   termination
 
-Every step runs on the device except the merge bookkeeping (numpy over the
-accepted entries); there is no CPU fallback.
+Default: the whole loop is one CUDA graph launch on the device
+(``fpssft_recover_large``, csrc/fpssft_loop.cuh: a conditional WHILE node;
+merge, amp_sum, residual and termination on the device, one host wait).
+``loop="host"`` keeps the round-1 host-driven path (device steps, numpy merge)
+for A/B.  There is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -29,7 +32,7 @@ import numpy as np
 from . import _native as N
 from . import ops
 from .core import CubeShape, SparseSpectrum
-from .driver import (TERMINATED_MAX_ITERATIONS, TERMINATED_RESIDUAL_CLEAN, TERMINATED_STALL,
+from .driver import (TERMINATED_MAX_ITERATIONS, TERMINATED_RESIDUAL_CLEAN, TERMINATED_STALL, _params,
                      C_ref, FpsSftConfig, IterationStats, RecoveryReport, _precision_code,
                      default_max_iterations)
 from .schedule import schedule_from_seed
@@ -148,10 +151,97 @@ def _project(shape, freqs, amps, count, k_cap, at, out, precision, device, shape
 
 
 def fps_sft_large(cube, shape: CubeShape | None = None, config: FpsSftConfig = FpsSftConfig(),
-                  *, precision: str = "fp64", schedule=None) -> RecoveryReport:
+                  *, precision: str = "fp64", schedule=None, loop: str = "device",
+                  k_cap: int | None = None) -> RecoveryReport:
     """``fps_sft`` for a single large problem (CUDA tensor ``cube``).  Same
     arguments, defaults, schedule and report as the reference's entry point;
-    float64 by default (the imaging path compares pixels to 1e-6)."""
+    float64 by default (the imaging path compares pixels to 1e-6).
+
+    ``loop="device"`` (default, float64): the whole loop is one CUDA graph
+    launch (``fpssft_recover_large``: a conditional WHILE node, the device
+    decides termination, one host wait); ``loop="host"``: the host drives one
+    device step per launch (the round-1 path, kept for A/B)."""
+    if loop == "device" and _precision_code(precision) == N.F64:
+        return _fps_sft_large_device(cube, shape, config, schedule, k_cap)
+    if loop not in ("device", "host"):
+        raise ValueError('loop must be "device" or "host"')
+    return _fps_sft_large_host(cube, shape, config, precision=precision, schedule=schedule)
+
+
+_RUNNERS: dict = {}  # persistent device buffers of the device loop, by shape
+
+
+def _fps_sft_large_device(cube, shape, config, schedule, k_cap):
+    """The device-resident loop (csrc/fpssft_loop.cuh)."""
+    import torch
+
+    shape = shape or CubeShape(tuple(cube.shape))
+    if tuple(cube.shape) != shape.dims:
+        raise ValueError(f"cube extents {tuple(cube.shape)} do not match {shape.dims}")
+    if cube.dtype not in (torch.complex64, torch.complex128):
+        raise TypeError("cube must be complex64 or complex128")
+    if not cube.is_cuda:
+        raise ValueError("cube must be a CUDA tensor")
+    D, L = shape.ndim, shape.line_len
+    dev = cube.device
+    t_max = config.max_iterations or default_max_iterations(shape)
+    if schedule is None:
+        schedule = schedule_from_seed(shape, config.seed, t_max)
+    schedule = np.ascontiguousarray(np.asarray(schedule, np.int32)[:t_max])
+    if schedule.shape != (t_max, 2, D):
+        raise ValueError(f"schedule must be [{t_max}, 2, {D}]")
+    if k_cap is None:  # every slot a key may take, incl. re-appends after pruning
+        k_cap = 1 << int(2 * shape.n_total - 1).bit_length()
+    # persistent buffers per (device, shape, dtype, k_cap, t_max): the cube and
+    # schedule are copied into them, so every pointer the library's graph bakes
+    # in is stable and a repeated call only re-launches the cached graph
+    rk = (str(dev), shape.dims, cube.dtype, k_cap, t_max)
+    r = _RUNNERS.get(rk)
+    lib = N.lib()
+    if r is None:
+        sh = N.make_shape(shape.dims)
+        ws_bytes = int(lib.fpssft_recover_large_workspace(C_ref(sh), k_cap))
+        if ws_bytes < 0:
+            N.check(-1)
+        r = dict(sh=sh, ws_bytes=ws_bytes,
+                 ws=torch.empty(ws_bytes, dtype=torch.uint8, device=dev),
+                 cube=torch.empty(shape.dims, dtype=cube.dtype, device=dev),
+                 sched=torch.empty((t_max, 2, D), dtype=torch.int32, device=dev),
+                 freqs=torch.empty((k_cap, D), dtype=torch.int32, device=dev),
+                 amps=torch.empty(k_cap, dtype=torch.complex128, device=dev),
+                 scal=torch.zeros(3, dtype=torch.int32, device=dev),  # count, iterations, term
+                 samples=torch.zeros(1, dtype=torch.int64, device=dev),
+                 stats=torch.zeros((t_max, 3), dtype=torch.int32, device=dev))
+        if len(_RUNNERS) >= 4:
+            _RUNNERS.pop(next(iter(_RUNNERS)))
+        _RUNNERS[rk] = r
+    r["cube"].copy_(cube)
+    r["sched"].copy_(torch.as_tensor(schedule))
+    params = _params(config, t_max, k_cap, N.F64)
+    cube_prec = N.F64 if cube.dtype == torch.complex128 else N.F32
+    scal, samples, stats, freqs, amps = r["scal"], r["samples"], r["stats"], r["freqs"], r["amps"]
+    N.check(lib.fpssft_recover_large(N.ptr(r["cube"]), cube_prec, C_ref(r["sh"]), C_ref(params),
+                                     N.ptr(r["sched"]), N.ptr(r["ws"]), r["ws_bytes"],
+                                     N.ptr(freqs), N.ptr(amps), N.ptr(scal), N.ptr(scal[1:]),
+                                     N.ptr(samples), N.ptr(scal[2:]), N.ptr(stats),
+                                     N.stream_ptr(dev)))
+    count, its, term = (int(v) for v in scal.cpu())
+    f = freqs[:count].cpu().numpy().astype(np.int64)
+    a = amps[:count].cpu().numpy()
+    st = stats[:its].cpu().numpy()
+    log = tuple(IterationStats(t + 1, tuple(int(v) for v in schedule[t, 0]),
+                               tuple(int(v) for v in schedule[t, 1]), int(st[t, 0]),
+                               int(st[t, 1]), int(st[t, 2])) for t in range(its))
+    order = np.lexsort(f.T[::-1]) if count else np.zeros(0, np.int64)
+    return RecoveryReport(iterations_run=its, samples_used=int(samples.item()),
+                          recovered=SparseSpectrum._trusted(shape, f[order], a[order]),
+                          terminated_by=N.TERM_NAMES[term], iteration_log=log)
+
+
+def _fps_sft_large_host(cube, shape: CubeShape | None = None,
+                        config: FpsSftConfig = FpsSftConfig(), *, precision: str = "fp64",
+                        schedule=None) -> RecoveryReport:
+    """Host-driven loop over device steps (one launch per step)."""
     import torch
 
     shape = shape or CubeShape(tuple(cube.shape))

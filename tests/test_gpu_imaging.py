@@ -93,3 +93,44 @@ def test_long_line_spectra_and_large_projection_vs_oracle():
     np.testing.assert_array_equal(acc, bins[keep])
     np.testing.assert_array_equal(fr[0].cpu().numpy()[acc], m[keep])
     assert int(nc[0]) == n_cand
+
+
+@pytest.mark.parametrize("case", GOLD["small"][:3], ids=lambda c: c["name"])
+def test_device_loop_equals_host_loop(case):
+    """The device-resident loop (one graph launch, device merge/termination)
+    and the host-driven loop give the same report: support, amplitudes,
+    iterations, termination and per-iteration log."""
+    px = ARR[f"{case['name']}/pixels"]
+    cfg = P.FpsSftConfig(**case["cfg"])
+    _, dev = I.reconstruct_sparse_image(I.GrayImage(px), cfg, loop="device")
+    _, host = I.reconstruct_sparse_image(I.GrayImage(px), cfg, loop="host")
+    assert dev.iterations_run == host.iterations_run
+    assert dev.terminated_by == host.terminated_by
+    assert dev.samples_used == host.samples_used
+    assert [(s.candidates, s.accepted, s.rejected) for s in dev.iteration_log] == \
+        [(s.candidates, s.accepted, s.rejected) for s in host.iteration_log]
+    np.testing.assert_array_equal(dev.recovered.freq_array, host.recovered.freq_array)
+    np.testing.assert_allclose(dev.recovered.amp_array, host.recovered.amp_array, rtol=1e-12,
+                               atol=1e-15)
+
+
+def test_device_loop_generic_problem_matches_oracle():
+    """fps_sft_large on an ordinary dense cube (device loop, float64) equals
+    the oracle, logs included, and a tiny k_cap overflows cleanly."""
+    from paper_1711_11407_b200 import workloads as W
+    from paper_1711_11407_b200.large import fps_sft_large
+
+    dims = (48, 40)
+    f, a = W.reference_generate(dims, 30, 11)
+    cube = W.synthesize_np(dims, f, a)
+    prof = dict(mag_tol=1e-4, verify_tol=1e-4, residual_stop=1e-6)
+    cfg = P.FpsSftConfig(seed=5, **prof)
+    rep = fps_sft_large(torch.as_tensor(cube).cuda(), P.CubeShape(dims), cfg)
+    ref = O.recover(cube, dims, O.Profile(**prof), seed=5)
+    np.testing.assert_array_equal(rep.recovered.freq_array.reshape(-1, 2), ref.freqs)
+    assert np.abs(rep.recovered.amp_array - ref.amps).max() <= 1e-9 * np.abs(ref.amps).max()
+    assert rep.iterations_run == ref.iterations_run and rep.terminated_by == ref.terminated_by
+    assert [(s.candidates, s.accepted, s.rejected) for s in rep.iteration_log] == \
+        [tuple(int(v) for v in x[2:]) for x in ref.log]
+    small = fps_sft_large(torch.as_tensor(cube).cuda(), P.CubeShape(dims), cfg, k_cap=8)
+    assert small.terminated_by == "k_cap_overflow"

@@ -26,17 +26,18 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--loop", default="device", choices=["device", "host"])
     args = ap.parse_args()
     ph = I.synthetic_phantom((512, 576), 1)
     for level, target in enumerate((0.0285, 0.0448, 0.0661)):
         sparse = I.sparsify(ph, I.threshold_for_fraction(ph, target))
         cfg = FpsSftConfig(stall_limit=10, seed=800 + level)
-        I.reconstruct_sparse_image(sparse, cfg)  # warm-up
+        I.reconstruct_sparse_image(sparse, cfg, loop=args.loop)  # warm-up
         ts = []
         for _ in range(args.reps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            recon, rep = I.reconstruct_sparse_image(sparse, cfg)
+            recon, rep = I.reconstruct_sparse_image(sparse, cfg, loop=args.loop)
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
         err = float(np.abs(recon.pixels - sparse.pixels).max())
@@ -50,7 +51,7 @@ def main():
         xhat = np.fft.fftn(sparse.pixels.astype(np.complex128)) / n
         ref = O.recover(xhat, (512, 576), prof, seed=800 + level)
         cpu = time.perf_counter() - t0
-        print(json.dumps(dict(level=level, k=k, iterations=rep.iterations_run,
+        print(json.dumps(dict(loop=args.loop, level=level, k=k, iterations=rep.iterations_run,
                               terminated_by=rep.terminated_by,
                               percent_samples=rep.percent_samples(), max_pixel_error=err,
                               gpu_s=min(ts), gpu_ms_per_iteration=1e3 * min(ts) / rep.iterations_run,
