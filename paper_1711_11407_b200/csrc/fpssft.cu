@@ -68,6 +68,9 @@
 #ifndef FPSSFT_PROJ_LANE
 #define FPSSFT_PROJ_LANE 1  // warp kernel float32: projection from per-lane contributions
 #endif
+#ifndef FPSSFT_GROUP_MINB
+#define FPSSFT_GROUP_MINB 2  // group kernel: CTAs per SM its registers must allow (3: compact layout)
+#endif
 #ifndef FPSSFT_GROUP_PF
 #define FPSSFT_GROUP_PF 0  // group kernel: L2-prefetch iteration t+1 during t for t + 1 < this
 #endif
@@ -514,14 +517,18 @@ __host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, 
     if (!grouped && stage16_ok(D, L, cs, 32) && spec_bytes < (size_t)(D + 1) * L * 16)
         spec_bytes = (size_t)(D + 1) * L * 16;  // 16-byte staging slots (gather_lines_cg16)
     const size_t sort_bytes = 1024 + (size_t)k_cap * 4;
+    // compact (group kernel at FPSSFT_GROUP_MINB 3 CTAs/SM): hash of k_cap
+    // entries, candidate list inside the projection staging (not live together)
+    const bool compact = grouped && FPSSFT_GROUP_MINB >= 3 && !guard && cs == 8 &&
+                         (size_t)L * 2 <= 32 * (size_t)cs * (size_t)(D + 1);
     size_t o = 0;
-    y.H = 2 * k_cap;
+    y.H = compact ? k_cap : 2 * k_cap;
     y.spec = o;      o = align16(o + (spec_bytes > sort_bytes ? spec_bytes : sort_bytes));
     y.slot_amp = o;  o = align16(o + (size_t)k_cap * acs);
     y.slot_key = o;  o = align16(o + (size_t)k_cap * 4);
     y.hash = o;      o = align16(o + (size_t)y.H * 2);
     y.slot_live = o; o = align16(o + (size_t)k_cap);
-    y.cand = o;      o = align16(o + (size_t)L * 2);
+    y.cand = o;      if (!compact) o = align16(o + (size_t)L * 2);
     // projection staging: per lane, its slot's contribution on every line
     // (and, guarded, the float64 line-0 one and |a|)
     // (float64: the slots' phases and amplitudes instead)
@@ -561,14 +568,14 @@ __device__ __forceinline__ int hash16_find(const unsigned short *hash, const int
         const unsigned short s = hash[h];
         FPSSFT_CHECK(++probes <= H);
         if (s == HASH_EMPTY) return -1;
-        FPSSFT_CHECK((int)s < H / 2);  // H = 2 k_cap
+        FPSSFT_CHECK((int)s < H);  // H = 2 k_cap (k_cap in the compact layout)
         if (slot_key[s] == key) return s;
         h = (h + 1) & (unsigned)(H - 1);
     }
 }
 __device__ __forceinline__ void hash16_insert(unsigned short *hash, int H, int key, int slot) {
     unsigned h = hash32(key) & (unsigned)(H - 1);
-    FPSSFT_CHECK(slot >= 0 && slot < H / 2);
+    FPSSFT_CHECK(slot >= 0 && slot < H);
     [[maybe_unused]] int probes = 0;
     while (atomicCAS(hash + h, HASH_EMPTY, (unsigned short)slot) != HASH_EMPTY) {
         FPSSFT_CHECK(++probes < H);
@@ -612,7 +619,7 @@ __device__ __forceinline__ bool team_bar_or(int id, int n, bool p) {
 // flags on every float32 decision statistic, flagged bins re-evaluated in
 // float64 by the whole warp.
 template <class R, int LC, int DC, bool GUARD = false, int WG = 0, int KC = 0>
-__global__ void __launch_bounds__(FPSSFT_WARP_NT, FPSSFT_WARP_MINB) recover_warp_kernel(const float2 *__restrict__ cubes,
+__global__ void __launch_bounds__(FPSSFT_WARP_NT, WG ? FPSSFT_GROUP_MINB : FPSSFT_WARP_MINB) recover_warp_kernel(const float2 *__restrict__ cubes,
                                                            long long batch, long long batch_stride,
                                                            Geo g_in, Knobs kn,
                                                            const int *__restrict__ schedule,
