@@ -68,6 +68,13 @@
 #ifndef FPSSFT_PROJ_LANE
 #define FPSSFT_PROJ_LANE 1  // warp kernel float32: projection from per-lane contributions
 #endif
+#ifndef FPSSFT_WARP_MINB_SHORT
+#define FPSSFT_WARP_MINB_SHORT 1  // lines of <= 64 points: registers for ILP (config 3 has ~7
+                                  // instances per SM anyway; guarded 1.344 -> 1.221 ms)
+#endif
+#ifndef FPSSFT_PROJ_X2
+#define FPSSFT_PROJ_X2 0  // A/B: lines of <= 64 points, projection two chunks at a time (+2 %: off)
+#endif
 #ifndef FPSSFT_GROUP_MINB
 #define FPSSFT_GROUP_MINB 2  // group kernel: CTAs per SM its registers must allow (3: compact layout)
 #endif
@@ -619,7 +626,10 @@ __device__ __forceinline__ bool team_bar_or(int id, int n, bool p) {
 // flags on every float32 decision statistic, flagged bins re-evaluated in
 // float64 by the whole warp.
 template <class R, int LC, int DC, bool GUARD = false, int WG = 0, int KC = 0>
-__global__ void __launch_bounds__(FPSSFT_WARP_NT, WG ? FPSSFT_GROUP_MINB : FPSSFT_WARP_MINB) recover_warp_kernel(const float2 *__restrict__ cubes,
+__global__ void __launch_bounds__(FPSSFT_WARP_NT, WG ? FPSSFT_GROUP_MINB
+                                                      : (LC != 0 && LC <= 64 ? FPSSFT_WARP_MINB_SHORT
+                                                                              : FPSSFT_WARP_MINB))
+    recover_warp_kernel(const float2 *__restrict__ cubes,
                                                            long long batch, long long batch_stride,
                                                            Geo g_in, Knobs kn,
                                                            const int *__restrict__ schedule,
@@ -905,69 +915,85 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, WG ? FPSSFT_GROUP_MINB : FPSSF
                 }
                 __syncwarp();
             }
-        } else
-        for (int c0 = 0; c0 < n_slots; c0 += 32) {
-            const int s = c0 + lane;
-            const bool valid = s < n_slots && slot_live[s];
-            int b = -1 - lane;
+        } else {
             // every lane: its slot's contribution a root[u_i] on each line
-            cpx<R> C[MAXD + 1];
-            [[maybe_unused]] cpx<double> C0 = {0.0, 0.0};
-            [[maybe_unused]] float ca = 0.f;
-            if (valid) {
-                int m[MAXD];
-                unpack_key(slot_key[s], g, m);
-                b = bin_of(m, g, al);
-                const int u0 = phase_of(m, g, ta);
-                const cpx<A> aj = slot_amp[s];
-                const cpx<R> ar = {(R)aj.re, (R)aj.im};
-#pragma unroll
-                for (int i = 0; i < MAXD + 1; ++i)
-                    if (i < nl) C[i] = ar * roots[phase_step(u0, i, m, g)];
-                if constexpr (GUARD) {
-                    C0 = cpx<double>{(double)aj.re, (double)aj.im} * roots64[u0];
-                    ca = cabs(ar);
-                }
-            }
-            // slots sharing a bin are summed by their lowest lane in lane
-            // (= slot) order; a bin hit once is updated by its own lane
-            const unsigned grp = __match_any_sync(FULL, b);
-            const bool multi = (grp & (grp - 1)) != 0;
-            const bool lead = valid && lane == __ffs(grp) - 1;
-            if (__any_sync(FULL, valid && multi)) {
-                if (valid && multi && !lead) {
+            auto contrib = [&](int s, bool &valid, int &b, cpx<R> *C, cpx<double> &C0, float &ca) {
+                valid = s < n_slots && slot_live[s];
+                b = -1 - lane;
+                C0 = {0.0, 0.0};
+                ca = 0.f;
+                if (valid) {
+                    int m[MAXD];
+                    unpack_key(slot_key[s], g, m);
+                    b = bin_of(m, g, al);
+                    const int u0 = phase_of(m, g, ta);
+                    const cpx<A> aj = slot_amp[s];
+                    const cpx<R> ar = {(R)aj.re, (R)aj.im};
 #pragma unroll
                     for (int i = 0; i < MAXD + 1; ++i)
-                        if (i < nl) scr_c[i * 32 + lane] = C[i];
+                        if (i < nl) C[i] = ar * roots[phase_step(u0, i, m, g)];
                     if constexpr (GUARD) {
-                        scr_c0[lane] = C0;
-                        scr_ca[lane] = ca;
+                        C0 = cpx<double>{(double)aj.re, (double)aj.im} * roots64[u0];
+                        ca = cabs(ar);
                     }
                 }
-                __syncwarp();
-                if (lead && multi) {
-                    for (unsigned rest = grp & (grp - 1); rest; rest &= rest - 1) {
-                        const int j = __ffs(rest) - 1;
+            };
+            // slots sharing a bin are summed by their lowest lane in lane
+            // (= slot) order; a bin hit once is updated by its own lane
+            auto apply = [&](bool valid, int b, cpx<R> *C, cpx<double> C0, float ca) {
+                const unsigned grp = __match_any_sync(FULL, b);
+                const bool multi = (grp & (grp - 1)) != 0;
+                const bool lead = valid && lane == __ffs(grp) - 1;
+                if (__any_sync(FULL, valid && multi)) {
+                    if (valid && multi && !lead) {
 #pragma unroll
                         for (int i = 0; i < MAXD + 1; ++i)
-                            if (i < nl) C[i] = C[i] + scr_c[i * 32 + j];
+                            if (i < nl) scr_c[i * 32 + lane] = C[i];
                         if constexpr (GUARD) {
-                            C0 = C0 + scr_c0[j];
-                            ca += scr_ca[j];
+                            scr_c0[lane] = C0;
+                            scr_ca[lane] = ca;
+                        }
+                    }
+                    __syncwarp();
+                    if (lead && multi) {
+                        for (unsigned rest = grp & (grp - 1); rest; rest &= rest - 1) {
+                            const int j = __ffs(rest) - 1;
+#pragma unroll
+                            for (int i = 0; i < MAXD + 1; ++i)
+                                if (i < nl) C[i] = C[i] + scr_c[i * 32 + j];
+                            if constexpr (GUARD) {
+                                C0 = C0 + scr_c0[j];
+                                ca += scr_ca[j];
+                            }
                         }
                     }
                 }
-            }
-            if (lead) {
+                if (lead) {
 #pragma unroll
-                for (int i = 0; i < MAXD + 1; ++i)
-                    if (i < nl) spec[padi<PAD>(i * L + b)] = spec[padi<PAD>(i * L + b)] - C[i];
-                if constexpr (GUARD) {
-                    x0d[padi<PAD>(b)] = x0d[padi<PAD>(b)] - C0;
-                    pabs[b] += ca;
+                    for (int i = 0; i < MAXD + 1; ++i)
+                        if (i < nl) spec[padi<PAD>(i * L + b)] = spec[padi<PAD>(i * L + b)] - C[i];
+                    if constexpr (GUARD) {
+                        x0d[padi<PAD>(b)] = x0d[padi<PAD>(b)] - C0;
+                        pabs[b] += ca;
+                    }
                 }
+                __syncwarp();
+            };
+            // short lines (few instances per SM, registers to spare): two
+            // chunks' contributions computed together, applied in slot order
+            constexpr bool X2 = FPSSFT_PROJ_X2 && LC != 0 && LC <= 64;
+            for (int c0 = 0; c0 < n_slots; c0 += X2 ? 64 : 32) {
+                bool va, vb = false;
+                int ba, bb = 0;
+                cpx<R> Ca[MAXD + 1], Cb[MAXD + 1];
+                cpx<double> C0a, C0b;
+                float caa, cab;
+                contrib(c0 + lane, va, ba, Ca, C0a, caa);
+                if constexpr (X2) contrib(c0 + 32 + lane, vb, bb, Cb, C0b, cab);
+                apply(va, ba, Ca, C0a, caa);
+                if constexpr (X2)
+                    if (c0 + 32 < n_slots) apply(vb, bb, Cb, C0b, cab);
             }
-            __syncwarp();
         }
 
         // (4) classify + (5) merge, 32 bins at a time in ascending order
