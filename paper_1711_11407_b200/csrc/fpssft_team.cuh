@@ -22,6 +22,9 @@
 #ifndef FPSSFT_TEAM_REGFFT
 #define FPSSFT_TEAM_REGFFT 1  // 512-point lines: per-warp register FFTs (regfft::)
 #endif
+#ifndef FPSSFT_TEAM_GUARD_THREADS
+#define FPSSFT_TEAM_GUARD_THREADS 384  // guarded team kernel: threads per SM its registers allow
+#endif
 #ifndef FPSSFT_TEAM_PROJ_Q
 #define FPSSFT_TEAM_PROJ_Q 2  // projection sub-rounds per ordered apply
 #endif
@@ -75,7 +78,8 @@ __host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, 
 constexpr unsigned short U16_NONE = 0xFFFF;
 
 template <class R, int LC, int DC, int NT, bool GUARD = false>
-__global__ void __launch_bounds__(NT, GUARD ? (384 / NT > 1 ? 384 / NT : 1)
+__global__ void __launch_bounds__(NT, GUARD ? (FPSSFT_TEAM_GUARD_THREADS / NT > 1
+                                                     ? FPSSFT_TEAM_GUARD_THREADS / NT : 1)
                                             : (512 / NT > 1 ? 512 / NT : 1))
     recover_team_kernel(const float2 *__restrict__ cubes, long long batch_stride, Geo g_in,
                         Knobs kn, const int *__restrict__ schedule,
