@@ -9,6 +9,7 @@ mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
 timeout 1200 python -m pytest tests -m gpu -q > $O/gpu_tests.log 2>&1; echo "rc=$?" >> $O/gpu_tests.log
+timeout 600 python tools/bench_imaging.py --reps 5 > $O/imaging.jsonl 2>&1
 : > $O/bench_lines.jsonl
 timeout 900 python bench.py >> $O/bench_lines.jsonl 2> $O/bench_c2.err
 timeout 900 python bench.py --impl reference >> $O/bench_lines.jsonl 2> $O/bench_ref.err
