@@ -595,10 +595,32 @@ def gpu_rank(args):
 
     # ---- e2e through the public API: cubes in pinned host memory -> recovered
     #      spectra (and config-5 images) in pinned host memory (hostpath.py)
-    e2e = None
+    e2e = e2e_bm = None
     if not args.no_e2e:
         from paper_1711_11407_b200.hostpath import HostBatchRunner
 
+        e_steps = max(1, min(args.steps, 5))
+
+        def time_host(hr, host, himg, n_host):
+            e_ms = []
+            for i in range(e_steps):
+                flush.fill_(i)
+                torch.cuda.synchronize()
+                a_ = torch.cuda.Event(enable_timing=True)
+                b_ = torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                for _ in range(n_host):
+                    o = hr.run(host, himg)
+                b_.record(stream)
+                b_.synchronize()
+                e_ms.append(a_.elapsed_time(b_))
+            return o, shard.max_over_ranks(sum(e_ms), dev)
+
+        def out_bytes(o):
+            return sum(v.numel() * v.element_size() for v in o.values() if v is not None)
+
+        # (a) batch-major host cubes, what a user of make_dense_source holds:
+        #     zero-copy / bulk-copy split tuned untimed
         cube_bytes = cubes[0].numel() * cubes.element_size()
         hb = max(1, min(B, (4 << 30) // cube_bytes))  # instances per pinned host batch
         while B % hb:
@@ -610,33 +632,46 @@ def gpu_rank(args):
         hr = HostBatchRunner(shape, cfg, hb, k_cap=k_cap, precision=args.precision, device=dev)
         frac = hr.tune(host, himg)
         bz = hr.split_count()
-        e_steps = max(1, min(args.steps, 5))
-        e_ms = []
-        for i in range(e_steps):
-            flush.fill_(i)
-            torch.cuda.synchronize()
-            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a_.record(stream)
-            for _ in range(n_host):
-                o = hr.run(host, himg)
-            b_.record(stream)
-            b_.synchronize()
-            e_ms.append(a_.elapsed_time(b_))
+        o, e_total = time_host(hr, host, himg, n_host)
         zc_samples = int(o["samples_used"][:bz].sum())
         h2d = n_host * ((hb - bz) * cube_bytes + 16 * zc_samples)
-        d2h = n_host * (sum(v.numel() * v.element_size() for v in o.values() if v is not None)
-                        + (himg.numel() * himg.element_size() if synth else 0))
-        e_total = shard.max_over_ranks(sum(e_ms), dev)
-        e2e = {"value": B_total * e_steps / (e_total / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e_total / e_steps,
-               "path": f"{n_host} x {hb} instances from pinned host memory per step per rank: "
-                       f"{bz} gathered in place (zero copy), {hb - bz} copied in "
-                       f"{hr.chunk}-instance double-buffered chunks (split {frac:.2f} tuned "
-                       f"untimed); results{' and images' if synth else ''} to pinned host",
-               "note": "h2d counts whole cubes for the copied part and 16 B per gathered "
-                       "sample (one 16-byte read request each) for the zero-copy part"}
+        d2h = n_host * (out_bytes(o) + (himg.numel() * himg.element_size() if synth else 0))
+        e2e_bm = {"value": B_total * e_steps / (e_total / 1e3), "unit": UNIT,
+                  "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                  "ms_per_step": e_total / e_steps,
+                  "path": f"batch-major [B, *dims] pinned host cubes, {n_host} x {hb} instances "
+                          f"per step per rank: {bz} gathered in place (zero copy), {hb - bz} "
+                          f"copied in {hr.chunk}-instance double-buffered chunks (split "
+                          f"{frac:.2f} tuned untimed); results"
+                          f"{' and images' if synth else ''} to pinned host",
+                  "note": "h2d counts whole cubes for the copied part and 16 B per gathered "
+                          "sample (one 16-byte read request each) for the zero-copy part"}
         del host, himg, hr
+        e2e = e2e_bm
+        # (b) the same batch in the interleaved layout on the host (the layout
+        #     `value` is measured on): every instance gathered in place by the
+        #     group kernel, one 64-byte PCIe read per segment serving `group`
+        #     instances
+        if group > 1 and not synth and B % group == 0:
+            host = torch.empty(run_cubes.shape, dtype=run_cubes.dtype, pin_memory=True)
+            host.copy_(run_cubes)
+            hr = HostBatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision,
+                                 device=dev, group=group)
+            hr.run(host)
+            o, e_total = time_host(hr, host, None, 1)
+            segs_h = _segments_per_launch(shape, hr._runner(0, B).schedule_host,
+                                          o["iterations"].numpy(), group=group)
+            e2e = {"value": B_total * e_steps / (e_total / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(64 * segs_h), "d2h_bytes_per_step": out_bytes(o),
+                   "ms_per_step": e_total / e_steps,
+                   "path": f"interleaved [B/{group}, *dims, {group}] pinned host cubes (the "
+                           f"layout `value` runs on), all {B} instances per step gathered in "
+                           f"place by the group kernel (zero copy: one 64-byte PCIe read per "
+                           f"segment serves {group} instances); results to pinned host",
+                   "note": "h2d = distinct 64-byte segments the gathers touch x 64 B",
+                   "outputs_identical_to_device_run": bool(all(
+                       torch.equal(o[k], runner.out[k].cpu()) for k in o if o[k] is not None))}
+            del host, hr
 
     # ---- CPU baseline on this host (rank 0, N=1), same inputs; parity of the
     #      GPU results of exactly those instances against the oracle's
@@ -676,7 +711,7 @@ def gpu_rank(args):
                     "terminated_clean": int((term == 0).sum()),
                     "rank0_instances": [b0, b1]},
             "roofline": roofline, "parity": parity, "cpu_baseline": cpu,
-            "batch_major": batch_major, "e2e": e2e, "clocks": clk,
+            "batch_major": batch_major, "e2e": e2e, "e2e_batch_major": e2e_bm, "clocks": clk,
             "gpu_launches": args.steps * (int(P._native.lib().fpssft_launches_per_batch())
                                           + (1 if synth else 0)),
         }

@@ -71,11 +71,23 @@ class HostBatchRunner:
                  k_cap: int = 256, precision: str = "auto", device=None, mode: str = "auto",
                  zero_copy_fraction: float | None = None, chunk: int | None = None,
                  chunk_bytes: int = 256 << 20, schedule=None, sched_index=None,
-                 graphs: bool = True):
+                 graphs: bool = True, group: int = 1):
         import torch
 
         if mode not in ("auto", "copy", "zero_copy", "split"):
             raise ValueError("mode must be auto, copy, zero_copy or split")
+        # group > 1: the host batch is interleaved [ceil(B/G), *dims, G] (the
+        # producer's layout choice, like the device bench's): every batch is
+        # gathered in place by the group kernel, one PCIe read per 64-byte
+        # segment serving G instances (config 2: 6.7 vs 23 ms per batch
+        # batch-major, tools/zc_group_probe.py)
+        self.group = int(group)
+        if self.group > 1:
+            if mode not in ("auto", "zero_copy"):
+                raise ValueError("an interleaved host batch is gathered in place (zero_copy)")
+            if sched_index is not None:
+                raise ValueError("an interleaved host batch shares one schedule")
+            mode = "zero_copy"
         if mode == "split" and zero_copy_fraction is None:
             raise ValueError("split mode needs zero_copy_fraction")
         self.shape, self.config, self.batch = shape, config, int(batch)
@@ -141,7 +153,8 @@ class HostBatchRunner:
         if r is None:
             si = None if self._sched_index is None else self._sched_index[b0:b0 + n]
             r = BatchRunner(self.shape, self.config, n, schedule=self._schedule, sched_index=si,
-                            k_cap=self.k_cap, precision=self.precision, device=self.device)
+                            k_cap=self.k_cap, precision=self.precision, device=self.device,
+                            group=self.group)
             self._runners[key] = r
         return r
 
@@ -206,12 +219,16 @@ class HostBatchRunner:
         if not (isinstance(host_cubes, torch.Tensor) and not host_cubes.is_cuda
                 and host_cubes.is_pinned()):
             raise ValueError("host_cubes must be a pinned host tensor")
-        if tuple(host_cubes.shape) != (self.batch, *self.shape.dims) or \
-                host_cubes.dtype != torch.complex64:
-            raise ValueError(f"host_cubes must be complex64 [{self.batch}, {self.shape.dims}]")
+        G = self.group
+        want = ((self.batch, *self.shape.dims) if G == 1
+                else (-(-self.batch // G), *self.shape.dims, G))
+        if tuple(host_cubes.shape) != want or host_cubes.dtype != torch.complex64:
+            raise ValueError(f"host_cubes must be complex64 {list(want)}")
         if not host_cubes.is_contiguous():
             raise ValueError("host_cubes must be contiguous")
         synth = images is not None
+        if synth and G > 1:
+            raise ValueError("re-synthesis needs a batch-major host batch")
         if synth and not (not images.is_cuda and images.is_pinned()
                           and images.shape == host_cubes.shape):
             raise ValueError("images must be a pinned host tensor shaped like host_cubes")
