@@ -75,6 +75,9 @@
 #ifndef FPSSFT_PROJ_X2
 #define FPSSFT_PROJ_X2 0  // A/B: lines of <= 64 points, projection two chunks at a time (+2 %: off)
 #endif
+#ifndef FPSSFT_OUT_BITONIC
+#define FPSSFT_OUT_BITONIC 1  // warp kernel, k_cap <= 128: output order by a register bitonic sort
+#endif
 #ifndef FPSSFT_GROUP_MINB
 #define FPSSFT_GROUP_MINB 2  // group kernel: CTAs per SM its registers must allow (3: compact layout)
 #endif
@@ -1234,9 +1237,75 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, WG ? FPSSFT_GROUP_MINB
 
     PCLK(7);
     // ---- RecoveryReport: live entries sorted by packed key (= lexicographic).
+    __syncwarp();
+    if constexpr (KC != 0 && KC <= 128 && FPSSFT_OUT_BITONIC) {
+        // compile-time capacity <= 128: a bitonic sort of (key << 7 | slot)
+        // in registers, 4 per lane (element i = 4 lane + j), shuffles only
+        if (g.key_bits_ + 7 <= 31) {  // (block-uniform)
+            unsigned v[4];
+            int my = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int sl = 4 * lane + j;
+                const bool live = sl < n_slots && slot_live[sl];
+                my += live;
+                v[j] = live ? ((unsigned)slot_key[sl] << 7) | (unsigned)sl : 0x7FFFFFFFu;
+            }
+            const int count = __shfl_sync(FULL, warp_sum(my), 0);
+#pragma unroll
+            for (int k = 2; k <= 128; k <<= 1) {
+#pragma unroll
+                for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                    if (jj >= 4) {
+                        const bool lower = (lane & (jj >> 2)) == 0;
+                        const bool asc = ((4 * lane) & k) == 0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const unsigned y = __shfl_xor_sync(FULL, v[j], jj >> 2);
+                            v[j] = (lower == asc) ? min(v[j], y) : max(v[j], y);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if ((j ^ jj) > j) {
+                                const bool asc = ((4 * lane + j) & k) == 0;
+                                const unsigned x = v[j], y = v[j ^ jj];
+                                v[j] = asc ? min(x, y) : max(x, y);
+                                v[j ^ jj] = asc ? max(x, y) : min(x, y);
+                            }
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int r = 4 * lane + j;
+                if (r < count) {
+                    const int sl = (int)(v[j] & 127u);
+                    int m[MAXD];
+                    unpack_key((int)(v[j] >> 7), g, m);
+                    int *fo = out.freqs + (inst * k_cap + r) * D;
+#pragma unroll
+                    for (int k = 0; k < MAXD; ++k)
+                        if (k < D) fo[k] = m[k];
+                    double *ao = out.amps + (inst * k_cap + r) * 2;
+                    ao[0] = (double)slot_amp[sl].re;
+                    ao[1] = (double)slot_amp[sl].im;
+                }
+            }
+            if (lane == 0) {
+                out.count[inst] = count;
+                out.iterations[inst] = it_run;
+                out.samples_used[inst] = (long long)it_run * nl * L;
+                out.terminated_by[inst] = term;
+            }
+            PCLK(8);
+            PCLK_FLUSH();
+            return;
+        }
+    }
     // Counting sort on the key's top 8 bits (shared-memory histogram, warp
     // scan, scatter), then insertion sort inside the (short) buckets.
-    __syncwarp();
     int *hist = (int *)spec;          // 256 buckets
     int *sslot = hist + 256;          // n_slots entries
     const int kb = g.key_bits_;
