@@ -75,6 +75,10 @@
 #ifndef FPSSFT_PROJ_X2
 #define FPSSFT_PROJ_X2 0  // A/B: lines of <= 64 points, projection two chunks at a time (+2 %: off)
 #endif
+#ifndef FPSSFT_DECODE_KEEP
+#define FPSSFT_DECODE_KEEP 1  // group kernel: decode values/roots reused by the merge (-1.4 %;
+                              // batch-major +1.6 %, config 3 +10 %: group kernel only)
+#endif
 #ifndef FPSSFT_OUT_BITONIC
 #define FPSSFT_OUT_BITONIC 1  // warp kernel, k_cap <= 128: output order by a register bitonic sort
 #endif
@@ -1082,12 +1086,16 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, WG ? FPSSFT_GROUP_MINB
                 nx_st = decode_candidate<R, PAD>(spec, g, nx_b, al, ta, roots, round_tol,
                                                  verify_tol, nx_m, &nx_a);
         }
+        // unguarded float32: the decode's bin values and roots stay in
+        // registers for the merge and the residual (no re-reads)
+        constexpr bool KEEP = !GUARD && sizeof(R) == 4 && FPSSFT_DECODE_KEEP && !PIPE && WG != 0;
         for (int c0 = 0; c0 < n_cand; c0 += 32) {
             const int ce = c0 + lane < n_cand ? cand[c0 + lane] : -1;
             const int b = ce >= 0 ? (ce & ~(int)CAND_FLAG) : -1;
             int m[MAXD];
             cpx<R> a;
             int st = 0;
+            [[maybe_unused]] cpx<R> sv[MAXD + 1], rv[MAXD + 1];
             if constexpr (PIPE) {
                 st = nx_st;
                 a = nx_a;
@@ -1142,7 +1150,8 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, WG ? FPSSFT_GROUP_MINB
             } else {
                 if (b >= 0)
                     st = decode_candidate<R, PAD>(spec, g, b, al, ta, roots, round_tol,
-                                                  verify_tol, m, &a);
+                                                  verify_tol, m, &a, KEEP ? sv : nullptr,
+                                                  KEEP ? rv : nullptr);
             }
             const unsigned acc = __ballot_sync(FULL, st == 2);
             if constexpr (GUARD) n_cand_x += __popc(__ballot_sync(FULL, st >= 1));
@@ -1181,12 +1190,28 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, WG ? FPSSFT_GROUP_MINB
                 d_amp += (keep ? av_new : (A)0) - (found < 0 ? (A)0 : cabs(slot_amp[s]));
                 slot_amp[s] = keep ? v : cpx<A>{(A)0, (A)0};
                 slot_live[s] = keep;
-                const int u0 = phase_of(m, g, ta);  // driver.py:189-194
-                for (int i = 0; i < nl; ++i)
-                    spec[padi<PAD>(i * L + b)] =
-                        spec[padi<PAD>(i * L + b)] - a * roots[phase_step(u0, i, m, g)];
+                if constexpr (KEEP) {  // the decode's values and roots, in registers
+#pragma unroll
+                    for (int i = 0; i < MAXD + 1; ++i)
+                        if (i < nl) {
+                            sv[i] = sv[i] - a * rv[i];
+                            spec[padi<PAD>(i * L + b)] = sv[i];
+                        }
+                } else {
+                    const int u0 = phase_of(m, g, ta);  // driver.py:189-194
+                    for (int i = 0; i < nl; ++i)
+                        spec[padi<PAD>(i * L + b)] =
+                            spec[padi<PAD>(i * L + b)] - a * roots[phase_step(u0, i, m, g)];
+                }
             }
-            if (b >= 0) resid = max(resid, bin_residual<R, PAD>(spec, g, b));
+            if constexpr (KEEP) {
+                if (b >= 0)
+#pragma unroll
+                    for (int i = 0; i < MAXD + 1; ++i)
+                        if (i < nl) resid = max(resid, cabs2(sv[i]));
+            } else if (b >= 0) {
+                resid = max(resid, bin_residual<R, PAD>(spec, g, b));
+            }
             n_slots += __popc(fresh);
             __syncwarp();
         }

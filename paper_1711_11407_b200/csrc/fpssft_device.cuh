@@ -1224,16 +1224,23 @@ __device__ __forceinline__ int classify_bin(const cpx<R> *spec, const Geo &g, in
 }
 
 // As classify_bin for a bin already known to pass the magnitude test.
+// s_out / r_out (optional): the bin's D+1 values and, when verified, the D+1
+// roots of the re-prediction (what the merge subtracts with).
 template <class R, bool PAD = false>
 __device__ __forceinline__ int decode_candidate(const cpx<R> *spec, const Geo &g, int b,
                                             const int *al, const int *ta, const cpx<R> *roots,
                                             R round_tol, R verify_tol,
-                                            int *m, cpx<R> *amp_out) {
+                                            int *m, cpx<R> *amp_out, cpx<R> *s_out = nullptr,
+                                            cpx<R> *r_out = nullptr) {
     const int L = g.L, D = g.D;
     cpx<R> s[MAXD + 1];
 #pragma unroll
     for (int i = 0; i < MAXD + 1; ++i)
         if (i <= D) s[i] = spec[padi<PAD>(i * L + b)];
+    if (s_out)
+#pragma unroll
+        for (int i = 0; i < MAXD + 1; ++i)
+            if (i <= D) s_out[i] = s[i];
     const R mag0 = cabs(s[0]);
     const R two_pi = (R)6.283185307179586476925286766559;
     bool ok = true;
@@ -1258,7 +1265,9 @@ __device__ __forceinline__ int decode_candidate(const cpx<R> *spec, const Geo &g
 #pragma unroll
     for (int i = 0; i < MAXD + 1; ++i) {
         if (i <= D) {
-            cpx<R> d = amp * roots[phase_step(u0, i, m, g)] - s[i];
+            const cpx<R> r = roots[phase_step(u0, i, m, g)];
+            if (r_out) r_out[i] = r;
+            cpx<R> d = amp * r - s[i];
             ok = ok && (sizeof(R) == 8 ? cabs(d) <= lim : cabs2(d) <= lim * lim);
         }
     }
