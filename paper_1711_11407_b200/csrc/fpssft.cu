@@ -75,6 +75,9 @@
 #ifndef FPSSFT_PROJ_X2
 #define FPSSFT_PROJ_X2 0  // A/B: lines of <= 64 points, projection two chunks at a time (+2 %: off)
 #endif
+#ifndef FPSSFT_WARP_FFT_JOINT2
+#define FPSSFT_WARP_FFT_JOINT2 0  // A/B: group kernel, 256-point lines 0 and 1 transformed together
+#endif
 #ifndef FPSSFT_DECODE_KEEP
 #define FPSSFT_DECODE_KEEP 1  // group kernel: decode values/roots reused by the merge (-1.4 %;
                               // batch-major +1.6 %, config 3 +10 %: group kernel only)
@@ -854,7 +857,13 @@ __global__ void __launch_bounds__(FPSSFT_WARP_NT, WG ? FPSSFT_GROUP_MINB
             if constexpr (FPSSFT_WARP_FFT_JOINT && DC + 1 <= 3)
                 my_energy = (R)regfft::fft256_lines_joint<DC + 1>((cpx<float> *)spec,
                                                                   (const cpx<float> *)roots, lane);
-            else
+            else if constexpr (FPSSFT_WARP_FFT_JOINT2 && WG != 0 && DC + 1 == 3) {
+                // lines 0 and 1 together, then line 2
+                my_energy = (R)regfft::fft256_lines_joint<2>((cpx<float> *)spec,
+                                                             (const cpx<float> *)roots, lane);
+                my_energy += (R)regfft::fft256_lines_warp((cpx<float> *)spec + 2 * 272, 1,
+                                                          (const cpx<float> *)roots, lane);
+            } else
                 my_energy = (R)regfft::fft256_lines_warp((cpx<float> *)spec, DC + 1,
                                                          (const cpx<float> *)roots, lane);
             if constexpr (GUARD) fft_static<double, LC, 1, 32, WarpTeam, Roots64>(x0d, roots64, lane);
