@@ -371,6 +371,8 @@ def parity_summary(gpu: dict, reports, tol: float) -> dict:
     return {"instances": n, "identical_support": same_sup, "identical_iterations": same_it,
             "max_rel_amp_err": worst, "tolerance": tol,
             "pass": same_sup == n and same_it == n and worst <= tol,
+            # BASELINE.json north star: support bit-exact, amplitudes within tolerance
+            "north_star_pass": same_sup == n and worst <= tol,
             "oracle": "oracle/fps_oracle.py (float64 numpy port, pinned to the reference's "
                       "golden runs), same complex64 cubes and schedule"}
 
