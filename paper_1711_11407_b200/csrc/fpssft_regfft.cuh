@@ -8,6 +8,10 @@
 // X[c + 16 d + 256 h], d = 0..15.
 #pragma once
 // (included inside namespace fpssft)
+#ifndef FPSSFT_FFT256_LEAN
+#define FPSSFT_FFT256_LEAN 0  // A/B: 256-point lines, scale folded into twiddles, fma signs, static
+                              // offsets (group +1.2 % from a spill, batch-major -0.8 %: off)
+#endif
 #ifndef FPSSFT_FFT256_TW_HOIST
 #define FPSSFT_FFT256_TW_HOIST 0  // A/B: 256-point lines, first-stage twiddles held across lines
 #endif
@@ -142,6 +146,33 @@ __device__ __forceinline__ float fft256_lines_warp(cpx<float> *spec, int nlines,
 #pragma unroll
         for (int be = 0; be < 8; ++be) v[be] = base[k1 * S + 4 * be + h];
         dft8(v);
+#if FPSSFT_FFT256_LEAN
+        // the 1/256 (a power of two: exact) folded into the twiddles and v[0]
+        const float inv = 1.f / 256.f;
+        v[0] = make_float2(v[0].x * inv, v[0].y * inv);
+#pragma unroll
+        for (int d = 1; d < 8; ++d) {  // e^{2 pi i h d / 32} = roots[8 h d] (a runtime h)
+            const cpx<float> r = roots[8 * h * d];
+            v[d] = cmul(v[d], make_float2(r.re * inv, r.im * inv));
+        }
+        // 4-point DFT across lanes h (xor 2, then xor 1); x + p or p - x as
+        // one fma with the lane's sign (exactly the same roundings)
+        const float s2 = (h & 2) ? -1.f : 1.f, s1 = (h & 1) ? -1.f : 1.f;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+            float2 x = v[d];
+            float2 p = make_float2(__shfl_xor_sync(FULL, x.x, 2), __shfl_xor_sync(FULL, x.y, 2));
+            x = make_float2(fmaf(s2, x.x, p.x), fmaf(s2, x.y, p.y));
+            if (h == 3) x = mul_i(x);
+            p = make_float2(__shfl_xor_sync(FULL, x.x, 1), __shfl_xor_sync(FULL, x.y, 1));
+            v[d] = make_float2(fmaf(s1, x.x, p.x), fmaf(s1, x.y, p.y));
+        }
+        __syncwarp();  // every lane has read the exchange before outputs land in it
+        // X[k], k = k1 + 8 (d + 8 k2b), at k + (k >> 4) = k1 + 68 k2b + 8 d + (d >> 1)
+        float2 *ob = base + k1 + 68 * k2b;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) ob[8 * d + (d >> 1)] = make_float2(v[d].x, -v[d].y);  // conj out
+#else
 #pragma unroll
         for (int d = 1; d < 8; ++d) {  // e^{2 pi i h d / 32} = roots[8 h d] (a runtime h)
             const cpx<float> r = roots[8 * h * d];
@@ -163,6 +194,7 @@ __device__ __forceinline__ float fft256_lines_warp(cpx<float> *spec, int nlines,
             const int k = k1 + 8 * (d + 8 * k2b);
             base[k + (k >> 4)] = make_float2(v[d].x * inv, -v[d].y * inv);  // conjugate out
         }
+#endif
         __syncwarp();
     }
     return energy;
