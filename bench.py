@@ -654,22 +654,25 @@ def gpu_rank(args):
         #     `value` is measured on): every instance gathered in place by the
         #     group kernel, one 64-byte PCIe read per segment serving `group`
         #     instances
-        if group > 1 and not synth and B % group == 0:
-            host = torch.empty(run_cubes.shape, dtype=run_cubes.dtype, pin_memory=True)
-            host.copy_(run_cubes)
+        hg = args.host_group
+        if group > 1 and not synth and hg > 1 and B % hg == 0:
+            host_il = P.interleave(cubes, hg)
+            host = torch.empty(host_il.shape, dtype=host_il.dtype, pin_memory=True)
+            host.copy_(host_il)
+            del host_il
             hr = HostBatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision,
-                                 device=dev, group=group)
+                                 device=dev, group=hg)
             hr.run(host)
             o, e_total = time_host(hr, host, None, 1)
             segs_h = _segments_per_launch(shape, hr._runner(0, B).schedule_host,
-                                          o["iterations"].numpy(), group=group)
+                                          o["iterations"].numpy(), group=hg)
             e2e_il = {"value": B_total * e_steps / (e_total / 1e3), "unit": UNIT,
                    "h2d_bytes_per_step": int(64 * segs_h), "d2h_bytes_per_step": out_bytes(o),
                    "ms_per_step": e_total / e_steps,
-                   "path": f"interleaved [B/{group}, *dims, {group}] pinned host cubes (the "
-                           f"layout `value` runs on), all {B} instances per step gathered in "
-                           f"place by the group kernel (zero copy: one 64-byte PCIe read per "
-                           f"segment serves {group} instances); results to pinned host",
+                   "path": f"interleaved [B/{hg}, *dims, {hg}] pinned host cubes, all {B} "
+                           f"instances per step gathered in place by the group kernel (zero "
+                           f"copy: one {8 * hg}-byte PCIe read per sample position serves {hg} "
+                           f"instances); results to pinned host",
                    "note": "h2d = distinct 64-byte segments the gathers touch x 64 B",
                    "outputs_identical_to_device_run": bool(all(
                        torch.equal(o[k], runner.out[k].cpu()) for k in o if o[k] is not None))}
@@ -755,6 +758,9 @@ def main():
                          "instances interleaved sample by sample (--group); auto = "
                          "interleaved for batches of >= 64 instances")
     ap.add_argument("--group", type=int, default=8)
+    ap.add_argument("--host-group", type=int, default=16,
+                    help="interleave group of the e2e host batch (16: one 128-byte PCIe read "
+                         "per position serves 16 instances; 1 = batch-major only)")
     ap.add_argument("--mode", default="auto", choices=["auto", "warp", "cta"],
                     help="kernel family (auto: the planner's choice for this batch)")
     ap.add_argument("--batch", type=int, default=None,

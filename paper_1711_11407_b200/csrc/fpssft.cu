@@ -636,9 +636,11 @@ __device__ __forceinline__ bool team_bar_or(int id, int n, bool p) {
 // flags on every float32 decision statistic, flagged bins re-evaluated in
 // float64 by the whole warp.
 template <class R, int LC, int DC, bool GUARD = false, int WG = 0, int KC = 0>
-__global__ void __launch_bounds__(FPSSFT_WARP_NT, WG ? FPSSFT_GROUP_MINB
-                                                      : (LC != 0 && LC <= 64 ? FPSSFT_WARP_MINB_SHORT
-                                                                              : FPSSFT_WARP_MINB))
+__global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
+                                  WG > 8 ? 1
+                                         : (WG ? FPSSFT_GROUP_MINB
+                                               : (LC != 0 && LC <= 64 ? FPSSFT_WARP_MINB_SHORT
+                                                                      : FPSSFT_WARP_MINB)))
     recover_warp_kernel(const float2 *__restrict__ cubes,
                                                            long long batch, long long batch_stride,
                                                            Geo g_in, Knobs kn,
@@ -2151,14 +2153,32 @@ int warp_kernel_regs(const Geo &g, int precision, int k_cap) {
 #ifndef FPSSFT_GROUP_TEAM
 #define FPSSFT_GROUP_TEAM FPSSFT_GROUP_WG  // warps per gather team (a divisor of the CTA width)
 #endif
-const void *group_kernel_for(const Geo &g, int precision, int group, int k_cap) {
+#ifndef FPSSFT_GROUP_WIDE
+#define FPSSFT_GROUP_WIDE 16  // a second group kernel for groups of this many (one CTA of 16
+                              // warps: a 128-byte read per sample position); 0 = off
+#endif
+// The group kernel for an interleave group of `group` instances, and its CTA
+// width in warps (*wg): 16-wide when the group is a multiple of 16 (one
+// 128-byte read per position serves 16 instances: the host-memory path's
+// request economy, tools/zc_group_probe.py), else 8-wide.
+const void *group_kernel_for(const Geo &g, int precision, int group, int k_cap, int *wg = nullptr) {
     if (!FPSSFT_GROUP_WG || precision != FPSSFT_F32 || !g.off32 || group < FPSSFT_GROUP_WG ||
         group % FPSSFT_GROUP_WG)
         return nullptr;
 #if FPSSFT_GROUP_WG
-    if (g.D == 2 && g.L == 256)
+    if (g.D == 2 && g.L == 256) {
+#if FPSSFT_GROUP_WIDE
+        if (group % FPSSFT_GROUP_WIDE == 0) {
+            if (wg) *wg = FPSSFT_GROUP_WIDE;
+            return k_cap == 128
+                       ? (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_WIDE, 128>
+                       : (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_WIDE>;
+        }
+#endif
+        if (wg) *wg = FPSSFT_GROUP_WG;
         return k_cap == 128 ? (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_TEAM, 128>
                             : (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_TEAM>;
+    }
 #endif
     return nullptr;
 }
@@ -2196,13 +2216,14 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp,
                 wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * best_w, best_w,
                                 wl.roots + (size_t)best_w * wl.per_warp,
                                 warp_kernel_for(gw, precision, kn.k_cap)};
+            int gwd = FPSSFT_GROUP_WG;
             const void *gk =
-                shared_sched ? group_kernel_for(gw, precision, kn.group, kn.k_cap) : nullptr;
+                shared_sched ? group_kernel_for(gw, precision, kn.group, kn.k_cap, &gwd) : nullptr;
             if (best_w && gk) {
                 const WarpLayout gl = make_warp_layout(g.D, g.L, kn.k_cap, cs, false, true);
-                const size_t smem = gl.roots + (size_t)FPSSFT_GROUP_WG * gl.per_warp;
+                const size_t smem = gl.roots + (size_t)gwd * gl.per_warp;
                 if ((long long)smem <= SMEM_PER_CTA)
-                    wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * FPSSFT_GROUP_WG, FPSSFT_GROUP_WG, smem, gk};
+                    wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * gwd, gwd, smem, gk};
             }
         }
         if (want == FPSSFT_MODE_WARP) {

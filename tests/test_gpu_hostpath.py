@@ -149,7 +149,8 @@ def test_zero_copy_graph_replay_sees_new_host_data():
     assert hr._graphs and all(g is not None for g in hr._graphs.values())
 
 
-def test_interleaved_host_batch_gathered_in_place():
+@pytest.mark.parametrize("G", [8, 16])
+def test_interleaved_host_batch_gathered_in_place(G):
     """An interleaved pinned host batch [B/8, *dims, 8] is recovered in place by
     the group kernel (one PCIe read per 64-byte segment for 8 instances), with
     outputs identical to the device run of the same batch."""
@@ -163,14 +164,15 @@ def test_interleaved_host_batch_gathered_in_place():
     B = 64
     inst = [W.make_instance(w, r) for r in W.instance_rngs(w.seed, B)]
     cubes = torch.as_tensor(np.stack([c for _, _, c in inst])).cuda()
-    il = P.interleave(cubes, 8)
     cfg = P.FpsSftConfig(seed=2, **P.PROFILES["P32"])
     shape = P.CubeShape(w.dims)
-    dev = P.BatchRunner(shape, cfg, B, k_cap=128, group=8)
-    dev.run(il)
+    dev = P.BatchRunner(shape, cfg, B, k_cap=128)  # batch-major device run
+    dev.run(cubes)
+    il = P.interleave(cubes, G)
     host = torch.empty(il.shape, dtype=il.dtype, pin_memory=True)
     host.copy_(il)
-    hr = HostBatchRunner(shape, cfg, B, k_cap=128, group=8)
+    hr = HostBatchRunner(shape, cfg, B, k_cap=128, group=G)
+    assert hr._runner(0, B).plan["instances_per_cta"] == G  # the G-wide group kernel
     out = hr.run(host)
     for k, v in out.items():
         if v is not None:
