@@ -85,6 +85,9 @@
 #ifndef FPSSFT_OUT_BITONIC
 #define FPSSFT_OUT_BITONIC 1  // warp kernel, k_cap <= 128: output order by a register bitonic sort
 #endif
+#ifndef FPSSFT_TEAM256
+#define FPSSFT_TEAM256 0  // A/B: team kernels for 256-point lines
+#endif
 #ifndef FPSSFT_GROUP_MINB
 #define FPSSFT_GROUP_MINB 2  // group kernel: CTAs per SM its registers must allow (3: compact layout)
 #endif
@@ -2087,6 +2090,13 @@ const void *team_kernel_for_t(const Geo &g, int *nt) {
         *nt = 128;
         return (const void *)recover_team_kernel<R, 512, 2, 128>;
     }
+#if FPSSFT_TEAM256
+    if (g.L == 256) {  // A/B: small batches of 256-point lines, several warps per instance
+        if (*nt == 64) return (const void *)recover_team_kernel<R, 256, 2, 64>;
+        *nt = 128;
+        return (const void *)recover_team_kernel<R, 256, 2, 128>;
+    }
+#endif
     return nullptr;
 }
 // Guarded float32 team kernels (fpssft_guard.cuh): the shapes of the noisy
