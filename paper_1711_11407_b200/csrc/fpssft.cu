@@ -88,6 +88,9 @@
 #ifndef FPSSFT_TEAM256
 #define FPSSFT_TEAM256 0  // A/B: team kernels for 256-point lines
 #endif
+#ifndef FPSSFT_GROUP_ASSIST
+#define FPSSFT_GROUP_ASSIST 1  // group kernel: idle warps transform the last members' lines
+#endif
 #ifndef FPSSFT_GROUP_MINB
 #define FPSSFT_GROUP_MINB 2  // group kernel: CTAs per SM its registers must allow (3: compact layout)
 #endif
@@ -739,6 +742,11 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
         nta[k] = k < D ? sched[D + k] : 0;
     }
     bool active = sched_ok && has_inst;
+    // FPSSFT_GROUP_ASSIST: group kernel of 256-point lines, unguarded float32
+    constexpr bool ASSIST = FPSSFT_GROUP_ASSIST && WG != 0 && LC == 256 && DC + 1 <= 3 &&
+                            sizeof(R) == 4 && !GUARD && FPSSFT_WARP_REGFFT256;
+    [[maybe_unused]] __shared__ int s_act[ASSIST ? 32 : 1];
+    [[maybe_unused]] bool assisted = false;
     PCLK_DECL();
     for (int it = 0; it < kn.t_max; ++it) {
         int al[MAXD], ta[MAXD];
@@ -754,6 +762,8 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
             PCLK(0);
             GroupGather<LC, DC, WG> gg;
             if (lines_ok) gg.load(gbase, g, al, ta, team_tid);
+            if constexpr (ASSIST)
+                if (lane == 0) s_act[warp] = (int)(active && lines_ok);
             const bool any = team_is_cta ? __syncthreads_or(active && lines_ok)
                                          : team_bar_or(1 + team, WG * 32, active && lines_ok);
             if (!any) {
@@ -771,6 +781,32 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
             }
             if (team_is_cta) __syncthreads();
             else team_bar(1 + team, WG * 32);
+            if constexpr (ASSIST) {
+                // straggler iterations (at most 2 members still running): the
+                // group's idle warps transform the active members' lines, one
+                // line per warp (the same per-line code and energy order as
+                // fft256_lines_warp), results and per-lane energies in place
+                if (team_is_cta) {
+                    unsigned amask = 0;
+#pragma unroll
+                    for (int w2 = 0; w2 < WG; ++w2) amask |= (unsigned)(s_act[w2] != 0) << w2;
+                    const int n_act = __popc(amask);
+                    assisted = n_act > 0 && n_act <= 2;
+                    if (assisted) {
+                        if (warp < (DC + 1) * n_act) {
+                            unsigned rest = amask;
+                            for (int q = warp / (DC + 1); q > 0; --q) rest &= rest - 1;
+                            const int mem = __ffs(rest) - 1, line = warp % (DC + 1);
+                            unsigned char *mb = sm + lay.roots + (size_t)mem * lay.per_warp;
+                            cpx<float> *ml = (cpx<float> *)(mb + lay.spec) + line * 272;
+                            const float e = regfft::fft256_lines_warp(ml, 1,
+                                                                      (const cpx<float> *)roots, lane);
+                            ((float *)(mb + lay.scr_u))[line * 32 + lane] = e;
+                        }
+                        __syncthreads();
+                    }
+                }
+            }
             // L2 prefetch of the next iteration's segments (one request per
             // segment) while this one computes: only for the leading
             // iterations nearly every instance runs (FPSSFT_GROUP_PF)
@@ -868,6 +904,12 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
                                                              (const cpx<float> *)roots, lane);
                 my_energy += (R)regfft::fft256_lines_warp((cpx<float> *)spec + 2 * 272, 1,
                                                           (const cpx<float> *)roots, lane);
+            } else if (ASSIST && assisted) {  // transformed by the group's idle warps
+                const float *es = (const float *)scr_c;
+                float e = es[lane];
+#pragma unroll
+                for (int i = 1; i < DC + 1; ++i) e += es[i * 32 + lane];
+                my_energy = (R)e;
             } else
                 my_energy = (R)regfft::fft256_lines_warp((cpx<float> *)spec, DC + 1,
                                                          (const cpx<float> *)roots, lane);

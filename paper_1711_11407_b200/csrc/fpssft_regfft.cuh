@@ -122,13 +122,15 @@ __device__ __forceinline__ float fft256_lines_warp(cpx<float> *spec, int nlines,
     for (int line = 0; line < nlines; ++line) {
         float2 *base = (float2 *)(spec + line * PADL);
         float2 v[8];
+        float el = 0.f;  // this line's share, then added (the assisted path's order)
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
             const int i = 32 * a + lane;
             const float2 x = base[i + (i >> 4)];
-            energy += x.x * x.x + x.y * x.y;
+            el += x.x * x.x + x.y * x.y;
             v[a] = make_float2(x.x, -x.y);  // conjugate in
         }
+        energy = line == 0 ? el : energy + el;
         dft8(v);
 #pragma unroll
         for (int c = 1; c < 8; ++c) {
