@@ -3,7 +3,7 @@
 instances (BASELINE.json config 2 by default: 4096 x 256x256 complex64,
 K=100, noiseless, profile P32).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--scaling strong|weak]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--scaling weak|strong]
     python bench.py --impl reference ...      # the CPU reference arm
 
 One step = one ``fpssft_run_batch`` (one fused kernel launch) over the
@@ -12,9 +12,11 @@ every timed step and only the step is inside the CUDA events.
 
 Multi-GPU: ``--gpus N`` is N ranks, one process per GPU -- started by
 torchrun, or spawned here (``shard.launch``) when the environment has no
-``WORLD_SIZE``.  ``--scaling strong`` (default) splits the config's global
-batch (4096 instances for config 2, 16384 frames for config 5) into N
-contiguous slices; ``weak`` gives every rank the whole batch.  No
+``WORLD_SIZE``.  ``--scaling weak`` (default: instances are independent, so
+the path shards with no data-path collective) gives every rank the config's
+whole batch; ``strong`` splits the global batch (4096 instances for config 2,
+16384 frames for config 5) into N contiguous slices.  A weak-scaling run with
+N > 1 also times the strong-scaling split and reports it as ``strong``.  No
 collective sits on the data path: each rank times its own launches, the job
 time is the max over ranks, and the padded results are gathered to rank 0
 over NCCL after the timed region (timed separately, ``gather``).
@@ -477,8 +479,8 @@ def gpu_rank(args):
     run_cubes = P.interleave(cubes, group) if group > 1 else cubes
     torch.cuda.synchronize()
 
-    def make_runner(kc, grp):
-        return P.BatchRunner(shape, cfg, B, k_cap=kc, precision=args.precision, device=dev,
+    def make_runner(kc, grp, batch=B):
+        return P.BatchRunner(shape, cfg, batch, k_cap=kc, precision=args.precision, device=dev,
                              mode=args.mode, group=grp)
 
     runner = make_runner(k_cap, group)
@@ -546,6 +548,33 @@ def gpu_rank(args):
                                  "make_dense_source users hand in)",
                        "outputs_identical_to_interleaved": bool(same)}
         del bm
+
+    # ---- N > 1, weak scaling: the strong-scaling point too -- the config's
+    #      global batch split over the ranks (instances r*B/N .. (r+1)*B/N-1
+    #      of the same instance stream), timed the same way
+    strong = None
+    if world > 1 and args.scaling == "weak" and B % world == 0 and not args.no_strong:
+        sb = B // world
+        s0, _ = shard.instance_range(rank, world, total=B)
+        s_cubes = W.synthesize_batch_torch(w.dims, W.make_spectra(w, sb, s0), dev, w.noise_var,
+                                           noise_seed=w.seed * 1000003 + s0)
+        s_group = group if sb % group == 0 else 1
+        s_run = P.interleave(s_cubes, s_group) if s_group > 1 else s_cubes
+        sr = make_runner(k_cap, s_group, sb)
+        for _ in range(max(3, args.warmup)):
+            sr.run(s_run)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        s_ms, _, _ = _time_steps(lambda: sr.run(s_run), args.steps, stream, flush,
+                                 (lambda r: ops.synthesize(r, out=s_cubes)) if synth else None)
+        s_total = shard.max_over_ranks(sum(s_ms), dev)
+        strong = {"value": B / (s_total / args.steps / 1e3), "unit": UNIT,
+                  "ms_per_step": s_total / args.steps, "global_batch": B,
+                  "instances_per_rank": sb,
+                  "note": "strong scaling: the config's global batch split over the ranks "
+                          "(the main line is weak scaling: every rank a whole batch)"}
+        del sr, s_run, s_cubes
 
     # ---- result gather to rank 0 over NCCL (after the timed region, timed alone)
     gather = None
@@ -733,6 +762,7 @@ def gpu_rank(args):
             line["comm"] = {"backend": "nccl", "world": world, "allreduce_ones": comm_check,
                             "log": _nccl_log_summary(nccl_log)}
             line["gather"] = gather
+            line["strong"] = strong
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -746,7 +776,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+    ap.add_argument("--no-strong", action="store_true",
+                    help="N > 1, weak scaling: skip the strong-scaling point")
+    ap.add_argument("--scaling", default="weak", choices=["strong", "weak"],
                     help="strong: the config's global batch split over the ranks; weak: the "
                          "whole batch on every rank")
     ap.add_argument("--precision", default="auto",

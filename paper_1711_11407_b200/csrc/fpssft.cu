@@ -28,6 +28,11 @@
 #ifndef FPSSFT_PREFETCH_FROM
 #define FPSSFT_PREFETCH_FROM 4  // L2-prefetch iteration t+1 from iteration t >= this on
 #endif
+#ifndef FPSSFT_PREFETCH_SMEM
+#define FPSSFT_PREFETCH_SMEM 0  // A/B: warp kernel, lines of <= 64 points: iteration t+1 samples
+                                // copied into a second buffer (cp.async) during t (config 3
+                                // guarded 1.21 -> 1.82 ms: a second wave; -1.6 % warp cycles)
+#endif
 #ifndef FPSSFT_TEAM_GATHER_NC
 #define FPSSFT_TEAM_GATHER_NC FPSSFT_GATHER_NC
 #endif
@@ -528,10 +533,17 @@ __global__ void __launch_bounds__(1024, 1) recover_kernel(const float2 *__restri
 struct WarpLayout {
     size_t spec, slot_amp, slot_key, hash, slot_live, cand, scr_u, scr_amp;
     size_t x0d, pabs;  // GUARD only
+    size_t spec_nx;    // warp_prefetch_smem(): the next iteration's samples
     size_t per_warp, roots, roots64;
     int H;
 };
 
+// Warp kernel shapes whose next iteration's line samples are prefetched into
+// a second spectra buffer (short lines: the loop runs tens of iterations and
+// the gather latency is a fixed share of each).
+__host__ __device__ constexpr bool warp_prefetch_smem(int L, int cs, bool grouped) {
+    return FPSSFT_PREFETCH_SMEM && cs == 8 && !grouped && L <= 64 && L % 32 == 0;
+}
 __host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, int cs,
                                                        bool guard = false, bool grouped = false) {
     WarpLayout y;
@@ -547,6 +559,10 @@ __host__ __device__ inline WarpLayout make_warp_layout(int D, int L, int k_cap, 
     size_t o = 0;
     y.H = compact ? k_cap : 2 * k_cap;
     y.spec = o;      o = align16(o + (spec_bytes > sort_bytes ? spec_bytes : sort_bytes));
+    y.spec_nx = y.spec;
+    if (warp_prefetch_smem(L, cs, grouped)) {
+        y.spec_nx = o; o = align16(o + (spec_bytes > sort_bytes ? spec_bytes : sort_bytes));
+    }
     y.slot_amp = o;  o = align16(o + (size_t)k_cap * acs);
     y.slot_key = o;  o = align16(o + (size_t)k_cap * 4);
     y.hash = o;      o = align16(o + (size_t)y.H * 2);
@@ -701,6 +717,11 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
     const bool has_inst = inst < batch;
     unsigned char *base = sm + lay.roots + (size_t)warp * lay.per_warp;
     cpx<R> *spec = (cpx<R> *)(base + lay.spec);
+    // PFS: iteration t+1's samples land in spec_nx (cp.async) while t runs;
+    // the two buffers swap roles at the top of each iteration
+    constexpr bool PFS = sizeof(R) == 4 && !WG && LC != 0 && DC != 0 && warp_prefetch_smem(LC, 8, false);
+    [[maybe_unused]] cpx<R> *spec_nx = (cpx<R> *)(base + lay.spec_nx);
+    [[maybe_unused]] bool pf_ok = false;  // spec_nx holds the coming iteration's samples
     cpx<A> *slot_amp = (cpx<A> *)(base + lay.slot_amp);
     int *slot_key = (int *)(base + lay.slot_key);
     unsigned short *hash = (unsigned short *)(base + lay.hash);
@@ -742,6 +763,12 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
         nta[k] = k < D ? sched[D + k] : 0;
     }
     bool active = sched_ok && has_inst;
+    if constexpr (PFS) {
+        if (active && g.off32 && line_params_ok(g, nal, nta)) {
+            gather_lines_async<LC>((cpx<float> *)spec_nx, cube, g, nal, nta, lane, 32);
+            pf_ok = true;
+        }
+    }
     // FPSSFT_GROUP_ASSIST: group kernel of 256-point lines, unguarded float32
     constexpr bool ASSIST = FPSSFT_GROUP_ASSIST && WG != 0 && LC == 256 && DC + 1 <= 3 &&
                             sizeof(R) == 4 && !GUARD && FPSSFT_WARP_REGFFT256;
@@ -832,20 +859,29 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
         if constexpr (WG != 0) {
             // the group gather above filled the spectra
         } else if constexpr (sizeof(R) == 4) {
-            bool reg_gather = false;
+            bool reg_gather = false, pf_used = false;
+            if constexpr (PFS) {
+                if (pf_ok) {  // prefetched during the previous iteration
+                    cpx<R> *t = spec;
+                    spec = spec_nx;
+                    spec_nx = t;
+                    pf_used = true;
+                }
+            }
             // register gather for short lines (config 3: 1.2% faster), cp.async
             // for L >= 256 (config 2: 1% faster) -- measured, profiles/README.md
             if constexpr (FPSSFT_GATHER_NC && LC != 0 && LC < 256 && DC != 0 &&
                           !stage16_ok(DC, LC, 8, 32)) {
-                reg_gather = g.off32;
+                reg_gather = g.off32 && !pf_used;
                 if (reg_gather) gather_lines_nc<LC, DC>(spec, cube, g, al, ta, lane);
             }
             if constexpr (LC != 0 && stage16_ok(DC, LC, 8, 32)) {
-                staged = g.off32 && !reg_gather;
+                staged = g.off32 && !reg_gather && !pf_used;
                 if (staged)
                     par = gather_lines_cg16<LC, DC>((float4 *)spec, cube, g, al, ta, lane, &dup);
             }
-            if (!reg_gather && !staged) gather_lines_async<LC>(spec, cube, g, al, ta, lane, 32);
+            if (!reg_gather && !staged && !pf_used)
+                gather_lines_async<LC>(spec, cube, g, al, ta, lane, 32);
             if (it + 1 < kn.t_max) {
 #pragma unroll
                 for (int k = 0; k < MAXD; ++k) {
@@ -856,7 +892,7 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
                 // L2-prefetch the next iteration's lines; short ones do not --
                 // on config 2 (~3 iterations) the extra random DRAM fetches of
                 // a last-iteration prefetch cost more than the latency saved
-                if (LC != 0 && it >= FPSSFT_PREFETCH_FROM && g.off32 &&
+                if (!PFS && LC != 0 && it >= FPSSFT_PREFETCH_FROM && g.off32 &&
                     line_params_ok(g, nal, nta))
                     prefetch_lines_l2<LC>(cube, g, nal, nta, lane);
             }
@@ -864,6 +900,15 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
                 for (int b = lane; b < L; b += 32) pabs[b] = 0.f;
             cp_async_wait_all();
             __syncwarp();
+            if constexpr (PFS) {
+                // the next iteration's lines into the buffer this one left
+                // (every lane's reads of it ended before the last __syncwarp)
+                pf_ok = false;
+                if (it + 1 < kn.t_max && g.off32 && line_params_ok(g, nal, nta)) {
+                    gather_lines_async<LC>((cpx<float> *)spec_nx, cube, g, nal, nta, lane, 32);
+                    pf_ok = true;
+                }
+            }
             if constexpr (LC != 0 && stage16_ok(DC, LC, 8, 32)) {
                 if (staged) {
                     compact_stage16<LC, DC + 1, 32, WarpTeam>(spec, par, dup, lane,
@@ -1315,6 +1360,7 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
         } while (0);
     }
     if (!has_inst) return;  // (WG: a padding warp of the batch's last group)
+    if constexpr (PFS) cp_async_wait_all();  // a prefetch past the last iteration
 
     PCLK(7);
     // ---- RecoveryReport: live entries sorted by packed key (= lexicographic).

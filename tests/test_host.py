@@ -235,3 +235,24 @@ def test_segment_model_batch_major_and_interleaved():
     its = np.array([1] * 7 + [2] + [1] * 8)
     two = bench._segments_per_launch(shape, sch, np.array([2]), seg=1)
     assert bench._segments_per_launch(shape, sch, its, group=8) == two + positions
+
+
+def test_bench_scaling_plan():
+    """bench.py: weak scaling by default (every rank a whole batch, the
+    instance ranges disjoint); strong splits the config's global batch."""
+    import argparse
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    from paper_1711_11407_b200 import workloads as W
+
+    w = W.CONFIGS[2]
+    weak = argparse.Namespace(batch=None, scaling="weak", precision="auto")
+    assert bench.batch_plan(weak, w, 8) == (8 * 4096, 4096)
+    assert bench.workload_config(weak, w, 8)["scaling"] == "weak"
+    strong = argparse.Namespace(batch=None, scaling="strong", precision="auto")
+    assert bench.batch_plan(strong, w, 8) == (4096, 512)
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    assert 'ap.add_argument("--scaling", default="weak"' in src
