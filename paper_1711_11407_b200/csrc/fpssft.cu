@@ -45,6 +45,10 @@
 #ifndef FPSSFT_SYNTH_RC
 #define FPSSFT_SYNTH_RC 16  // rows per chunk of synth512_kernel
 #endif
+#ifndef FPSSFT_SYNTH_PAIR
+#define FPSSFT_SYNTH_PAIR 1  // synth512_kernel: row pairs per warp (second FFT stage without shuffles),
+                             // bank-conflict-free column order
+#endif
 #ifndef FPSSFT_SYNTH_DB
 #define FPSSFT_SYNTH_DB 0  // synth512_kernel: double-buffered chunks (measured slower)
 #endif

@@ -105,6 +105,26 @@ __global__ void __launch_bounds__(NT, 2) synth512_kernel(const int *__restrict__
         ecol[p] = freqs[src * 2];  // m0, column-sorted
     }
     __syncthreads();
+#if FPSSFT_SYNTH_PAIR
+    // column order: the 32 columns of each residue class c mod 16 ranked by
+    // descending entry count (ties by column); position = rank * 16 + residue.
+    // A half-warp then holds 16 distinct residues (its 64-bit stores into a
+    // row of V hit 16 distinct bank pairs: conflict-free) of the same rank
+    // (near-equal loop lengths).
+    int *corder = col_fill;  // col_fill is free now
+    for (int c = tid; c < NL; c += NT) {
+        const int cnt = col_start[c + 1] - col_start[c];
+        int rank = 0;
+#pragma unroll 4
+        for (int j = 0; j < NL / 16; ++j) {
+            const int c2 = (c & 15) + 16 * j;
+            const int cnt2 = col_start[c2 + 1] - col_start[c2];
+            rank += (cnt2 > cnt) || (cnt2 == cnt && c2 < c);
+        }
+        corder[rank * 16 + (c & 15)] = c;
+    }
+    __syncthreads();
+#else
     // columns by descending entry count (bucket min(count, 31)); the order
     // inside a bucket does not matter: one thread sums one column
     int *corder = col_fill;  // col_fill is free now
@@ -127,6 +147,7 @@ __global__ void __launch_bounds__(NT, 2) synth512_kernel(const int *__restrict__
     for (int c = tid; c < NL; c += NT)
         corder[atomicAdd(&ired[31 - min(col_start[c + 1] - col_start[c], 31)], 1)] = c;
     __syncthreads();
+#endif
     // per-lane twiddles e^{2 pi i lane c / 512}, c = 0..15 (exact table phases)
     float2 tw[16];
 #pragma unroll
@@ -164,6 +185,54 @@ __global__ void __launch_bounds__(NT, 2) synth512_kernel(const int *__restrict__
             for (int r = 0; r < RC; ++r) Vb[r * VS + c] = acc[r];
         }
     };
+#if FPSSFT_SYNTH_PAIR
+    // dense part of chunk r0 from buffer Vb: one warp per pair of rows.  First
+    // stage (lane b, one row at a time) as above; second stage: lane (c, q) =
+    // (lane % 16, lane / 16) holds all 32 values b of row q's column c (eight
+    // 16-byte loads per 16 values, conflict-free per quarter warp), two
+    // 16-point DFTs over the even and odd b and the radix-2 combine in its
+    // own registers: no shuffles, and every warp store writes one whole
+    // 128-byte line of each of the two rows.
+    auto dense = [&](int r0, float2 *Vb) {
+        static_assert(RW % 2 == 0, "row pairs");
+#pragma unroll 1
+        for (int rr = 0; rr < RW; rr += 2) {
+            const int r = warp * RW + rr;
+#pragma unroll 1
+            for (int q = 0; q < 2; ++q) {
+                float2 *Vr = Vb + (r + q) * VS;
+                float2 v[16];
+#pragma unroll
+                for (int a = 0; a < 16; ++a) v[a] = Vr[32 * a + lane];
+                dft16(v);
+#pragma unroll
+                for (int c = 1; c < 16; ++c) v[c] = cmul(v[c], tw[c]);
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < 16; ++c) Vr[34 * c + lane] = v[c];
+            }
+            __syncwarp();
+            const int cc = lane & 15, q = lane >> 4;
+            const float4 *X = (const float4 *)(Vb + (r + q) * VS + 34 * cc);
+            float2 e[16], o[16];
+#pragma unroll
+            for (int b = 0; b < 16; ++b) {
+                const float4 x = X[b];
+                e[b] = make_float2(x.x, x.y);
+                o[b] = make_float2(x.z, x.w);
+            }
+            dft16(e);
+            dft16(o);
+            float2 *row = img + (long long)(r0 + r + q) * NL + cc;
+#pragma unroll
+            for (int d = 0; d < 16; ++d) {
+                const float2 t = cmul(w32(d), o[d]);
+                __stcs(row + 16 * d, cadd(e[d], t));
+                __stcs(row + 16 * d + 256, csub(e[d], t));
+            }
+        }
+    };
+#else
     // dense part of chunk r0 from buffer Vb: one warp per row
     auto dense = [&](int r0, float2 *Vb) {
 #pragma unroll 1
@@ -198,6 +267,7 @@ __global__ void __launch_bounds__(NT, 2) synth512_kernel(const int *__restrict__
             }
         }
     };
+#endif
     // two V buffers: chunk k+1's sparse part and chunk k's dense part run in
     // the same phase, so one barrier per chunk and the sparse part's uneven
     // per-warp work is absorbed by the (even) dense work
