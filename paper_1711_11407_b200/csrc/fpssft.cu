@@ -49,6 +49,15 @@
 #define FPSSFT_SYNTH_PAIR 1  // synth512_kernel: row pairs per warp (second FFT stage without shuffles),
                              // bank-conflict-free column order
 #endif
+#ifndef FPSSFT_SYNTH_NT
+#define FPSSFT_SYNTH_NT 256  // threads per CTA of synth512_kernel (512 / NT CTAs per SM)
+#endif
+#ifndef FPSSFT_SYNTH_PACKED
+#define FPSSFT_SYNTH_PACKED 0  // synth512_kernel: packed float32 pairs (FADD2 / FMUL2 / FFMA2); A/B: same time
+#endif
+#ifndef FPSSFT_SYNTH_SPARSE
+#define FPSSFT_SYNTH_SPARSE 0  // A/B: 1 = packed pairs in the sparse part only, 2 = two phasor chains
+#endif
 #ifndef FPSSFT_SYNTH_DB
 #define FPSSFT_SYNTH_DB 0  // synth512_kernel: double-buffered chunks (measured slower)
 #endif
@@ -2882,15 +2891,16 @@ int fpssft_synthesize(const int32_t *freqs, const double *amps, const int32_t *c
         // config 5's 512 x 512 images in float32: register row FFTs (fpssft_synth.cuh)
         const size_t smr = align16((size_t)(FPSSFT_SYNTH_DB ? 2 : 1) * FPSSFT_SYNTH_RC * synth::VS * 8) +
                            align16((size_t)gc.L * 8) +
-                           align16((size_t)k_cap * 8) + 2 * align16((size_t)k_cap * 4) +
+                           align16((size_t)k_cap * 8) + align16((size_t)k_cap * 4) +
                            align16((size_t)513 * 4) + align16((size_t)512 * 4) + 64 * 8;
-        if ((long long)smr <= SMEM_PER_CTA) {
-            auto k = synth::synth512_kernel<FPSSFT_SYNTH_RC, 256, (bool)FPSSFT_SYNTH_DB>;
+        if ((long long)smr <= SMEM_PER_CTA &&
+            (size_t)k_cap * 4 <= (size_t)FPSSFT_SYNTH_RC * synth::VS * 8) {
+            auto k = synth::synth512_kernel<FPSSFT_SYNTH_RC, FPSSFT_SYNTH_NT, (bool)FPSSFT_SYNTH_DB>;
             cudaError_t e =
                 cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
             if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(synth512)");
-            k<<<(unsigned)batch, 256, smr, (cudaStream_t)stream>>>(freqs, amps, counts, k_cap, gc,
-                                                                   (float2 *)cubes, batch_stride);
+            k<<<(unsigned)batch, FPSSFT_SYNTH_NT, smr, (cudaStream_t)stream>>>(
+                freqs, amps, counts, k_cap, gc, (float2 *)cubes, batch_stride);
             return check_launch("synth512_kernel");
         }
     }

@@ -75,6 +75,70 @@ __device__ __forceinline__ void dft16(float2 *v) {
         for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
 }
 
+// Packed float32 pairs (sm_100 FADD2 / FMUL2 / FFMA2: one instruction per
+// complex add, two per complex multiply; the (-y, x) swap of a multiply by i
+// and the scalar broadcast fold into SASS operand modifiers).
+typedef unsigned long long f32x2_t;
+__device__ __forceinline__ f32x2_t pk2(float x, float y) {
+    f32x2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(f32x2_t a) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(a));
+    return r;
+}
+__device__ __forceinline__ float2 cadd_p(float2 a, float2 b) {
+    f32x2_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+    return upk2(r);
+}
+__device__ __forceinline__ float2 csub_p(float2 a, float2 b) {
+    f32x2_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+    return upk2(r);
+}
+// a * b = b.x (a.x, a.y) + b.y (-a.y, a.x): the data operand first, the
+// broadcast factor second (the order ptxas folds into modifiers)
+__device__ __forceinline__ float2 cmul_p(float2 a, float2 b) {
+    f32x2_t t, r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.x)));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(-a.y, a.x)), "l"(pk2(b.y, b.y)), "l"(t));
+    return upk2(r);
+}
+__device__ __forceinline__ void dft4_p(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
+    const float2 t0 = cadd_p(x0, x2), t1 = csub_p(x0, x2), t2 = cadd_p(x1, x3),
+                 t3 = mul_i(csub_p(x1, x3));
+    x0 = cadd_p(t0, t2);
+    x2 = csub_p(t0, t2);
+    x1 = cadd_p(t1, t3);
+    x3 = csub_p(t1, t3);
+}
+// dft16 with packed arithmetic (same index maps)
+__device__ __forceinline__ void dft16_p(float2 *v) {
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4_p(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+        for (int k1 = 1; k1 < 4; ++k1) {
+            if (n2 * k1 == 4)
+                v[4 * k1 + n2] = mul_i(v[4 * k1 + n2]);
+            else
+                v[4 * k1 + n2] = cmul_p(v[4 * k1 + n2], w16(n2 * k1));
+        }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4_p(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+    float2 t[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = v[i];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
+}
+
 // X[k] = sum_n v[n] e^{+2 pi i n k / 8}, in place, natural order (radix 2 x 4).
 __device__ __forceinline__ void dft8(float2 *v) {
     float2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];

@@ -25,10 +25,22 @@ namespace synth {
 // helpers: regfft:: in fpssft_regfft.cuh
 using namespace regfft;
 
+#if FPSSFT_SYNTH_PACKED
+#define SY_CMUL cmul_p
+#define SY_CADD cadd_p
+#define SY_CSUB csub_p
+#define SY_DFT16 dft16_p
+#else
+#define SY_CMUL cmul
+#define SY_CADD cadd
+#define SY_CSUB csub
+#define SY_DFT16 dft16
+#endif
+
 constexpr int VS = 544;  // row stride of V (cpx): holds the 16 x 34 exchange tile
 
 template <int RC, int NT, bool DB>
-__global__ void __launch_bounds__(NT, 2) synth512_kernel(const int *__restrict__ freqs,
+__global__ void __launch_bounds__(NT, 512 / NT) synth512_kernel(const int *__restrict__ freqs,
                                                          const double *__restrict__ amps,
                                                          const int *__restrict__ counts, int k_cap,
                                                          Geo gc, float2 *out, long long out_stride) {
@@ -43,7 +55,7 @@ __global__ void __launch_bounds__(NT, 2) synth512_kernel(const int *__restrict__
     float2 *V = (float2 *)(sm + o);      o = align16(o + (size_t)(DB ? 2 : 1) * RC * VS * 8);
     float2 *rootsL = (float2 *)(sm + o); o = align16(o + (size_t)L * 8);
     float2 *samp = (float2 *)(sm + o);   o = align16(o + (size_t)k_cap * 8);  // column-sorted
-    int *sm0 = (int *)(sm + o);          o = align16(o + (size_t)k_cap * 4);
+    int *sm0 = (int *)V;  // entry ids, set-up only: V is first written after the set-up
     int *ecol = (int *)(sm + o);         o = align16(o + (size_t)k_cap * 4);
     int *col_start = (int *)(sm + o);    o = align16(o + (size_t)(NL + 1) * 4);
     int *col_fill = (int *)(sm + o);     o = align16(o + (size_t)NL * 4);
@@ -173,13 +185,37 @@ __global__ void __launch_bounds__(NT, 2) synth512_kernel(const int *__restrict__
                 const unsigned m0 = (unsigned)ecol[p];
                 const unsigned step = fastmod((unsigned)c0 * m0, magicL, (unsigned)L);
                 const unsigned u = fastmod(r0L * m0, magicL, (unsigned)L);
-                float2 z = cmul(samp[p], rootsL[u]);
+#if FPSSFT_SYNTH_SPARSE == 1  // A/B: packed pairs in the sparse part only
+                float2 z = cmul_p(samp[p], rootsL[u]);
                 const float2 ws = rootsL[step];
 #pragma unroll
                 for (int r = 0; r < RC; ++r) {
-                    acc[r] = cadd(acc[r], z);
-                    if (r + 1 < RC) z = cmul(z, ws);
+                    acc[r] = cadd_p(acc[r], z);
+                    if (r + 1 < RC) z = cmul_p(z, ws);
                 }
+#elif FPSSFT_SYNTH_SPARSE == 2  // A/B: two interleaved phasor chains (rows r, r + 1 step by ws^2)
+                float2 z = cmul(samp[p], rootsL[u]);
+                const float2 ws = rootsL[step];
+                float2 z1 = cmul(z, ws);
+                const float2 ws2 = cmul(ws, ws);
+#pragma unroll
+                for (int r = 0; r < RC; r += 2) {
+                    acc[r] = cadd(acc[r], z);
+                    acc[r + 1] = cadd(acc[r + 1], z1);
+                    if (r + 2 < RC) {
+                        z = cmul(z, ws2);
+                        z1 = cmul(z1, ws2);
+                    }
+                }
+#else
+                float2 z = SY_CMUL(samp[p], rootsL[u]);
+                const float2 ws = rootsL[step];
+#pragma unroll
+                for (int r = 0; r < RC; ++r) {
+                    acc[r] = SY_CADD(acc[r], z);
+                    if (r + 1 < RC) z = SY_CMUL(z, ws);
+                }
+#endif
             }
 #pragma unroll
             for (int r = 0; r < RC; ++r) Vb[r * VS + c] = acc[r];
@@ -204,9 +240,9 @@ __global__ void __launch_bounds__(NT, 2) synth512_kernel(const int *__restrict__
                 float2 v[16];
 #pragma unroll
                 for (int a = 0; a < 16; ++a) v[a] = Vr[32 * a + lane];
-                dft16(v);
+                SY_DFT16(v);
 #pragma unroll
-                for (int c = 1; c < 16; ++c) v[c] = cmul(v[c], tw[c]);
+                for (int c = 1; c < 16; ++c) v[c] = SY_CMUL(v[c], tw[c]);
                 __syncwarp();
 #pragma unroll
                 for (int c = 0; c < 16; ++c) Vr[34 * c + lane] = v[c];
@@ -221,14 +257,14 @@ __global__ void __launch_bounds__(NT, 2) synth512_kernel(const int *__restrict__
                 e[b] = make_float2(x.x, x.y);
                 o[b] = make_float2(x.z, x.w);
             }
-            dft16(e);
-            dft16(o);
+            SY_DFT16(e);
+            SY_DFT16(o);
             float2 *row = img + (long long)(r0 + r + q) * NL + cc;
 #pragma unroll
             for (int d = 0; d < 16; ++d) {
-                const float2 t = cmul(w32(d), o[d]);
-                __stcs(row + 16 * d, cadd(e[d], t));
-                __stcs(row + 16 * d + 256, csub(e[d], t));
+                const float2 t = SY_CMUL(o[d], w32(d));
+                __stcs(row + 16 * d, SY_CADD(e[d], t));
+                __stcs(row + 16 * d + 256, SY_CSUB(e[d], t));
             }
         }
     };
