@@ -55,6 +55,10 @@
 #ifndef FPSSFT_SYNTH_PACKED
 #define FPSSFT_SYNTH_PACKED 0  // synth512_kernel: packed float32 pairs (FADD2 / FMUL2 / FFMA2); A/B: same time
 #endif
+#ifndef FPSSFT_SYNTH_QUAD
+#define FPSSFT_SYNTH_QUAD 1  // synth512_kernel: a chunk is 4 rows of each quarter of the image, whose sparse
+                             // parts share one phasor recurrence (quarter-period shift = i^(m0 q))
+#endif
 #ifndef FPSSFT_SYNTH_SPARSE
 #define FPSSFT_SYNTH_SPARSE 0  // A/B: 1 = packed pairs in the sparse part only, 2 = two phasor chains
 #endif

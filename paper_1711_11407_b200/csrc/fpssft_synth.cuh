@@ -25,6 +25,9 @@ namespace synth {
 // helpers: regfft:: in fpssft_regfft.cuh
 using namespace regfft;
 
+#if FPSSFT_SYNTH_QUAD && !(FPSSFT_SYNTH_PAIR && FPSSFT_SYNTH_RC == 16 && FPSSFT_SYNTH_SPARSE == 0)
+#error "FPSSFT_SYNTH_QUAD needs the row-pair dense part, 16-row chunks and the default sparse part"
+#endif
 #if FPSSFT_SYNTH_PACKED
 #define SY_CMUL cmul_p
 #define SY_CADD cadd_p
@@ -171,7 +174,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) synth512_kernel(const int *__res
     // long loops; each entry's RC row phasors a w^{u0 + r step} by recurrence
     // from the exact table value at the chunk's first row (|error| ~ RC ulp)
     auto sparse = [&](int r0, float2 *Vb) {
-        const unsigned r0L = fastmod((unsigned)c0 * (unsigned)r0, magicL, (unsigned)L);
+        // QUAD: chunk r0 holds rows (r0 / 4) + j + (N0 / 4) q
+        const unsigned r0L = fastmod((unsigned)c0 * (unsigned)(FPSSFT_SYNTH_QUAD ? r0 >> 2 : r0),
+                                     magicL, (unsigned)L);
         for (int i = 0; i < NL / NT; ++i) {
             // snake over the count-sorted columns: warp w takes group w of even
             // passes and group NW-1-w of odd ones, evening out the warps' loads
@@ -206,6 +211,24 @@ __global__ void __launch_bounds__(NT, 512 / NT) synth512_kernel(const int *__res
                         z = cmul(z, ws2);
                         z1 = cmul(z1, ws2);
                     }
+                }
+#elif FPSSFT_SYNTH_QUAD
+                // rows n0 + j + (N0/4) q, j, q = 0..3: the quarter-period shift
+                // multiplies an entry's phasor by i^(m0 q), a swap and signs
+                // (per-entry constants), so one recurrence step serves 4 rows
+                float2 z = cmul(samp[p], rootsL[u]);
+                const float2 ws = rootsL[step];
+                const bool sw = (m0 & 1u) != 0;
+                const float sx = ((m0 + 1u) & 2u) ? -1.f : 1.f, sy = (m0 & 2u) ? -1.f : 1.f;
+                const float s2 = sw ? -1.f : 1.f, sx3 = s2 * sx, sy3 = s2 * sy;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float tx = sw ? z.y : z.x, ty = sw ? z.x : z.y;
+                    acc[j] = cadd(acc[j], z);
+                    acc[4 + j] = make_float2(fmaf(sx, tx, acc[4 + j].x), fmaf(sy, ty, acc[4 + j].y));
+                    acc[8 + j] = make_float2(fmaf(s2, z.x, acc[8 + j].x), fmaf(s2, z.y, acc[8 + j].y));
+                    acc[12 + j] = make_float2(fmaf(sx3, tx, acc[12 + j].x), fmaf(sy3, ty, acc[12 + j].y));
+                    if (j + 1 < 4) z = cmul(z, ws);
                 }
 #else
                 float2 z = SY_CMUL(samp[p], rootsL[u]);
@@ -259,7 +282,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) synth512_kernel(const int *__res
             }
             SY_DFT16(e);
             SY_DFT16(o);
+#if FPSSFT_SYNTH_QUAD
+            const int rq = r + q;  // chunk row -> image row (r0 / 4) + rq % 4 + (N0 / 4) (rq / 4)
+            float2 *row = img + (long long)((r0 >> 2) + (rq & 3) + (N0 >> 2) * (rq >> 2)) * NL + cc;
+#else
             float2 *row = img + (long long)(r0 + r + q) * NL + cc;
+#endif
 #pragma unroll
             for (int d = 0; d < 16; ++d) {
                 const float2 t = SY_CMUL(o[d], w32(d));
