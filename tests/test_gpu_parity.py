@@ -331,7 +331,12 @@ def test_lazy_source_is_materialised():
 
 # ------------------------------------------------------------ re-synthesis
 @pytest.mark.parametrize("dims,k", [((512, 512), 500), ((12, 18), 9), ((4, 6, 5), 7), ((32,), 5),
-                                    ((64, 64, 64), 200), ((256, 256), 100), ((10, 15), 150)])
+                                    ((64, 64, 64), 200), ((256, 256), 100), ((10, 15), 150),
+                                    # synth512_kernel (512-point rows) with other row counts /
+                                    # line lengths and crowded columns (its quarter-image chunks,
+                                    # column ranking and entry sort)
+                                    ((128, 512), 300), ((48, 512), 300), ((1024, 512), 700),
+                                    ((64, 512), 2000)])
 @pytest.mark.parametrize("prec", ["fp32", "fp64"])
 def test_synthesize_matches_dense_evaluation(dims, k, prec, rng):
     """a15: dense re-synthesis vs the float64 evaluation of the same spectra
