@@ -112,6 +112,31 @@ int fpssft_run_batch_grouped(const void *cubes, int64_t batch, int32_t group,
                              void *stream);
 
 /*
+ * The same loop over an interleaved batch (fpssft_run_batch_grouped, one
+ * schedule for the batch) held in pinned, mapped HOST memory, with the line
+ * samples of the first `stage_iterations` iterations staged through HBM: the
+ * schedule is data-independent (driver.py:131,142-143), so those samples
+ * (extract_line, lines.py:36-64 + core.py:236-238) are known before the loop
+ * starts.  A staging kernel copies each needed 8*group-byte segment with one
+ * TMA bulk copy (group = 32: 256-byte segments, the host link's bulk rate
+ * instead of the request-rate bound of SM loads) into
+ * staging[group][t][line][l][group]; the recovery kernel reads iterations
+ * t < stage_iterations from there and later (straggler) iterations from the
+ * host cube.  Outputs identical to fpssft_run_batch_grouped.  float32, shapes
+ * the group-gather kernel is built for (FPSSFT_EUNSUPPORTED otherwise);
+ * cubes may also be device memory.
+ *   staging: device buffer of fpssft_stage_bytes(shape, group, batch,
+ *            min(stage_iterations, params->t_max)) bytes.
+ */
+int64_t fpssft_stage_bytes(const fpssft_shape *shape, int32_t group, int64_t batch,
+                           int32_t stage_iterations);
+int fpssft_run_batch_staged(const void *cubes, int64_t batch, int32_t group,
+                            int64_t group_stride, const fpssft_shape *shape,
+                            const fpssft_params *params, const int32_t *schedule,
+                            const fpssft_out *out, void *staging, int64_t staging_bytes,
+                            int32_t stage_iterations, void *stream);
+
+/*
  * D+1 line spectra of one iteration per instance.  Replaces
  *   [dft_forward(extract_line(DenseSource(cube), LineParams(alpha, off, L)))
  *    for off in decoding_offsets(tau)]

@@ -20,7 +20,8 @@ MODES = {"auto": MODE_AUTO, "cta": MODE_CTA, "warp": MODE_WARP}
 TERM_NAMES = {0: "residual_clean", 1: "stall", 2: "max_iterations", 3: "k_cap_overflow",
               -1: "invalid_schedule"}
 
-EXPORTS = ("fpssft_run_batch", "fpssft_run_batch_grouped", "fpssft_line_spectra", "fpssft_gather_lines", "fpssft_dft_forward",
+EXPORTS = ("fpssft_run_batch", "fpssft_run_batch_grouped", "fpssft_run_batch_staged",
+           "fpssft_stage_bytes", "fpssft_line_spectra", "fpssft_gather_lines", "fpssft_dft_forward",
            "fpssft_synthesize", "fpssft_recover_large", "fpssft_recover_large_workspace",
            "fpssft_decode_spectra", "fpssft_project_onto_bins", "fpssft_smem_bytes",
            "fpssft_block_threads", "fpssft_plan", "fpssft_plan_batch", "fpssft_launches_per_batch",
@@ -70,6 +71,11 @@ def lib() -> C.CDLL:
                                        I32, C.POINTER(Out), P]
         h.fpssft_run_batch_grouped.argtypes = [P, I64, I32, I64, C.POINTER(Shape),
                                                C.POINTER(Params), P, P, I32, C.POINTER(Out), P]
+        h.fpssft_run_batch_staged.argtypes = [P, I64, I32, I64, C.POINTER(Shape),
+                                              C.POINTER(Params), P, C.POINTER(Out), P, I64, I32,
+                                              P]
+        h.fpssft_stage_bytes.argtypes = [C.POINTER(Shape), I32, I64, I32]
+        h.fpssft_stage_bytes.restype = I64
         h.fpssft_line_spectra.argtypes = [P, I64, I64, C.POINTER(Shape), P, I32, P, I32, P]
         h.fpssft_dft_forward.argtypes = [P, I64, I32, P, I32, P]
         h.fpssft_gather_lines.argtypes = [P, I32, I64, I64, C.POINTER(Shape), P, I32, P, I32, P]
@@ -95,7 +101,7 @@ def lib() -> C.CDLL:
         h.fpssft_last_error.restype = C.c_char_p
         for name in EXPORTS:
             if name not in ("fpssft_smem_bytes", "fpssft_last_error",
-                            "fpssft_recover_large_workspace"):
+                            "fpssft_recover_large_workspace", "fpssft_stage_bytes"):
                 getattr(h, name).restype = C.c_int
         _lib = h
     return _lib

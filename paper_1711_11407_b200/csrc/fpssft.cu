@@ -116,6 +116,9 @@
 #ifndef FPSSFT_GROUP_MINB
 #define FPSSFT_GROUP_MINB 2  // group kernel: CTAs per SM its registers must allow (3: compact layout)
 #endif
+#ifndef FPSSFT_GROUP_LATE
+#define FPSSFT_GROUP_LATE 1  // group kernel: finished warps gather after the barrier (0: A/B)
+#endif
 #ifndef FPSSFT_GROUP_PF
 #define FPSSFT_GROUP_PF 0  // group kernel: L2-prefetch iteration t+1 during t for t + 1 < this
 #endif
@@ -805,7 +808,21 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
             const bool lines_ok = line_params_ok(g, al, ta);
             PCLK(0);
             GroupGather<LC, DC, WG> gg;
-            if (lines_ok) gg.load(gbase, g, al, ta, team_tid);
+            auto group_load = [&]() {
+                if (kn.staged != nullptr && it < kn.stage_T)
+                    gg.load_staged(kn.staged + (inst0 / kn.group) * kn.staged_group_stride +
+                                       (inst0 % kn.group),
+                                   it, kn.group, team_tid);
+                else
+                    gg.load(gbase, g, al, ta, team_tid);
+            };
+            // a warp whose instance has finished sends its share of the gather
+            // only once the barrier has shown that some member continues: the
+            // team's last pass (nobody left) then reads nothing.  (A running
+            // member is the last to arrive, so its own share already exposes
+            // one memory latency in a straggler iteration: no longer path.)
+            const bool early = !FPSSFT_GROUP_LATE || active;
+            if (lines_ok && early) group_load();
             if constexpr (ASSIST)
                 if (lane == 0) s_act[warp] = (int)(active && lines_ok);
             const bool any = team_is_cta ? __syncthreads_or(active && lines_ok)
@@ -815,6 +832,7 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
                 break;
             }
             PCLK(1);
+            if (!early) group_load();
             gg.store(spec0, (int)(lay.per_warp / sizeof(cpx<float>)), team_tid);
             if (it + 1 < kn.t_max) {
 #pragma unroll
@@ -1921,6 +1939,7 @@ __global__ void __launch_bounds__(1024, 1) project_kernel(const int *__restrict_
 
 #include "fpssft_large.cuh"
 #include "fpssft_loop.cuh"
+#include "fpssft_stage.cuh"
 
 // ================================================================== host
 namespace {
@@ -2132,6 +2151,9 @@ int make_knobs(const fpssft_params *p, Knobs *k) {
     k->stall_limit = p->stall_limit;
     k->k_cap = p->k_cap;
     k->group = 1;
+    k->staged = nullptr;
+    k->staged_group_stride = 0;
+    k->stage_T = 0;
     return FPSSFT_OK;
 }
 
@@ -2276,14 +2298,17 @@ int warp_kernel_regs(const Geo &g, int precision, int k_cap) {
 // width in warps (*wg): 16-wide when the group is a multiple of 16 (one
 // 128-byte read per position serves 16 instances: the host-memory path's
 // request economy, tools/zc_group_probe.py), else 8-wide.
-const void *group_kernel_for(const Geo &g, int precision, int group, int k_cap, int *wg = nullptr) {
+// (narrow: the 8-wide kernel whatever the group -- staged lines come from HBM,
+// where it is the faster one.)
+const void *group_kernel_for(const Geo &g, int precision, int group, int k_cap, int *wg = nullptr,
+                             bool narrow = false) {
     if (!FPSSFT_GROUP_WG || precision != FPSSFT_F32 || !g.off32 || group < FPSSFT_GROUP_WG ||
         group % FPSSFT_GROUP_WG)
         return nullptr;
 #if FPSSFT_GROUP_WG
     if (g.D == 2 && g.L == 256) {
 #if FPSSFT_GROUP_WIDE
-        if (group % FPSSFT_GROUP_WIDE == 0) {
+        if (group % FPSSFT_GROUP_WIDE == 0 && !narrow) {
             if (wg) *wg = FPSSFT_GROUP_WIDE;
             return k_cap == 128
                        ? (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_WIDE, 128>
@@ -2333,7 +2358,9 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp,
                                 warp_kernel_for(gw, precision, kn.k_cap)};
             int gwd = FPSSFT_GROUP_WG;
             const void *gk =
-                shared_sched ? group_kernel_for(gw, precision, kn.group, kn.k_cap, &gwd) : nullptr;
+                shared_sched ? group_kernel_for(gw, precision, kn.group, kn.k_cap, &gwd,
+                                               kn.staged != nullptr)
+                             : nullptr;
             if (best_w && gk) {
                 const WarpLayout gl = make_warp_layout(g.D, g.L, kn.k_cap, cs, false, true);
                 const size_t smem = gl.roots + (size_t)gwd * gl.per_warp;
@@ -2464,7 +2491,9 @@ int run_batch_t(const void *cubes, int64_t batch, int64_t batch_stride, Geo g,
         int sms = 0, dev = 0;
         if (lp.per_cta > 1 && lp.threads == 32 * lp.per_cta && cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-            sms > 0 && lp.kernel != group_kernel_for(g, prec, kn.group, kn.k_cap)) {
+            sms > 0 &&
+            lp.kernel != group_kernel_for(g, prec, kn.group, kn.k_cap, nullptr,
+                                          kn.staged != nullptr)) {
             const long long want = (batch + sms - 1) / sms;
             if (want < lp.per_cta) {
                 const WarpLayout wl = make_warp_layout(g.D, g.L, kn.k_cap, sizeof(R) == 8 ? 16 : 8,
@@ -2867,6 +2896,73 @@ int fpssft_run_batch_grouped(const void *cubes, int64_t batch, int32_t group,
                                    sched_index, n_sched, o, st);
     return run_batch_t<float>(cubes, batch, batch_stride, g, kn, params->mode, schedule,
                               sched_index, n_sched, o, st);
+}
+
+int64_t fpssft_stage_bytes(const fpssft_shape *shape, int32_t group, int64_t batch,
+                           int32_t stage_iterations) {
+    Geo g;
+    if (make_geo(shape, &g) != FPSSFT_OK) return -1;
+    if (group < 2 || group > 64 || (group & 1) || batch < 0 || stage_iterations < 1) return -1;
+    const int64_t groups = (batch + group - 1) / group;
+    return groups * stage_iterations * (int64_t)g.nlines * g.L * group * 8;
+}
+
+int fpssft_run_batch_staged(const void *cubes, int64_t batch, int32_t group,
+                            int64_t group_stride, const fpssft_shape *shape,
+                            const fpssft_params *params, const int32_t *schedule,
+                            const fpssft_out *out, void *staging, int64_t staging_bytes,
+                            int32_t stage_iterations, void *stream) {
+    Geo g;
+    Knobs kn;
+    int rc;
+    if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
+    if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
+    if (group < 2 || group > 64 || (group & 1))
+        return fail(FPSSFT_EINVAL, "staged lines: group must be even, in [2, 64]");
+    if (stage_iterations < 1) return fail(FPSSFT_EINVAL, "stage_iterations must be >= 1");
+    if (params->precision != FPSSFT_F32 ||
+        !group_kernel_for(g, FPSSFT_F32, group, params->k_cap, nullptr, true))
+        return fail(FPSSFT_EUNSUPPORTED,
+                    "staged lines need the group-gather kernel (float32, a shape it is built "
+                    "for, group a multiple of its width)");
+    if (batch < 0 || batch > INT_MAX) return fail(FPSSFT_EINVAL, "bad batch");
+    if (batch == 0) return FPSSFT_OK;
+    const int T0 = std::min<int>(stage_iterations, kn.t_max);
+    const int64_t need = fpssft_stage_bytes(shape, group, batch, T0);
+    if (!cubes || !schedule || !staging) return fail(FPSSFT_EINVAL, "NULL buffer");
+    if (staging_bytes < need)
+        return fail(FPSSFT_EINVAL, "staging buffer smaller than fpssft_stage_bytes()");
+    for (int k = 0; k < g.D; ++k)
+        if (shape->strides[k] % group)
+            return fail(FPSSFT_EINVAL, "staged lines: strides must be multiples of group");
+    if (((uintptr_t)cubes | (uintptr_t)staging) & 15 || (group_stride * 8) % 16)
+        return fail(FPSSFT_EINVAL, "staged lines: 16-byte aligned cubes and staging buffer");
+    const int64_t groups = (batch + group - 1) / group;
+    if (groups > 65535 || T0 > 65535) return fail(FPSSFT_EINVAL, "staged lines: too many groups");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int NLL = g.nlines * g.L;
+    const size_t smem = (size_t)stage::POS * 8 * group;
+    cudaError_t e = cudaFuncSetAttribute(stage::stage_lines_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stage_lines_kernel)");
+    const long long sgs = (long long)T0 * NLL * group;
+    dim3 grid((unsigned)((NLL + stage::POS - 1) / stage::POS), (unsigned)T0, (unsigned)groups);
+    stage::stage_lines_kernel<<<grid, stage::POS, smem, st>>>(
+        (const float2 *)cubes, (long long)group_stride, g, group, schedule, T0,
+        (float2 *)staging, sgs);
+    if ((rc = check_launch("stage_lines_kernel")) != FPSSFT_OK) return rc;
+    kn.group = group;
+    kn.staged = (const float2 *)staging;
+    kn.staged_group_stride = sgs;
+    kn.stage_T = T0;
+    set_noise_floor(&kn, g, FPSSFT_F32);
+    if (!out || !out->freqs || !out->amps || !out->count || !out->iterations ||
+        !out->samples_used || !out->terminated_by)
+        return fail(FPSSFT_EINVAL, "NULL buffer");
+    OutPtrs o{out->freqs, out->amps, out->count, out->iterations,
+              (long long *)out->samples_used, out->terminated_by, out->iter_stats};
+    return run_batch_t<float>(cubes, batch, group_stride, g, kn, params->mode, schedule, nullptr,
+                              1, o, st);
 }
 
 int fpssft_synthesize(const int32_t *freqs, const double *amps, const int32_t *counts,

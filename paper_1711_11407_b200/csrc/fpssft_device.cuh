@@ -126,6 +126,11 @@ struct Knobs {
     double guard_coef;  // guarded float32: transform error bound coef * sqrt(sum |x|^2)
     int t_max, stall_limit, k_cap;
     int group;  // instances interleaved per sample (batch layout [B/group, *dims, group])
+    // staged lines (fpssft_stage.cuh): iterations t < stage_T of a group read
+    // their line samples from staged[group][t][line][l][group] instead of the cube
+    const float2 *staged;
+    long long staged_group_stride;
+    int stage_T;
 };
 
 // Base of instance `inst`'s cube: batch layout [B/G, *dims, G] (G = kn.group
@@ -622,6 +627,16 @@ struct GroupGather {
                 v[i * LQ + j] = ld_nc16(gbase + off + 2 * c);
             }
         }
+    }
+    // iteration `it` from the staging buffer (fpssft_stage.cuh): sbase = the
+    // team's first member in staged[group], positions in line order, G
+    // instances per position
+    __device__ __forceinline__ void load_staged(const float2 *__restrict__ sbase, int it, int G,
+                                                int tid) {
+        const int c = tid % CH, q0 = tid / CH;
+        const float2 *p = sbase + ((long long)it * (NL * LC) + q0) * G + 2 * c;
+#pragma unroll
+        for (int t = 0; t < PPT; ++t) v[t] = ld_nc16(p + (long long)(QS * t) * G);
     }
     // the same segments into L2 only (one request per 64-byte segment: the
     // thread that loads the segment's first chunk)

@@ -274,12 +274,23 @@ class BatchRunner:
 
     def __init__(self, shape: CubeShape, config: FpsSftConfig, batch: int, *, schedule=None,
                  sched_index=None, k_cap: int = 256, precision: str = "auto",
-                 iter_stats: bool = False, device=None, mode: str = "auto", group: int = 1):
+                 iter_stats: bool = False, device=None, mode: str = "auto", group: int = 1,
+                 stage_iterations: int = 0):
         import torch
 
         if not 1 <= int(group) <= 64:
             raise ValueError("group must be in [1, 64]")
         self.group = int(group)
+        # stage_iterations > 0 (interleaved batch, one schedule): the line
+        # samples of the first iterations are staged through HBM by TMA bulk
+        # copies (``fpssft_run_batch_staged``: a pinned host batch then crosses
+        # the link at its bulk rate instead of the SM loads' request rate)
+        self.stage_iterations = int(stage_iterations)
+        if self.stage_iterations < 0:
+            raise ValueError("stage_iterations must be >= 0")
+        if self.stage_iterations and (self.group < 2 or self.group % 2 or sched_index is not None):
+            raise ValueError("staged lines need an interleaved batch (even group) that shares "
+                             "one schedule")
         self.shape = shape
         self.config = config
         self.batch = int(batch)
@@ -314,6 +325,15 @@ class BatchRunner:
                             N.ptr(o["terminated_by"]), N.ptr(o["iter_stats"]))
         self.smem_bytes = self.plan["smem_bytes"]
         self.threads = self.plan["threads_per_cta"]
+        self._staging = None
+        if self.stage_iterations:
+            if self.schedule_host.shape[0] != 1:
+                raise ValueError("staged lines need a single schedule")
+            nbytes = int(N.lib().fpssft_stage_bytes(C_ref(self._shape_c), self.group, self.batch,
+                                                    min(self.stage_iterations, self.t_max)))
+            if nbytes < 0:
+                raise ValueError("staged lines: unsupported shape / group")
+            self._staging = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=self.device)
 
     def run(self, cubes) -> BatchResult:
         import torch
@@ -344,10 +364,17 @@ class BatchRunner:
         # budget of the algorithm); its UVA address is valid on the device
         dev = cubes.device if cubes.is_cuda else self.device
         with torch.cuda.device(dev):
-            N.check(N.lib().fpssft_run_batch_grouped(
-                N.ptr(cubes), self.batch, G, int(cubes.stride(0)), C_ref(sh),
-                C_ref(self._params_c), N.ptr(self.schedule), N.ptr(self.sched_index),
-                int(self.schedule_host.shape[0]), C_ref(self._out_c), N.stream_ptr(dev)))
+            if self._staging is not None:
+                N.check(N.lib().fpssft_run_batch_staged(
+                    N.ptr(cubes), self.batch, G, int(cubes.stride(0)), C_ref(sh),
+                    C_ref(self._params_c), N.ptr(self.schedule), C_ref(self._out_c),
+                    N.ptr(self._staging), int(self._staging.numel()), self.stage_iterations,
+                    N.stream_ptr(dev)))
+            else:
+                N.check(N.lib().fpssft_run_batch_grouped(
+                    N.ptr(cubes), self.batch, G, int(cubes.stride(0)), C_ref(sh),
+                    C_ref(self._params_c), N.ptr(self.schedule), N.ptr(self.sched_index),
+                    int(self.schedule_host.shape[0]), C_ref(self._out_c), N.stream_ptr(dev)))
         o = self.out
         return BatchResult(self.shape, self.k_cap, o["freqs"], o["amps"], o["count"],
                            o["iterations"], o["samples_used"], o["terminated_by"],

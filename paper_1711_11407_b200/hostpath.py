@@ -71,7 +71,7 @@ class HostBatchRunner:
                  k_cap: int = 256, precision: str = "auto", device=None, mode: str = "auto",
                  zero_copy_fraction: float | None = None, chunk: int | None = None,
                  chunk_bytes: int = 256 << 20, schedule=None, sched_index=None,
-                 graphs: bool = True, group: int = 1):
+                 graphs: bool = True, group: int = 1, stage_iterations: int = 0):
         import torch
 
         if mode not in ("auto", "copy", "zero_copy", "split"):
@@ -82,6 +82,13 @@ class HostBatchRunner:
         # segment serving G instances (config 2: 6.7 vs 23 ms per batch
         # batch-major, tools/zc_group_probe.py)
         self.group = int(group)
+        # stage_iterations > 0: the first iterations' line samples cross the
+        # link as TMA bulk copies of whole 8 G-byte segments into an HBM staging
+        # buffer (fpssft_run_batch_staged; G = 32: 256-byte segments at the
+        # link's bulk rate, tools/seg_probe.cu), later iterations in place
+        self.stage_iterations = int(stage_iterations)
+        if self.stage_iterations and self.group < 2:
+            raise ValueError("staged lines need an interleaved host batch (group >= 2)")
         if self.group > 1:
             if mode not in ("auto", "zero_copy"):
                 raise ValueError("an interleaved host batch is gathered in place (zero_copy)")
@@ -154,7 +161,7 @@ class HostBatchRunner:
             si = None if self._sched_index is None else self._sched_index[b0:b0 + n]
             r = BatchRunner(self.shape, self.config, n, schedule=self._schedule, sched_index=si,
                             k_cap=self.k_cap, precision=self.precision, device=self.device,
-                            group=self.group)
+                            group=self.group, stage_iterations=self.stage_iterations)
             self._runners[key] = r
         return r
 

@@ -179,3 +179,51 @@ def test_interleaved_host_batch_gathered_in_place(G):
             assert torch.equal(v, dev.out[k].cpu()), k
     with pytest.raises(ValueError):
         hr.run(torch.empty((B, *w.dims), dtype=torch.complex64, pin_memory=True))
+
+
+@pytest.mark.parametrize("G,T0,B", [(32, 3, 96), (32, 1, 70), (16, 2, 64), (8, 50, 40), (64, 3, 64)])
+def test_staged_lines_from_interleaved_host_batch(G, T0, B):
+    """fpssft_run_batch_staged: the first T0 iterations' line samples staged
+    through HBM by TMA bulk copies of whole 8 G-byte host segments, later
+    iterations gathered in place -- outputs bit-identical to the batch-major
+    device run (partial last group, T0 beyond the iteration cap included)."""
+    import numpy as np
+
+    w = W.CONFIGS[2]
+    inst = [W.make_instance(w, r) for r in W.instance_rngs(w.seed, B)]
+    cubes = torch.as_tensor(np.stack([c for _, _, c in inst])).cuda()
+    cfg = P.FpsSftConfig(seed=2, **P.PROFILES["P32"])
+    shape = P.CubeShape(w.dims)
+    dev = P.BatchRunner(shape, cfg, B, k_cap=128)
+    dev.run(cubes)
+    assert int(dev.out["iterations"].max()) > 1
+    il = P.interleave(cubes, G)
+    host = torch.empty(il.shape, dtype=il.dtype, pin_memory=True)
+    host.copy_(il)
+    hr = HostBatchRunner(shape, cfg, B, k_cap=128, group=G, stage_iterations=T0)
+    for _ in range(2):  # second run: the captured graph
+        out = hr.run(host)
+        for k, v in out.items():
+            if v is not None:
+                assert torch.equal(v, dev.out[k].cpu()), k
+    # the same from a device-resident interleaved batch
+    st = P.BatchRunner(shape, cfg, B, k_cap=128, group=G, stage_iterations=T0)
+    st.run(il)
+    for k, v in st.out.items():
+        if v is not None:
+            assert torch.equal(v, dev.out[k]), k
+
+
+def test_staged_lines_argument_errors():
+    w = W.CONFIGS[2]
+    shape = P.CubeShape(w.dims)
+    cfg = P.FpsSftConfig(seed=2, **P.PROFILES["P32"])
+    with pytest.raises(ValueError):
+        P.BatchRunner(shape, cfg, 8, k_cap=128, group=1, stage_iterations=3)
+    with pytest.raises(ValueError):
+        P.BatchRunner(shape, cfg, 8, k_cap=128, group=8, stage_iterations=3,
+                      sched_index=[0] * 8)
+    with pytest.raises(ValueError):  # no group kernel for this shape
+        r = P.BatchRunner(P.CubeShape((64, 64, 64)), cfg, 8, k_cap=128, group=8,
+                          stage_iterations=3)
+        r.run(torch.zeros((1, 64, 64, 64, 8), dtype=torch.complex64, device=DEV))
