@@ -722,8 +722,9 @@ def gpu_rank(args):
         sg, st0 = args.host_stage_group, args.host_stage_iterations
         if group > 1 and not synth and sg > 1 and st0 > 0 and B % sg == 0:
             try:
+                pipe = args.host_stage_pipeline if B % (sg * args.host_stage_pipeline) == 0 else 1
                 hr = HostBatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision,
-                                     device=dev, group=sg, stage_iterations=st0)
+                                     device=dev, group=sg, stage_iterations=st0, pipeline=pipe)
                 host_il = P.interleave(cubes, sg)
                 host = torch.empty(host_il.shape, dtype=host_il.dtype, pin_memory=True)
                 host.copy_(host_il)
@@ -745,7 +746,9 @@ def gpu_rank(args):
                                   f"samples of iterations 0..{t0 - 1} of all {B} instances staged "
                                   f"through HBM by one TMA bulk copy per {8 * sg}-byte segment "
                                   f"(fpssft_run_batch_staged), later iterations gathered in place "
-                                  f"(64-byte reads per 8-instance team); results to pinned host",
+                                  f"(64-byte reads per 8-instance team); {pipe} chunks pipelined "
+                                  f"(chunk i+1 staged while chunk i recovers and its results "
+                                  f"return); results to pinned host",
                           "note": "h2d = staged segments x segment bytes + 64 B per position of "
                                   "the teams' iterations past the staged ones",
                           "outputs_identical_to_device_run": bool(all(
@@ -850,6 +853,8 @@ def main():
     ap.add_argument("--host-stage-group", type=int, default=32,
                     help="interleave group of the staged e2e host batch (32: 256-byte segments, "
                          "one TMA bulk copy each; 0 = off)")
+    ap.add_argument("--host-stage-pipeline", type=int, default=4,
+                    help="chunks of the staged e2e batch pipelined over two streams")
     ap.add_argument("--host-stage-iterations", type=int, default=5,
                     help="iterations whose line samples the staged e2e path copies up front")
     ap.add_argument("--no-e2e", action="store_true")

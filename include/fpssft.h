@@ -134,7 +134,14 @@ int fpssft_run_batch_staged(const void *cubes, int64_t batch, int32_t group,
                             int64_t group_stride, const fpssft_shape *shape,
                             const fpssft_params *params, const int32_t *schedule,
                             const fpssft_out *out, void *staging, int64_t staging_bytes,
-                            int32_t stage_iterations, void *stream);
+                            int32_t stage_iterations, int32_t already_staged, void *stream);
+/* The staging pass alone (already_staged != 0 above then skips it): lets a
+ * caller stage the next chunk of a batch on one stream while the previous
+ * chunk recovers on another (hostpath.py). */
+int fpssft_stage_lines(const void *cubes, int64_t batch, int32_t group, int64_t group_stride,
+                       const fpssft_shape *shape, const fpssft_params *params,
+                       const int32_t *schedule, void *staging, int64_t staging_bytes,
+                       int32_t stage_iterations, void *stream);
 
 /*
  * D+1 line spectra of one iteration per instance.  Replaces

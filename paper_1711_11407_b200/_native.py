@@ -21,7 +21,7 @@ TERM_NAMES = {0: "residual_clean", 1: "stall", 2: "max_iterations", 3: "k_cap_ov
               -1: "invalid_schedule"}
 
 EXPORTS = ("fpssft_run_batch", "fpssft_run_batch_grouped", "fpssft_run_batch_staged",
-           "fpssft_stage_bytes", "fpssft_line_spectra", "fpssft_gather_lines", "fpssft_dft_forward",
+           "fpssft_stage_bytes", "fpssft_stage_lines", "fpssft_line_spectra", "fpssft_gather_lines", "fpssft_dft_forward",
            "fpssft_synthesize", "fpssft_recover_large", "fpssft_recover_large_workspace",
            "fpssft_decode_spectra", "fpssft_project_onto_bins", "fpssft_smem_bytes",
            "fpssft_block_threads", "fpssft_plan", "fpssft_plan_batch", "fpssft_launches_per_batch",
@@ -73,7 +73,9 @@ def lib() -> C.CDLL:
                                                C.POINTER(Params), P, P, I32, C.POINTER(Out), P]
         h.fpssft_run_batch_staged.argtypes = [P, I64, I32, I64, C.POINTER(Shape),
                                               C.POINTER(Params), P, C.POINTER(Out), P, I64, I32,
-                                              P]
+                                              I32, P]
+        h.fpssft_stage_lines.argtypes = [P, I64, I32, I64, C.POINTER(Shape), C.POINTER(Params),
+                                         P, P, I64, I32, P]
         h.fpssft_stage_bytes.argtypes = [C.POINTER(Shape), I32, I64, I32]
         h.fpssft_stage_bytes.restype = I64
         h.fpssft_line_spectra.argtypes = [P, I64, I64, C.POINTER(Shape), P, I32, P, I32, P]

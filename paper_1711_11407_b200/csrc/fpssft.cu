@@ -2907,58 +2907,97 @@ int64_t fpssft_stage_bytes(const fpssft_shape *shape, int32_t group, int64_t bat
     return groups * stage_iterations * (int64_t)g.nlines * g.L * group * 8;
 }
 
-int fpssft_run_batch_staged(const void *cubes, int64_t batch, int32_t group,
-                            int64_t group_stride, const fpssft_shape *shape,
-                            const fpssft_params *params, const int32_t *schedule,
-                            const fpssft_out *out, void *staging, int64_t staging_bytes,
-                            int32_t stage_iterations, void *stream) {
-    Geo g;
-    Knobs kn;
+namespace {
+// Argument checks shared by fpssft_stage_lines and fpssft_run_batch_staged;
+// *t0 = the iterations really staged.
+int staged_args(const void *cubes, int64_t batch, int32_t group, int64_t group_stride,
+                const fpssft_shape *shape, const fpssft_params *params, const int32_t *schedule,
+                const void *staging, int64_t staging_bytes, int32_t stage_iterations, Geo *g,
+                Knobs *kn, int *t0) {
     int rc;
-    if ((rc = make_geo(shape, &g)) != FPSSFT_OK) return rc;
-    if ((rc = make_knobs(params, &kn)) != FPSSFT_OK) return rc;
+    if ((rc = make_geo(shape, g)) != FPSSFT_OK) return rc;
+    if ((rc = make_knobs(params, kn)) != FPSSFT_OK) return rc;
     if (group < 2 || group > 64 || (group & 1))
         return fail(FPSSFT_EINVAL, "staged lines: group must be even, in [2, 64]");
     if (stage_iterations < 1) return fail(FPSSFT_EINVAL, "stage_iterations must be >= 1");
     if (params->precision != FPSSFT_F32 ||
-        !group_kernel_for(g, FPSSFT_F32, group, params->k_cap, nullptr, true))
+        !group_kernel_for(*g, FPSSFT_F32, group, params->k_cap, nullptr, true))
         return fail(FPSSFT_EUNSUPPORTED,
                     "staged lines need the group-gather kernel (float32, a shape it is built "
                     "for, group a multiple of its width)");
     if (batch < 0 || batch > INT_MAX) return fail(FPSSFT_EINVAL, "bad batch");
+    *t0 = std::min<int>(stage_iterations, kn->t_max);
     if (batch == 0) return FPSSFT_OK;
-    const int T0 = std::min<int>(stage_iterations, kn.t_max);
-    const int64_t need = fpssft_stage_bytes(shape, group, batch, T0);
     if (!cubes || !schedule || !staging) return fail(FPSSFT_EINVAL, "NULL buffer");
-    if (staging_bytes < need)
+    if (staging_bytes < fpssft_stage_bytes(shape, group, batch, *t0))
         return fail(FPSSFT_EINVAL, "staging buffer smaller than fpssft_stage_bytes()");
-    for (int k = 0; k < g.D; ++k)
+    for (int k = 0; k < g->D; ++k)
         if (shape->strides[k] % group)
             return fail(FPSSFT_EINVAL, "staged lines: strides must be multiples of group");
     if (((uintptr_t)cubes | (uintptr_t)staging) & 15 || (group_stride * 8) % 16)
         return fail(FPSSFT_EINVAL, "staged lines: 16-byte aligned cubes and staging buffer");
+    if ((batch + group - 1) / group > 65535 || *t0 > 65535)
+        return fail(FPSSFT_EINVAL, "staged lines: too many groups");
+    return FPSSFT_OK;
+}
+
+int launch_stage(const void *cubes, int64_t batch, int32_t group, int64_t group_stride,
+                 const Geo &g, const int32_t *schedule, void *staging, int t0, cudaStream_t st) {
     const int64_t groups = (batch + group - 1) / group;
-    if (groups > 65535 || T0 > 65535) return fail(FPSSFT_EINVAL, "staged lines: too many groups");
-    cudaStream_t st = (cudaStream_t)stream;
     const int NLL = g.nlines * g.L;
-    const size_t smem = (size_t)stage::POS * 8 * group;
+    // one CTA per SM (a second one does not fit beside it): 256 bulk copies in
+    // flight per SM keep the host link full, and a recovery CTA of another
+    // stream still finds room (pipelined chunks, hostpath.py)
+    const size_t smem = std::max<size_t>((size_t)stage::POS * 8 * group, 120 * 1024);
     cudaError_t e = cudaFuncSetAttribute(stage::stage_lines_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stage_lines_kernel)");
-    const long long sgs = (long long)T0 * NLL * group;
-    dim3 grid((unsigned)((NLL + stage::POS - 1) / stage::POS), (unsigned)T0, (unsigned)groups);
+    dim3 grid((unsigned)((NLL + stage::POS - 1) / stage::POS), (unsigned)t0, (unsigned)groups);
     stage::stage_lines_kernel<<<grid, stage::POS, smem, st>>>(
-        (const float2 *)cubes, (long long)group_stride, g, group, schedule, T0,
-        (float2 *)staging, sgs);
-    if ((rc = check_launch("stage_lines_kernel")) != FPSSFT_OK) return rc;
-    kn.group = group;
-    kn.staged = (const float2 *)staging;
-    kn.staged_group_stride = sgs;
-    kn.stage_T = T0;
-    set_noise_floor(&kn, g, FPSSFT_F32);
+        (const float2 *)cubes, (long long)group_stride, g, group, schedule, t0,
+        (float2 *)staging, (long long)t0 * NLL * group);
+    return check_launch("stage_lines_kernel");
+}
+}  // namespace
+
+int fpssft_stage_lines(const void *cubes, int64_t batch, int32_t group, int64_t group_stride,
+                       const fpssft_shape *shape, const fpssft_params *params,
+                       const int32_t *schedule, void *staging, int64_t staging_bytes,
+                       int32_t stage_iterations, void *stream) {
+    Geo g;
+    Knobs kn;
+    int t0 = 0;
+    int rc = staged_args(cubes, batch, group, group_stride, shape, params, schedule, staging,
+                         staging_bytes, stage_iterations, &g, &kn, &t0);
+    if (rc != FPSSFT_OK || batch == 0) return rc;
+    return launch_stage(cubes, batch, group, group_stride, g, schedule, staging, t0,
+                        (cudaStream_t)stream);
+}
+
+int fpssft_run_batch_staged(const void *cubes, int64_t batch, int32_t group,
+                            int64_t group_stride, const fpssft_shape *shape,
+                            const fpssft_params *params, const int32_t *schedule,
+                            const fpssft_out *out, void *staging, int64_t staging_bytes,
+                            int32_t stage_iterations, int32_t already_staged, void *stream) {
+    Geo g;
+    Knobs kn;
+    int t0 = 0;
+    int rc = staged_args(cubes, batch, group, group_stride, shape, params, schedule, staging,
+                         staging_bytes, stage_iterations, &g, &kn, &t0);
+    if (rc != FPSSFT_OK || batch == 0) return rc;
     if (!out || !out->freqs || !out->amps || !out->count || !out->iterations ||
         !out->samples_used || !out->terminated_by)
         return fail(FPSSFT_EINVAL, "NULL buffer");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!already_staged &&
+        (rc = launch_stage(cubes, batch, group, group_stride, g, schedule, staging, t0, st)) !=
+            FPSSFT_OK)
+        return rc;
+    kn.group = group;
+    kn.staged = (const float2 *)staging;
+    kn.staged_group_stride = (long long)t0 * g.nlines * g.L * group;
+    kn.stage_T = t0;
+    set_noise_floor(&kn, g, FPSSFT_F32);
     OutPtrs o{out->freqs, out->amps, out->count, out->iterations,
               (long long *)out->samples_used, out->terminated_by, out->iter_stats};
     return run_batch_t<float>(cubes, batch, group_stride, g, kn, params->mode, schedule, nullptr,

@@ -335,7 +335,7 @@ class BatchRunner:
                 raise ValueError("staged lines: unsupported shape / group")
             self._staging = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=self.device)
 
-    def run(self, cubes) -> BatchResult:
+    def _check_cubes(self, cubes):
         import torch
 
         if not isinstance(cubes, torch.Tensor):
@@ -358,7 +358,28 @@ class BatchRunner:
                                  f"got {tuple(cubes.shape)}")
             strides = [int(s) for s in cubes.stride()[1:-1]]
         # element strides (complex64 units) of one cube and between cubes (groups)
-        sh = N.make_shape(self.shape.dims, strides)
+        return N.make_shape(self.shape.dims, strides)
+
+    def stage(self, cubes) -> None:
+        """The staging pass alone (``stage_iterations`` > 0), on the current
+        stream; ``run(cubes, staged=True)`` then skips it."""
+        if self._staging is None:
+            raise ValueError("this runner was built without stage_iterations")
+        sh = self._check_cubes(cubes)
+        dev = cubes.device if cubes.is_cuda else self.device
+        import torch
+
+        with torch.cuda.device(dev):
+            N.check(N.lib().fpssft_stage_lines(
+                N.ptr(cubes), self.batch, self.group, int(cubes.stride(0)), C_ref(sh),
+                C_ref(self._params_c), N.ptr(self.schedule), N.ptr(self._staging),
+                int(self._staging.numel()), self.stage_iterations, N.stream_ptr(dev)))
+
+    def run(self, cubes, staged: bool = False) -> BatchResult:
+        import torch
+
+        sh = self._check_cubes(cubes)
+        G = self.group
         # a pinned host tensor is read in place by the kernel (zero copy over the
         # host link: only the gathered samples cross it, the sub-linear sample
         # budget of the algorithm); its UVA address is valid on the device
@@ -369,7 +390,7 @@ class BatchRunner:
                     N.ptr(cubes), self.batch, G, int(cubes.stride(0)), C_ref(sh),
                     C_ref(self._params_c), N.ptr(self.schedule), C_ref(self._out_c),
                     N.ptr(self._staging), int(self._staging.numel()), self.stage_iterations,
-                    N.stream_ptr(dev)))
+                    int(bool(staged)), N.stream_ptr(dev)))
             else:
                 N.check(N.lib().fpssft_run_batch_grouped(
                     N.ptr(cubes), self.batch, G, int(cubes.stride(0)), C_ref(sh),

@@ -71,7 +71,8 @@ class HostBatchRunner:
                  k_cap: int = 256, precision: str = "auto", device=None, mode: str = "auto",
                  zero_copy_fraction: float | None = None, chunk: int | None = None,
                  chunk_bytes: int = 256 << 20, schedule=None, sched_index=None,
-                 graphs: bool = True, group: int = 1, stage_iterations: int = 0):
+                 graphs: bool = True, group: int = 1, stage_iterations: int = 0,
+                 pipeline: int = 1):
         import torch
 
         if mode not in ("auto", "copy", "zero_copy", "split"):
@@ -89,6 +90,13 @@ class HostBatchRunner:
         self.stage_iterations = int(stage_iterations)
         if self.stage_iterations and self.group < 2:
             raise ValueError("staged lines need an interleaved host batch (group >= 2)")
+        # pipeline > 1 (staged lines): the batch goes in that many chunks, chunk
+        # i+1 staged over the host link while chunk i recovers and its results
+        # return (two streams, the recovery one at high priority)
+        self.pipeline = max(1, int(pipeline))
+        if self.pipeline > 1 and (not self.stage_iterations
+                                  or int(batch) % (self.group * self.pipeline)):
+            raise ValueError("pipeline needs staged lines and a batch of whole groups per chunk")
         if self.group > 1:
             if mode not in ("auto", "zero_copy"):
                 raise ValueError("an interleaved host batch is gathered in place (zero_copy)")
@@ -116,6 +124,7 @@ class HostBatchRunner:
         self._bufs: list = []
         self._img_bufs: list = []
         self._streams = None
+        self._pipe_streams = None
 
     # ------------------------------------------------------------------ plan
     def split_count(self) -> int:
@@ -178,7 +187,41 @@ class HostBatchRunner:
             self._img_bufs.append(torch.empty((self.chunk, *self.shape.dims),
                                               dtype=torch.complex64, device=self.device))
 
-    def _graph_for(self, host_cubes, runner: BatchRunner):
+    def _launch_in_place(self, host_cubes):
+        """Everything of an in-place / staged run, enqueued behind the current
+        stream: one launch (pair) and the result copy, or the staged chunks
+        pipelined over two streams."""
+        import torch
+
+        if self.pipeline == 1:
+            r = self._runner(0, self.batch)
+            r.run(host_cubes)
+            self._copy_out(r, 0, self.batch)
+            return
+        if self._pipe_streams is None:
+            self._pipe_streams = (torch.cuda.Stream(self.device),
+                                  torch.cuda.Stream(self.device, priority=-1))
+        s_stage, s_run = self._pipe_streams
+        cur = torch.cuda.current_stream(self.device)
+        s_stage.wait_stream(cur)
+        s_run.wait_stream(cur)
+        n, G = self.batch // self.pipeline, self.group
+        for i in range(self.pipeline):
+            b0 = i * n
+            r = self._runner(b0, n)
+            hc = host_cubes[b0 // G:(b0 + n) // G]
+            with torch.cuda.stream(s_stage):
+                r.stage(hc)
+                ev = torch.cuda.Event()
+                ev.record(s_stage)
+            with torch.cuda.stream(s_run):
+                s_run.wait_event(ev)
+                r.run(hc, staged=True)
+                self._copy_out(r, b0, n)
+        cur.wait_stream(s_stage)
+        cur.wait_stream(s_run)
+
+    def _graph_for(self, host_cubes):
         """CUDA graph of (zero-copy recovery + result copy) for this host
         buffer: the launch sequence of a small batch costs more on the host
         than on the device (config 1: one instance, 24 us of kernel).  None if
@@ -193,13 +236,11 @@ class HostBatchRunner:
             side = torch.cuda.Stream(self.device)
             side.wait_stream(torch.cuda.current_stream(self.device))
             with torch.cuda.stream(side):  # warm: plans and attributes set outside capture
-                runner.run(host_cubes)
-                self._copy_out(runner, 0, self.batch)
+                self._launch_in_place(host_cubes)
             side.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=side):
-                runner.run(host_cubes)
-                self._copy_out(runner, 0, self.batch)
+                self._launch_in_place(host_cubes)
         except RuntimeError:
             g = None
             torch.cuda.synchronize(self.device)
@@ -243,13 +284,11 @@ class HostBatchRunner:
         if bz == self.batch and not synth:
             # all gathered in place: one launch and the result copy, in stream order,
             # replayed from a CUDA graph once captured for this host buffer
-            rz = self._runner(0, bz)
-            g = self._graph_for(host_cubes, rz) if self.graphs else None
+            g = self._graph_for(host_cubes) if self.graphs else None
             if g is not None:
                 g.replay()
             else:
-                rz.run(host_cubes)
-                self._copy_out(rz, 0, bz)
+                self._launch_in_place(host_cubes)
             torch.cuda.current_stream(self.device).synchronize()
             if self.mode == "auto":
                 self.last_mean_samples = float(self.out["samples_used"].double().mean())

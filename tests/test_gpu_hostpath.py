@@ -181,12 +181,15 @@ def test_interleaved_host_batch_gathered_in_place(G):
         hr.run(torch.empty((B, *w.dims), dtype=torch.complex64, pin_memory=True))
 
 
-@pytest.mark.parametrize("G,T0,B", [(32, 3, 96), (32, 1, 70), (16, 2, 64), (8, 50, 40), (64, 3, 64)])
-def test_staged_lines_from_interleaved_host_batch(G, T0, B):
+@pytest.mark.parametrize("G,T0,B,pipe", [(32, 3, 96, 1), (32, 1, 70, 1), (16, 2, 64, 1),
+                                         (8, 50, 40, 1), (64, 3, 64, 1), (32, 4, 128, 2),
+                                         (16, 5, 128, 4)])
+def test_staged_lines_from_interleaved_host_batch(G, T0, B, pipe):
     """fpssft_run_batch_staged: the first T0 iterations' line samples staged
     through HBM by TMA bulk copies of whole 8 G-byte host segments, later
     iterations gathered in place -- outputs bit-identical to the batch-major
-    device run (partial last group, T0 beyond the iteration cap included)."""
+    device run (partial last group, T0 beyond the iteration cap, and chunks
+    pipelined over two streams included)."""
     import numpy as np
 
     w = W.CONFIGS[2]
@@ -200,7 +203,7 @@ def test_staged_lines_from_interleaved_host_batch(G, T0, B):
     il = P.interleave(cubes, G)
     host = torch.empty(il.shape, dtype=il.dtype, pin_memory=True)
     host.copy_(il)
-    hr = HostBatchRunner(shape, cfg, B, k_cap=128, group=G, stage_iterations=T0)
+    hr = HostBatchRunner(shape, cfg, B, k_cap=128, group=G, stage_iterations=T0, pipeline=pipe)
     for _ in range(2):  # second run: the captured graph
         out = hr.run(host)
         for k, v in out.items():

@@ -20,12 +20,15 @@ def timeit(hr, host, n=5):
         a.record(); o = hr.run(host); b.record(); b.synchronize(); ms.append(a.elapsed_time(b))
     ok = all(torch.equal(o[k], dev.out[k].cpu()) for k in o if o[k] is not None)
     return round(float(np.median(ms)), 3), ok
+import os
+PIPES = [int(x) for x in os.environ.get("PIPES", "1").split(",")]
 for G, T0s in ((16, (0,)), (32, (0, 3, 4, 5)), (64, (4,))):
     il = P.interleave(cubes, G); host = torch.empty(il.shape, dtype=il.dtype, pin_memory=True); host.copy_(il); del il
     for T0 in T0s:
-        hr = HostBatchRunner(shape, cfg, B, k_cap=128, group=G, stage_iterations=T0)
-        print(json.dumps({'group': G, 'stage_iterations': T0, 'ms': timeit(hr, host)}), flush=True)
-        del hr
+        for pipe in (PIPES if T0 else [1]):
+            hr = HostBatchRunner(shape, cfg, B, k_cap=128, group=G, stage_iterations=T0, pipeline=pipe)
+            print(json.dumps({'group': G, 'stage_iterations': T0, 'pipeline': pipe, 'ms': timeit(hr, host)}), flush=True)
+            del hr
     del host
 # kernel-level timing of one staged run (CUPTI through torch.profiler)
 from torch.profiler import profile, ProfilerActivity
