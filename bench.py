@@ -720,6 +720,8 @@ def gpu_rank(args):
         #     through HBM by TMA bulk copies (fpssft_run_batch_staged): the link's
         #     bulk rate instead of the SM loads' request rate
         sg, st0 = args.host_stage_group, args.host_stage_iterations
+        if st0 == 0:  # auto: the slowest instance's iterations in the device run (untimed)
+            st0 = int(runner.out["iterations"].max())
         if group > 1 and not synth and sg > 1 and st0 > 0 and B % sg == 0:
             try:
                 pipe = args.host_stage_pipeline if B % (sg * args.host_stage_pipeline) == 0 else 1
@@ -737,20 +739,24 @@ def gpu_rank(args):
                 nll = (shape.ndim + 1) * shape.line_len
                 its = o["iterations"].numpy().astype(np.int64)
                 t0 = min(st0, hr.t_max)
-                late = np.maximum(its.reshape(-1, 8).max(axis=1) - t0, 0).sum()
+                if shape.ndim == 2 and shape.line_len == 256:  # the group-gather kernel
+                    late_b = np.maximum(its.reshape(-1, 8).max(axis=1) - t0, 0).sum() * nll * 64
+                else:  # per-instance kernels: one 32-byte sector per late sample
+                    late_b = np.maximum(its - t0, 0).sum() * nll * 32
                 staged_b = (B // sg) * t0 * nll * 8 * sg
                 e2e_st = {"value": B_total * e_steps / (e_total / 1e3), "unit": UNIT,
-                          "h2d_bytes_per_step": int(staged_b + late * nll * 64),
+                          "h2d_bytes_per_step": int(staged_b + late_b),
                           "d2h_bytes_per_step": out_bytes(o), "ms_per_step": e_total / e_steps,
                           "path": f"interleaved [B/{sg}, *dims, {sg}] pinned host cubes: the line "
                                   f"samples of iterations 0..{t0 - 1} of all {B} instances staged "
                                   f"through HBM by one TMA bulk copy per {8 * sg}-byte segment "
-                                  f"(fpssft_run_batch_staged), later iterations gathered in place "
-                                  f"(64-byte reads per 8-instance team); {pipe} chunks pipelined "
+                                  f"(fpssft_run_batch_staged), later iterations gathered in place; "
+                                  f"{pipe} chunks pipelined "
                                   f"(chunk i+1 staged while chunk i recovers and its results "
                                   f"return); results to pinned host",
-                          "note": "h2d = staged segments x segment bytes + 64 B per position of "
-                                  "the teams' iterations past the staged ones",
+                          "note": "h2d = staged segments x segment bytes + the in-place reads of "
+                                  "iterations past the staged ones (64 B per position and "
+                                  "8-instance team, or 32 B per sample for per-instance kernels)",
                           "outputs_identical_to_device_run": bool(all(
                               torch.equal(o[k], runner.out[k].cpu()) for k in o
                               if o[k] is not None))}
@@ -855,8 +861,9 @@ def main():
                          "one TMA bulk copy each; 0 = off)")
     ap.add_argument("--host-stage-pipeline", type=int, default=4,
                     help="chunks of the staged e2e batch pipelined over two streams")
-    ap.add_argument("--host-stage-iterations", type=int, default=5,
-                    help="iterations whose line samples the staged e2e path copies up front")
+    ap.add_argument("--host-stage-iterations", type=int, default=0,
+                    help="iterations whose line samples the staged e2e path copies up front "
+                         "(0 = the slowest instance's count in the device run, found untimed)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-batch-major", action="store_true")
     ap.add_argument("--no-synth", action="store_true", help="config 5 without re-synthesis")

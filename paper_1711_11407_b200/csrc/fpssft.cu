@@ -116,6 +116,9 @@
 #ifndef FPSSFT_GROUP_MINB
 #define FPSSFT_GROUP_MINB 2  // group kernel: CTAs per SM its registers must allow (3: compact layout)
 #endif
+#ifndef FPSSFT_STAGE_WARP
+#define FPSSFT_STAGE_WARP 1  // per-instance warp kernels read staged lines (0: A/B)
+#endif
 #ifndef FPSSFT_GROUP_LATE
 #define FPSSFT_GROUP_LATE 1  // group kernel: finished warps gather after the barrier (0: A/B)
 #endif
@@ -769,6 +772,13 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
 
     for (int h = lane; h < H; h += 32) hash[h] = HASH_EMPTY;
     __syncwarp();
+    // staged lines (fpssft_stage.cuh): this instance's (WG: the team's first
+    // member's) sample 0 of iteration 0 in staged[group][t][line][l][group]
+    const int sinst = (int)(WG ? inst0 : inst);
+    [[maybe_unused]] const float2 *sbase =
+        kn.staged != nullptr ? kn.staged + (long long)(sinst / kn.group) * kn.staged_group_stride +
+                                   (sinst % kn.group)
+                             : nullptr;
 
     int n_slots = 0, stall = 0, it_run = 0;
     int term = sched_ok ? FPSSFT_TERM_MAX_ITERATIONS : -1;
@@ -809,10 +819,8 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
             PCLK(0);
             GroupGather<LC, DC, WG> gg;
             auto group_load = [&]() {
-                if (kn.staged != nullptr && it < kn.stage_T)
-                    gg.load_staged(kn.staged + (inst0 / kn.group) * kn.staged_group_stride +
-                                       (inst0 % kn.group),
-                                   it, kn.group, team_tid);
+                if (sbase != nullptr && it < kn.stage_T)
+                    gg.load_staged(sbase, it, kn.group, team_tid);
                 else
                     gg.load(gbase, g, al, ta, team_tid);
             };
@@ -895,6 +903,14 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
             // the group gather above filled the spectra
         } else if constexpr (sizeof(R) == 4) {
             bool reg_gather = false, pf_used = false;
+            // staged lines (fpssft_stage.cuh): this iteration's samples sit in
+            // line order in HBM, kn.group instances per position
+            const bool from_hbm = FPSSFT_STAGE_WARP && !PFS && sbase != nullptr && it < kn.stage_T;
+            if (from_hbm) {
+                const float2 *sb = sbase + (long long)it * (nl * L) * kn.group;
+                for (int q = lane; q < nl * L; q += 32)
+                    cp_async8((cpx<float> *)spec + padi<PAD>(q), sb + (long long)q * kn.group);
+            }
             if constexpr (PFS) {
                 if (pf_ok) {  // prefetched during the previous iteration
                     cpx<R> *t = spec;
@@ -907,15 +923,15 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
             // for L >= 256 (config 2: 1% faster) -- measured, profiles/README.md
             if constexpr (FPSSFT_GATHER_NC && LC != 0 && LC < 256 && DC != 0 &&
                           !stage16_ok(DC, LC, 8, 32)) {
-                reg_gather = g.off32 && !pf_used;
+                reg_gather = g.off32 && !pf_used && !from_hbm;
                 if (reg_gather) gather_lines_nc<LC, DC>(spec, cube, g, al, ta, lane);
             }
             if constexpr (LC != 0 && stage16_ok(DC, LC, 8, 32)) {
-                staged = g.off32 && !reg_gather && !pf_used;
+                staged = g.off32 && !reg_gather && !pf_used && !from_hbm;
                 if (staged)
                     par = gather_lines_cg16<LC, DC>((float4 *)spec, cube, g, al, ta, lane, &dup);
             }
-            if (!reg_gather && !staged && !pf_used)
+            if (!reg_gather && !staged && !pf_used && !from_hbm)
                 gather_lines_async<LC>(spec, cube, g, al, ta, lane, 32);
             if (it + 1 < kn.t_max) {
 #pragma unroll
@@ -928,6 +944,7 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
                 // on config 2 (~3 iterations) the extra random DRAM fetches of
                 // a last-iteration prefetch cost more than the latency saved
                 if (!PFS && LC != 0 && it >= FPSSFT_PREFETCH_FROM && g.off32 &&
+                    !(FPSSFT_STAGE_WARP && sbase != nullptr && it + 1 < kn.stage_T) &&
                     line_params_ok(g, nal, nta))
                     prefetch_lines_l2<LC>(cube, g, nal, nta, lane);
             }
@@ -2920,11 +2937,21 @@ int staged_args(const void *cubes, int64_t batch, int32_t group, int64_t group_s
     if (group < 2 || group > 64 || (group & 1))
         return fail(FPSSFT_EINVAL, "staged lines: group must be even, in [2, 64]");
     if (stage_iterations < 1) return fail(FPSSFT_EINVAL, "stage_iterations must be >= 1");
-    if (params->precision != FPSSFT_F32 ||
-        !group_kernel_for(*g, FPSSFT_F32, group, params->k_cap, nullptr, true))
-        return fail(FPSSFT_EUNSUPPORTED,
-                    "staged lines need the group-gather kernel (float32, a shape it is built "
-                    "for, group a multiple of its width)");
+    {   // the warp-per-instance kernels read staged lines (the group-gather
+        // one for the team, the others per instance), in float32 / guarded
+        const int prec = effective_precision(*g, *kn, params->precision, params->mode);
+        Geo gp = *g;
+        LaunchPlan lp;
+        Knobs ks = *kn;
+        ks.group = group;
+        ks.staged = (const float2 *)staging;
+        if (prec == FPSSFT_F64 || !g->off32 ||
+            make_plan(gp, ks, prec, params->mode, &lp, true) != FPSSFT_OK ||
+            lp.mode != FPSSFT_MODE_WARP)
+            return fail(FPSSFT_EUNSUPPORTED,
+                        "staged lines need a warp-per-instance kernel in float32 or guarded "
+                        "float32 (short lines, 32-bit offsets)");
+    }
     if (batch < 0 || batch > INT_MAX) return fail(FPSSFT_EINVAL, "bad batch");
     *t0 = std::min<int>(stage_iterations, kn->t_max);
     if (batch == 0) return FPSSFT_OK;
@@ -2997,7 +3024,7 @@ int fpssft_run_batch_staged(const void *cubes, int64_t batch, int32_t group,
     kn.staged = (const float2 *)staging;
     kn.staged_group_stride = (long long)t0 * g.nlines * g.L * group;
     kn.stage_T = t0;
-    set_noise_floor(&kn, g, FPSSFT_F32);
+    set_noise_floor(&kn, g, effective_precision(g, kn, params->precision, params->mode));
     OutPtrs o{out->freqs, out->amps, out->count, out->iterations,
               (long long *)out->samples_used, out->terminated_by, out->iter_stats};
     return run_batch_t<float>(cubes, batch, group_stride, g, kn, params->mode, schedule, nullptr,

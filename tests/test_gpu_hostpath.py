@@ -217,6 +217,36 @@ def test_staged_lines_from_interleaved_host_batch(G, T0, B, pipe):
             assert torch.equal(v, dev.out[k]), k
 
 
+@pytest.mark.parametrize("cfg_id,B,G,T0,k_cap,dims", [(3, 20, 32, 400, 512, None),
+                                                      (3, 9, 8, 30, 512, None),
+                                                      (1, 6, 4, 2, 64, (32, 64))])
+def test_staged_lines_per_instance_kernels(cfg_id, B, G, T0, k_cap, dims):
+    """Staged lines read by the per-instance warp kernels (guarded float32 on
+    the noisy 64^3 shape, tens of iterations; the runtime-shape kernel on a
+    generic power-of-two shape): bit-identical to the batch-major device run."""
+    import dataclasses
+
+    w = W.CONFIGS[cfg_id]
+    if dims is not None:
+        w = dataclasses.replace(w, dims=dims, k=8)
+    spectra = W.make_spectra(w, B, 0)
+    cubes = W.synthesize_batch_torch(w.dims, spectra, DEV, w.noise_var, noise_seed=w.seed)
+    cfg = P.FpsSftConfig(seed=cfg_id, **P.PROFILES[w.profile])
+    shape = P.CubeShape(w.dims)
+    dev = P.BatchRunner(shape, cfg, B, k_cap=k_cap)
+    dev.run(cubes)
+    assert dev.plan["mode"] == "warp"
+    il = P.interleave(cubes, G)
+    host = torch.empty(il.shape, dtype=il.dtype, pin_memory=True)
+    host.copy_(il)
+    hr = HostBatchRunner(shape, cfg, B, k_cap=k_cap, group=G, stage_iterations=T0)
+    for _ in range(2):
+        out = hr.run(host)
+        for k, v in out.items():
+            if v is not None:
+                assert torch.equal(v, dev.out[k].cpu()), k
+
+
 def test_staged_lines_argument_errors():
     w = W.CONFIGS[2]
     shape = P.CubeShape(w.dims)
@@ -226,7 +256,11 @@ def test_staged_lines_argument_errors():
     with pytest.raises(ValueError):
         P.BatchRunner(shape, cfg, 8, k_cap=128, group=8, stage_iterations=3,
                       sched_index=[0] * 8)
-    with pytest.raises(ValueError):  # no group kernel for this shape
-        r = P.BatchRunner(P.CubeShape((64, 64, 64)), cfg, 8, k_cap=128, group=8,
+    with pytest.raises(ValueError):  # one CTA per instance: no staged read path
+        r = P.BatchRunner(P.CubeShape((1024, 2048)), cfg, 8, k_cap=2048, group=8,
                           stage_iterations=3)
-        r.run(torch.zeros((1, 64, 64, 64, 8), dtype=torch.complex64, device=DEV))
+        r.run(torch.zeros((1, 1024, 2048, 8), dtype=torch.complex64, device=DEV))
+    with pytest.raises(ValueError):  # float64
+        r = P.BatchRunner(shape, cfg, 8, k_cap=128, group=8, stage_iterations=3,
+                          precision="fp64")
+        r.run(torch.zeros((1, 256, 256, 8), dtype=torch.complex64, device=DEV))
