@@ -116,6 +116,9 @@
 #ifndef FPSSFT_GROUP_MINB
 #define FPSSFT_GROUP_MINB 2  // group kernel: CTAs per SM its registers must allow (3: compact layout)
 #endif
+#ifndef FPSSFT_STAGE_TEAM
+#define FPSSFT_STAGE_TEAM 1  // compile-time team kernels read staged lines (0: A/B)
+#endif
 #ifndef FPSSFT_STAGE_WARP
 #define FPSSFT_STAGE_WARP 1  // per-instance warp kernels read staged lines (0: A/B)
 #endif
@@ -2947,10 +2950,10 @@ int staged_args(const void *cubes, int64_t batch, int32_t group, int64_t group_s
         ks.staged = (const float2 *)staging;
         if (prec == FPSSFT_F64 || !g->off32 ||
             make_plan(gp, ks, prec, params->mode, &lp, true) != FPSSFT_OK ||
-            lp.mode != FPSSFT_MODE_WARP)
+            !(lp.mode == FPSSFT_MODE_WARP || (lp.mode == FPSSFT_MODE_CTA && lp.kernel)))
             return fail(FPSSFT_EUNSUPPORTED,
-                        "staged lines need a warp-per-instance kernel in float32 or guarded "
-                        "float32 (short lines, 32-bit offsets)");
+                        "staged lines need a warp-per-instance or compile-time team kernel in "
+                        "float32 or guarded float32 (32-bit offsets)");
     }
     if (batch < 0 || batch > INT_MAX) return fail(FPSSFT_EINVAL, "bad batch");
     *t0 = std::min<int>(stage_iterations, kn->t_max);

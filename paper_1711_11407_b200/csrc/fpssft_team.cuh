@@ -123,6 +123,11 @@ __global__ void __launch_bounds__(NT, GUARD ? (FPSSFT_TEAM_GUARD_THREADS / NT > 
     for (int h = tid; h < H; h += NT) hash[h] = U16_NONE;
     __syncthreads();
 
+    [[maybe_unused]] const float2 *sbase =
+        kn.staged != nullptr
+            ? kn.staged + (long long)((int)inst / kn.group) * kn.staged_group_stride +
+                  ((int)inst % kn.group)
+            : nullptr;
     int n_slots = 0, stall = 0, it_run = 0;
     int term = sched_ok ? FPSSFT_TERM_MAX_ITERATIONS : -1;
     A amp_sum = (A)0;
@@ -153,7 +158,14 @@ __global__ void __launch_bounds__(NT, GUARD ? (FPSSFT_TEAM_GUARD_THREADS / NT > 
         unsigned par = 0, dup = 0;
         if constexpr (sizeof(R) == 4) {
             bool reg_gather = false;
-            if constexpr (stage16_ok(DC, LC, 8, NT)) {
+            // staged lines (fpssft_stage.cuh): this iteration's samples sit in
+            // line order in HBM, kn.group instances per position
+            const bool from_hbm = FPSSFT_STAGE_TEAM && sbase != nullptr && it < kn.stage_T;
+            if (from_hbm) {
+                const float2 *sb = sbase + (long long)it * (nl * L) * kn.group;
+                for (int q = tid; q < nl * L; q += NT)
+                    cp_async8((cpx<float> *)spec + padi<PAD>(q), sb + (long long)q * kn.group);
+            } else if constexpr (stage16_ok(DC, LC, 8, NT)) {
                 staged = g.off32;
                 if (staged)
                     par = gather_lines_cg16<LC, DC, NT>((float4 *)spec, cube, g, al, ta, tid, &dup);
@@ -161,7 +173,8 @@ __global__ void __launch_bounds__(NT, GUARD ? (FPSSFT_TEAM_GUARD_THREADS / NT > 
                 reg_gather = g.off32;
                 if (reg_gather) gather_lines_nc<LC, DC, NT>(spec, cube, g, al, ta, tid);
             }
-            if (!reg_gather && !staged) gather_lines_async<LC, NT>(spec, cube, g, al, ta, tid, NT);
+            if (!reg_gather && !staged && !from_hbm)
+                gather_lines_async<LC, NT>(spec, cube, g, al, ta, tid, NT);
         } else {
             gather_lines<R, PAD>(spec, cube, g, al, ta, tid, NT);
         }

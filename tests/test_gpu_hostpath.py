@@ -219,11 +219,14 @@ def test_staged_lines_from_interleaved_host_batch(G, T0, B, pipe):
 
 @pytest.mark.parametrize("cfg_id,B,G,T0,k_cap,dims", [(3, 20, 32, 400, 512, None),
                                                       (3, 9, 8, 30, 512, None),
-                                                      (1, 6, 4, 2, 64, (32, 64))])
+                                                      (1, 6, 4, 2, 64, (32, 64)),
+                                                      (4, 6, 4, 3, 2048, None),
+                                                      (5, 10, 8, 60, 512, None)])
 def test_staged_lines_per_instance_kernels(cfg_id, B, G, T0, k_cap, dims):
-    """Staged lines read by the per-instance warp kernels (guarded float32 on
-    the noisy 64^3 shape, tens of iterations; the runtime-shape kernel on a
-    generic power-of-two shape): bit-identical to the batch-major device run."""
+    """Staged lines read by the per-instance kernels (guarded float32 on the
+    noisy 64^3 shape, tens of iterations; the runtime-shape warp kernel on a
+    generic power-of-two shape; the team kernels of configs 4 and 5):
+    bit-identical to the batch-major device run."""
     import dataclasses
 
     w = W.CONFIGS[cfg_id]
@@ -235,7 +238,7 @@ def test_staged_lines_per_instance_kernels(cfg_id, B, G, T0, k_cap, dims):
     shape = P.CubeShape(w.dims)
     dev = P.BatchRunner(shape, cfg, B, k_cap=k_cap)
     dev.run(cubes)
-    assert dev.plan["mode"] == "warp"
+    assert dev.plan["mode"] == ("cta" if cfg_id in (4, 5) else "warp")
     il = P.interleave(cubes, G)
     host = torch.empty(il.shape, dtype=il.dtype, pin_memory=True)
     host.copy_(il)
@@ -256,10 +259,10 @@ def test_staged_lines_argument_errors():
     with pytest.raises(ValueError):
         P.BatchRunner(shape, cfg, 8, k_cap=128, group=8, stage_iterations=3,
                       sched_index=[0] * 8)
-    with pytest.raises(ValueError):  # one CTA per instance: no staged read path
-        r = P.BatchRunner(P.CubeShape((1024, 2048)), cfg, 8, k_cap=2048, group=8,
+    with pytest.raises(ValueError):  # the runtime-shape CTA kernel has no staged read path
+        r = P.BatchRunner(P.CubeShape((12, 18)), cfg, 8, k_cap=64, group=8,
                           stage_iterations=3)
-        r.run(torch.zeros((1, 1024, 2048, 8), dtype=torch.complex64, device=DEV))
+        r.run(torch.zeros((1, 12, 18, 8), dtype=torch.complex64, device=DEV))
     with pytest.raises(ValueError):  # float64
         r = P.BatchRunner(shape, cfg, 8, k_cap=128, group=8, stage_iterations=3,
                           precision="fp64")
