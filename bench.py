@@ -722,20 +722,25 @@ def gpu_rank(args):
         sg, st0 = args.host_stage_group, args.host_stage_iterations
         if st0 == 0:  # auto: the slowest instance's iterations in the device run (untimed)
             st0 = int(runner.out["iterations"].max())
-        if group > 1 and not synth and sg > 1 and st0 > 0 and B % sg == 0:
+        # (re-synthesis configs: the same host batches as (a), images back to the host)
+        hb_c, n_c = (hb, n_host) if synth else (B, 1)
+        if group > 1 and sg > 1 and st0 > 0 and hb_c % sg == 0:
             try:
-                pipe = args.host_stage_pipeline if B % (sg * args.host_stage_pipeline) == 0 else 1
-                hr = HostBatchRunner(shape, cfg, B, k_cap=k_cap, precision=args.precision,
+                pipe = (args.host_stage_pipeline
+                        if not synth and hb_c % (sg * args.host_stage_pipeline) == 0 else 1)
+                hr = HostBatchRunner(shape, cfg, hb_c, k_cap=k_cap, precision=args.precision,
                                      device=dev, group=sg, stage_iterations=st0, pipeline=pipe)
-                host_il = P.interleave(cubes, sg)
+                host_il = P.interleave(cubes[:hb_c], sg)
                 host = torch.empty(host_il.shape, dtype=host_il.dtype, pin_memory=True)
                 host.copy_(host_il)
                 del host_il
-                hr.run(host)
-            except ValueError:  # no group-gather kernel for this shape / precision
+                himg = (torch.empty((hb_c, *shape.dims), dtype=torch.complex64, pin_memory=True)
+                        if synth else None)
+                hr.run(host, himg)
+            except ValueError:  # no staged read path for this shape / precision
                 hr = None
             if hr is not None:
-                o, e_total = time_host(hr, host, None, 1)
+                o, e_total = time_host(hr, host, himg, n_c)
                 nll = (shape.ndim + 1) * shape.line_len
                 its = o["iterations"].numpy().astype(np.int64)
                 t0 = min(st0, hr.t_max)
@@ -743,24 +748,29 @@ def gpu_rank(args):
                     late_b = np.maximum(its.reshape(-1, 8).max(axis=1) - t0, 0).sum() * nll * 64
                 else:  # per-instance kernels: one 32-byte sector per late sample
                     late_b = np.maximum(its - t0, 0).sum() * nll * 32
-                staged_b = (B // sg) * t0 * nll * 8 * sg
+                staged_b = (hb_c // sg) * t0 * nll * 8 * sg
+                img_b = himg.numel() * himg.element_size() if synth else 0
+                chunks = (f"{pipe} chunks pipelined (chunk i+1 staged while chunk i recovers and "
+                          f"its results return)" if not synth else
+                          f"{n_c} x {hb_c} instances per step in {hr.chunk}-instance chunks over "
+                          f"three streams (staging || recovery + re-synthesis || images back)")
                 e2e_st = {"value": B_total * e_steps / (e_total / 1e3), "unit": UNIT,
-                          "h2d_bytes_per_step": int(staged_b + late_b),
-                          "d2h_bytes_per_step": out_bytes(o), "ms_per_step": e_total / e_steps,
+                          "h2d_bytes_per_step": int(n_c * (staged_b + late_b)),
+                          "d2h_bytes_per_step": int(n_c * (out_bytes(o) + img_b)),
+                          "ms_per_step": e_total / e_steps,
                           "path": f"interleaved [B/{sg}, *dims, {sg}] pinned host cubes: the line "
-                                  f"samples of iterations 0..{t0 - 1} of all {B} instances staged "
-                                  f"through HBM by one TMA bulk copy per {8 * sg}-byte segment "
+                                  f"samples of iterations 0..{t0 - 1} staged through HBM by one "
+                                  f"TMA bulk copy per {8 * sg}-byte segment "
                                   f"(fpssft_run_batch_staged), later iterations gathered in place; "
-                                  f"{pipe} chunks pipelined "
-                                  f"(chunk i+1 staged while chunk i recovers and its results "
-                                  f"return); results to pinned host",
+                                  f"{chunks}; results{' and images' if synth else ''} to pinned "
+                                  f"host",
                           "note": "h2d = staged segments x segment bytes + the in-place reads of "
                                   "iterations past the staged ones (64 B per position and "
                                   "8-instance team, or 32 B per sample for per-instance kernels)",
                           "outputs_identical_to_device_run": bool(all(
-                              torch.equal(o[k], runner.out[k].cpu()) for k in o
+                              torch.equal(o[k], runner.out[k][:hb_c].cpu()) for k in o
                               if o[k] is not None))}
-                del host, hr
+                del host, hr, himg
                 if e2e_st["value"] > e2e["value"]:
                     prev = e2e
                     e2e = e2e_st

@@ -221,6 +221,61 @@ class HostBatchRunner:
         cur.wait_stream(s_stage)
         cur.wait_stream(s_run)
 
+    def _run_staged_synth(self, host_cubes, images) -> dict:
+        """Interleaved host batch, staged lines, images back to the host
+        (config 5): chunk by chunk over three streams -- the line samples of
+        chunk i+1 cross the link (TMA staging) while chunk i recovers and
+        re-synthesises and the images of chunk i-1 return.  Only the sampled
+        segments go up, so the link's downstream direction carries the images
+        at its full rate."""
+        import torch
+
+        from .ops import synthesize
+
+        G = self.group
+        n = max(G, self.chunk // G * G)
+        if self._streams is None:
+            self._streams = [torch.cuda.Stream(self.device) for _ in range(4)]
+        s_stage, s_run, s_d2h, _ = self._streams
+        while len(self._img_bufs) < 2:
+            self._img_bufs.append(torch.empty((min(n, self.batch), *self.shape.dims),
+                                              dtype=torch.complex64, device=self.device))
+        cur = torch.cuda.current_stream(self.device)
+        for s in (s_stage, s_run, s_d2h):
+            s.wait_stream(cur)
+        ev_free = [None, None]
+        for k, b0 in enumerate(range(0, self.batch, n)):
+            m = min(n, self.batch - b0)
+            i = k & 1
+            r = self._runner(b0, m)
+            hc = host_cubes[b0 // G:(b0 + m + G - 1) // G]
+            with torch.cuda.stream(s_stage):
+                r.stage(hc)
+                ev_st = torch.cuda.Event()
+                ev_st.record(s_stage)
+            with torch.cuda.stream(s_run):
+                s_run.wait_event(ev_st)
+                if ev_free[i] is not None:
+                    s_run.wait_event(ev_free[i])
+                res = r.run(hc, staged=True)
+                self._copy_out(r, b0, m)
+                img = self._img_bufs[i][:m]
+                synthesize(res, out=img)
+                ev_img = torch.cuda.Event()
+                ev_img.record(s_run)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev_img)
+                images[b0:b0 + m].copy_(img, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s_d2h)
+                ev_free[i] = ev
+        for s in (s_stage, s_run, s_d2h):
+            cur.wait_stream(s)
+        cur.synchronize()
+        if self.mode == "auto":
+            self.last_mean_samples = float(self.out["samples_used"].double().mean())
+        return self.out
+
     def _graph_for(self, host_cubes):
         """CUDA graph of (zero-copy recovery + result copy) for this host
         buffer: the launch sequence of a small batch costs more on the host
@@ -275,11 +330,15 @@ class HostBatchRunner:
         if not host_cubes.is_contiguous():
             raise ValueError("host_cubes must be contiguous")
         synth = images is not None
-        if synth and G > 1:
-            raise ValueError("re-synthesis needs a batch-major host batch")
+        if synth and G > 1 and not self.stage_iterations:
+            raise ValueError("re-synthesis from an interleaved host batch needs staged lines")
         if synth and not (not images.is_cuda and images.is_pinned()
-                          and images.shape == host_cubes.shape):
-            raise ValueError("images must be a pinned host tensor shaped like host_cubes")
+                          and tuple(images.shape) == (self.batch, *self.shape.dims)
+                          and images.dtype == torch.complex64 and images.is_contiguous()):
+            raise ValueError("images must be a contiguous pinned complex64 host tensor "
+                             "[batch, *dims]")
+        if synth and G > 1:
+            return self._run_staged_synth(host_cubes, images)
         bz = self.split_count()
         if bz == self.batch and not synth:
             # all gathered in place: one launch and the result copy, in stream order,

@@ -79,6 +79,32 @@ def test_cfg5_images_to_pinned_host():
         assert torch.equal(images, want), mode
 
 
+@pytest.mark.parametrize("G,B,chunk", [(8, 22, 8), (4, 6, 2), (32, 40, 32)])
+def test_cfg5_images_from_staged_interleaved_host_batch(G, B, chunk):
+    """Config 5 from an interleaved host batch: lines staged chunk by chunk,
+    recovery, re-synthesis, images and reports back in pinned host memory --
+    identical to the device run (partial last group and chunk included)."""
+    w, cubes, cfg = _cubes(5, B)
+    shape = P.CubeShape(w.dims)
+    r = P.BatchRunner(shape, cfg, B, k_cap=1024, device=DEV)
+    res = r.run(cubes)
+    want = ops.synthesize(res).cpu()
+    il = P.interleave(cubes, G)
+    host = torch.empty(il.shape, dtype=il.dtype, pin_memory=True)
+    host.copy_(il)
+    images = torch.zeros(cubes.shape, dtype=cubes.dtype, pin_memory=True)
+    hr = HostBatchRunner(shape, cfg, B, k_cap=1024, device=DEV, group=G, chunk=chunk,
+                         stage_iterations=int(r.out["iterations"].max()) - 3)
+    for _ in range(2):
+        out = hr.run(host, images)
+        assert torch.equal(images, want)
+        for k, v in out.items():
+            if v is not None:
+                assert torch.equal(v, r.out[k].cpu()), k
+    with pytest.raises(ValueError):  # no staged lines: interleaved re-synthesis refused
+        HostBatchRunner(shape, cfg, B, k_cap=1024, device=DEV, group=G).run(host, images)
+
+
 def test_tune_picks_a_measured_fraction():
     w, cubes, cfg = _cubes(2, 64)
     host = torch.empty(cubes.shape, dtype=cubes.dtype, pin_memory=True)
