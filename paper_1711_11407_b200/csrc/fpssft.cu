@@ -897,6 +897,12 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
             break;
         }
         it_run = it + 1;
+        // staged lines: this iteration's samples of this instance (else nullptr;
+        // the guarded kernel's rare exact re-evaluations still read the cube)
+        [[maybe_unused]] const float2 *sline =
+            (FPSSFT_STAGE_WARP && !PFS && !WG && sbase != nullptr && it < kn.stage_T)
+                ? sbase + (long long)it * (nl * L) * kn.group
+                : nullptr;
 
         // (1) gather + (2) DFT of the D+1 lines           driver.py:146-154
         R my_energy = (R)0;
@@ -908,11 +914,10 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
             bool reg_gather = false, pf_used = false;
             // staged lines (fpssft_stage.cuh): this iteration's samples sit in
             // line order in HBM, kn.group instances per position
-            const bool from_hbm = FPSSFT_STAGE_WARP && !PFS && sbase != nullptr && it < kn.stage_T;
+            const bool from_hbm = sline != nullptr;
             if (from_hbm) {
-                const float2 *sb = sbase + (long long)it * (nl * L) * kn.group;
                 for (int q = lane; q < nl * L; q += 32)
-                    cp_async8((cpx<float> *)spec + padi<PAD>(q), sb + (long long)q * kn.group);
+                    cp_async8((cpx<float> *)spec + padi<PAD>(q), sline + (long long)q * kn.group);
             }
             if constexpr (PFS) {
                 if (pf_ok) {  // prefetched during the previous iteration
@@ -2950,10 +2955,11 @@ int staged_args(const void *cubes, int64_t batch, int32_t group, int64_t group_s
         ks.staged = (const float2 *)staging;
         if (prec == FPSSFT_F64 || !g->off32 ||
             make_plan(gp, ks, prec, params->mode, &lp, true) != FPSSFT_OK ||
-            !(lp.mode == FPSSFT_MODE_WARP || (lp.mode == FPSSFT_MODE_CTA && lp.kernel)))
+            !(lp.mode == FPSSFT_MODE_WARP ||
+              (lp.mode == FPSSFT_MODE_CTA && lp.kernel && prec == FPSSFT_F32)))
             return fail(FPSSFT_EUNSUPPORTED,
-                        "staged lines need a warp-per-instance or compile-time team kernel in "
-                        "float32 or guarded float32 (32-bit offsets)");
+                        "staged lines need a warp-per-instance kernel (float32 or guarded) or a "
+                        "compile-time float32 team kernel, 32-bit offsets");
     }
     if (batch < 0 || batch > INT_MAX) return fail(FPSSFT_EINVAL, "bad batch");
     *t0 = std::min<int>(stage_iterations, kn->t_max);

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (FPSSFT_TEAM_GUARD_THREADS / NT > 
     __syncthreads();
 
     [[maybe_unused]] const float2 *sbase =
-        kn.staged != nullptr
+        (!GUARD && kn.staged != nullptr)
             ? kn.staged + (long long)((int)inst / kn.group) * kn.staged_group_stride +
                   ((int)inst % kn.group)
             : nullptr;
@@ -151,6 +151,11 @@ __global__ void __launch_bounds__(NT, GUARD ? (FPSSFT_TEAM_GUARD_THREADS / NT > 
             break;
         }
         it_run = it + 1;
+        // staged lines: this iteration's samples of this instance (else nullptr)
+        [[maybe_unused]] const float2 *sline =
+            (FPSSFT_STAGE_TEAM && sizeof(R) == 4 && !GUARD && sbase != nullptr && it < kn.stage_T)
+                ? sbase + (long long)it * (nl * L) * kn.group
+                : nullptr;
 
         PCLK(0);
         // (1) gather + (2) DFT                                 driver.py:146-154
@@ -160,11 +165,10 @@ __global__ void __launch_bounds__(NT, GUARD ? (FPSSFT_TEAM_GUARD_THREADS / NT > 
             bool reg_gather = false;
             // staged lines (fpssft_stage.cuh): this iteration's samples sit in
             // line order in HBM, kn.group instances per position
-            const bool from_hbm = FPSSFT_STAGE_TEAM && sbase != nullptr && it < kn.stage_T;
+            const bool from_hbm = sline != nullptr;
             if (from_hbm) {
-                const float2 *sb = sbase + (long long)it * (nl * L) * kn.group;
                 for (int q = tid; q < nl * L; q += NT)
-                    cp_async8((cpx<float> *)spec + padi<PAD>(q), sb + (long long)q * kn.group);
+                    cp_async8((cpx<float> *)spec + padi<PAD>(q), sline + (long long)q * kn.group);
             } else if constexpr (stage16_ok(DC, LC, 8, NT)) {
                 staged = g.off32;
                 if (staged)

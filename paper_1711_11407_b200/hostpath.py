@@ -234,9 +234,14 @@ class HostBatchRunner:
 
         G = self.group
         n = max(G, self.chunk // G * G)
+        if self._pipe_streams is None:
+            self._pipe_streams = (torch.cuda.Stream(self.device),
+                                  torch.cuda.Stream(self.device, priority=-1))
         if self._streams is None:
             self._streams = [torch.cuda.Stream(self.device) for _ in range(4)]
-        s_stage, s_run, s_d2h, _ = self._streams
+        # recovery at high priority: its CTAs are placed before the staging
+        # grid's pending ones
+        (s_stage, s_run), s_d2h = self._pipe_streams, self._streams[2]
         while len(self._img_bufs) < 2:
             self._img_bufs.append(torch.empty((min(n, self.batch), *self.shape.dims),
                                               dtype=torch.complex64, device=self.device))

@@ -86,7 +86,7 @@ def test_cfg5_images_from_staged_interleaved_host_batch(G, B, chunk):
     identical to the device run (partial last group and chunk included)."""
     w, cubes, cfg = _cubes(5, B)
     shape = P.CubeShape(w.dims)
-    r = P.BatchRunner(shape, cfg, B, k_cap=1024, device=DEV)
+    r = P.BatchRunner(shape, cfg, B, k_cap=1024, device=DEV, precision="fp32")
     res = r.run(cubes)
     want = ops.synthesize(res).cpu()
     il = P.interleave(cubes, G)
@@ -94,6 +94,7 @@ def test_cfg5_images_from_staged_interleaved_host_batch(G, B, chunk):
     host.copy_(il)
     images = torch.zeros(cubes.shape, dtype=cubes.dtype, pin_memory=True)
     hr = HostBatchRunner(shape, cfg, B, k_cap=1024, device=DEV, group=G, chunk=chunk,
+                         precision="fp32",
                          stage_iterations=int(r.out["iterations"].max()) - 3)
     for _ in range(2):
         out = hr.run(host, images)
@@ -103,6 +104,9 @@ def test_cfg5_images_from_staged_interleaved_host_batch(G, B, chunk):
                 assert torch.equal(v, r.out[k].cpu()), k
     with pytest.raises(ValueError):  # no staged lines: interleaved re-synthesis refused
         HostBatchRunner(shape, cfg, B, k_cap=1024, device=DEV, group=G).run(host, images)
+    with pytest.raises(ValueError):  # the guarded team kernel has no staged read path
+        HostBatchRunner(shape, cfg, B, k_cap=1024, device=DEV, group=G, chunk=chunk,
+                        stage_iterations=5).run(host, images)
 
 
 def test_tune_picks_a_measured_fraction():
@@ -247,7 +251,7 @@ def test_staged_lines_from_interleaved_host_batch(G, T0, B, pipe):
                                                       (3, 9, 8, 30, 512, None),
                                                       (1, 6, 4, 2, 64, (32, 64)),
                                                       (4, 6, 4, 3, 2048, None),
-                                                      (5, 10, 8, 60, 512, None)])
+                                                      (5, 10, 8, 60, 512, "fp32")])
 def test_staged_lines_per_instance_kernels(cfg_id, B, G, T0, k_cap, dims):
     """Staged lines read by the per-instance kernels (guarded float32 on the
     noisy 64^3 shape, tens of iterations; the runtime-shape warp kernel on a
@@ -256,19 +260,23 @@ def test_staged_lines_per_instance_kernels(cfg_id, B, G, T0, k_cap, dims):
     import dataclasses
 
     w = W.CONFIGS[cfg_id]
+    prec = "auto"
+    if dims == "fp32":  # config 5's team kernel, plain float32 (its guarded form has no staged reads)
+        dims, prec = None, "fp32"
     if dims is not None:
         w = dataclasses.replace(w, dims=dims, k=8)
     spectra = W.make_spectra(w, B, 0)
     cubes = W.synthesize_batch_torch(w.dims, spectra, DEV, w.noise_var, noise_seed=w.seed)
     cfg = P.FpsSftConfig(seed=cfg_id, **P.PROFILES[w.profile])
     shape = P.CubeShape(w.dims)
-    dev = P.BatchRunner(shape, cfg, B, k_cap=k_cap)
+    dev = P.BatchRunner(shape, cfg, B, k_cap=k_cap, precision=prec)
     dev.run(cubes)
     assert dev.plan["mode"] == ("cta" if cfg_id in (4, 5) else "warp")
     il = P.interleave(cubes, G)
     host = torch.empty(il.shape, dtype=il.dtype, pin_memory=True)
     host.copy_(il)
-    hr = HostBatchRunner(shape, cfg, B, k_cap=k_cap, group=G, stage_iterations=T0)
+    hr = HostBatchRunner(shape, cfg, B, k_cap=k_cap, group=G, stage_iterations=T0,
+                         precision=prec)
     for _ in range(2):
         out = hr.run(host)
         for k, v in out.items():
