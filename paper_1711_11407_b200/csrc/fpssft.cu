@@ -116,12 +116,6 @@
 #ifndef FPSSFT_GROUP_MINB
 #define FPSSFT_GROUP_MINB 2  // group kernel: CTAs per SM its registers must allow (3: compact layout)
 #endif
-#ifndef FPSSFT_STAGE_TEAM
-#define FPSSFT_STAGE_TEAM 1  // compile-time team kernels read staged lines (0: A/B)
-#endif
-#ifndef FPSSFT_STAGE_WARP
-#define FPSSFT_STAGE_WARP 1  // per-instance warp kernels read staged lines (0: A/B)
-#endif
 #ifndef FPSSFT_GROUP_LATE
 #define FPSSFT_GROUP_LATE 1  // group kernel: finished warps gather after the barrier (0: A/B)
 #endif
@@ -683,7 +677,9 @@ __device__ __forceinline__ bool team_bar_or(int id, int n, bool p) {
 // (fpssft_guard.cuh) -- float64 slot amplitudes and line-0 transform, guard
 // flags on every float32 decision statistic, flagged bins re-evaluated in
 // float64 by the whole warp.
-template <class R, int LC, int DC, bool GUARD = false, int WG = 0, int KC = 0>
+// STG: the instance that reads staged lines (fpssft_stage.cuh, Knobs::staged);
+// a separate instantiation, so the device-resident kernels carry none of it.
+template <class R, int LC, int DC, bool GUARD = false, int WG = 0, int KC = 0, bool STG = false>
 __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
                                   WG > 8 ? 1
                                          : (WG ? FPSSFT_GROUP_MINB
@@ -779,9 +775,10 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
     // member's) sample 0 of iteration 0 in staged[group][t][line][l][group]
     const int sinst = (int)(WG ? inst0 : inst);
     [[maybe_unused]] const float2 *sbase =
-        kn.staged != nullptr ? kn.staged + (long long)(sinst / kn.group) * kn.staged_group_stride +
-                                   (sinst % kn.group)
-                             : nullptr;
+        (STG && kn.staged != nullptr)
+            ? kn.staged + (long long)(sinst / kn.group) * kn.staged_group_stride +
+                  (sinst % kn.group)
+            : nullptr;
 
     int n_slots = 0, stall = 0, it_run = 0;
     int term = sched_ok ? FPSSFT_TERM_MAX_ITERATIONS : -1;
@@ -822,7 +819,7 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
             PCLK(0);
             GroupGather<LC, DC, WG> gg;
             auto group_load = [&]() {
-                if (sbase != nullptr && it < kn.stage_T)
+                if (STG && sbase != nullptr && it < kn.stage_T)
                     gg.load_staged(sbase, it, kn.group, team_tid);
                 else
                     gg.load(gbase, g, al, ta, team_tid);
@@ -900,7 +897,7 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
         // staged lines: this iteration's samples of this instance (else nullptr;
         // the guarded kernel's rare exact re-evaluations still read the cube)
         [[maybe_unused]] const float2 *sline =
-            (FPSSFT_STAGE_WARP && !PFS && !WG && sbase != nullptr && it < kn.stage_T)
+            (STG && !PFS && !WG && sbase != nullptr && it < kn.stage_T)
                 ? sbase + (long long)it * (nl * L) * kn.group
                 : nullptr;
 
@@ -952,7 +949,7 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
                 // on config 2 (~3 iterations) the extra random DRAM fetches of
                 // a last-iteration prefetch cost more than the latency saved
                 if (!PFS && LC != 0 && it >= FPSSFT_PREFETCH_FROM && g.off32 &&
-                    !(FPSSFT_STAGE_WARP && sbase != nullptr && it + 1 < kn.stage_T) &&
+                    !(STG && sbase != nullptr && it + 1 < kn.stage_T) &&
                     line_params_ok(g, nal, nta))
                     prefetch_lines_l2<LC>(cube, g, nal, nta, lane);
             }
@@ -2213,7 +2210,20 @@ const void *warp_kernel_for_t(const Geo &g, int k_cap) {
     if (g.off32 && g.D == 3 && g.L == 64) return (const void *)recover_warp_kernel<R, 64, 3>;
     return (const void *)recover_warp_kernel<R, 0, 0>;
 }
-const void *warp_kernel_for(const Geo &g, int precision, int k_cap) {
+// stg: the instances that read staged lines (float32 / guarded; nullptr: none)
+const void *warp_kernel_for(const Geo &g, int precision, int k_cap, bool stg = false) {
+    if (stg) {
+        if (!g.off32 || precision == FPSSFT_F64) return nullptr;
+        if (precision == FPSSFT_F32_GUARDED)
+            return g.D == 3 && g.L == 64
+                       ? (const void *)recover_warp_kernel<float, 64, 3, true, 0, 0, true>
+                       : nullptr;
+        if (g.D == 2 && g.L == 256)
+            return (const void *)recover_warp_kernel<float, 256, 2, false, 0, 0, true>;
+        if (g.D == 3 && g.L == 64)
+            return (const void *)recover_warp_kernel<float, 64, 3, false, 0, 0, true>;
+        return (const void *)recover_warp_kernel<float, 0, 0, false, 0, 0, true>;
+    }
     if (precision == FPSSFT_F32_GUARDED)  // guarded float32: the noisy config-3 shape
         return g.off32 && g.D == 3 && g.L == 64
                    ? (const void *)recover_warp_kernel<float, 64, 3, true>
@@ -2265,7 +2275,19 @@ const void *team_guard_kernel_for(const Geo &g, int *nt) {
     }
     return nullptr;
 }
-const void *team_kernel_for(const Geo &g, int precision, int *nt) {
+const void *team_kernel_for(const Geo &g, int precision, int *nt, bool stg = false) {
+    if (stg) {  // the float32 instances that read staged lines (configs 4 and 5's shapes)
+        if (!g.off32 || precision != FPSSFT_F32 || g.D != 2) return nullptr;
+        if (g.L == 2048 && (*nt == 512 || *nt == 0)) {
+            *nt = 512;
+            return (const void *)recover_team_kernel<float, 2048, 2, 512, false, true>;
+        }
+        if (g.L == 512) {
+            *nt = 128;
+            return (const void *)recover_team_kernel<float, 512, 2, 128, false, true>;
+        }
+        return nullptr;
+    }
     if (precision == FPSSFT_F32_GUARDED) return team_guard_kernel_for(g, nt);
     return precision == FPSSFT_F64 ? team_kernel_for_t<double>(g, nt)
                                    : team_kernel_for_t<float>(g, nt);
@@ -2294,11 +2316,10 @@ struct LaunchPlan {
 // CTA per instance.  `g` receives the FFT plan of the chosen mode.
 // Registers per thread of the warp kernel chosen for (precision, L, D): the
 // compiled value when a device is present, else the launch-bounds cap.
-const void *warp_kernel_for(const Geo &g, int precision, int k_cap);
-
-int warp_kernel_regs(const Geo &g, int precision, int k_cap) {
+int warp_kernel_regs(const Geo &g, int precision, int k_cap, bool stg = false) {
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, warp_kernel_for(g, precision, k_cap)) == cudaSuccess &&
+    const void *k = warp_kernel_for(g, precision, k_cap, stg);
+    if (k && cudaFuncGetAttributes(&fa, k) == cudaSuccess &&
         fa.numRegs > 0)
         return fa.numRegs;
     cudaGetLastError();  // no device: clear the error, assume the cap
@@ -2341,6 +2362,10 @@ const void *group_kernel_for(const Geo &g, int precision, int group, int k_cap, 
         }
 #endif
         if (wg) *wg = FPSSFT_GROUP_WG;
+        if (narrow)  // the instances that read staged lines
+            return k_cap == 128
+                       ? (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_TEAM, 128, true>
+                       : (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_TEAM, 0, true>;
         return k_cap == 128 ? (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_TEAM, 128>
                             : (const void *)recover_warp_kernel<float, 256, 2, false, FPSSFT_GROUP_TEAM>;
     }
@@ -2352,6 +2377,7 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp,
               bool shared_sched = false) {
     const int cs = precision == FPSSFT_F64 ? 16 : 8;
     const bool guard = precision == FPSSFT_F32_GUARDED;
+    const bool stg = kn.staged != nullptr;  // the instances that read staged lines
     // candidate 1: warp per instance
     long long warp_warps = 0;
     LaunchPlan wp{};
@@ -2359,10 +2385,10 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp,
     if (want != FPSSFT_MODE_CTA) {
         bool ok = g.key_bits_ <= 31 && kn.k_cap <= 32768 && (long long)g.nlines * g.L <= 2048 &&
                   (g.L & (g.L - 1)) == 0 && plan_fft(&gw, g.nlines, precision, 32) > 0 &&
-                  (!guard || warp_kernel_for(g, precision, kn.k_cap) != nullptr);
+                  (!(guard || stg) || warp_kernel_for(g, precision, kn.k_cap, stg) != nullptr);
         if (ok) {
             const WarpLayout wl = make_warp_layout(g.D, g.L, kn.k_cap, cs, guard);
-            const int regs = (warp_kernel_regs(gw, precision, kn.k_cap) + 7) / 8 * 8;
+            const int regs = (warp_kernel_regs(gw, precision, kn.k_cap, stg) + 7) / 8 * 8;
             const long long reg_warps = 65536 / (regs * 32);
             int best_w = 0;
             for (int w : {8, 7, 6, 5, 4, 3, 2, 1}) {
@@ -2380,7 +2406,7 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp,
             if (best_w)
                 wp = LaunchPlan{FPSSFT_MODE_WARP, 32 * best_w, best_w,
                                 wl.roots + (size_t)best_w * wl.per_warp,
-                                warp_kernel_for(gw, precision, kn.k_cap)};
+                                warp_kernel_for(gw, precision, kn.k_cap, stg)};
             int gwd = FPSSFT_GROUP_WG;
             const void *gk =
                 shared_sched ? group_kernel_for(gw, precision, kn.group, kn.k_cap, &gwd,
@@ -2413,7 +2439,7 @@ int make_plan(Geo &g, const Knobs &kn, int precision, int want, LaunchPlan *lp,
             if (FPSSFT_TEAM_NT && want_nt) continue;  // compile-time A/B: one pass at that size
             const int req = FPSSFT_TEAM_NT ? FPSSFT_TEAM_NT : want_nt;
             int tnt = req;
-            const void *tk = team_kernel_for(g, precision, &tnt);
+            const void *tk = team_kernel_for(g, precision, &tnt, stg);
             if (!tk || (req && tnt != req)) continue;
             const TeamLayout tl = make_team_layout(g.D, g.L, kn.k_cap, cs, tnt, guard);
             if ((long long)tl.total > SMEM_PER_CTA) continue;

@@ -77,7 +77,7 @@ __host__ __device__ inline TeamLayout make_team_layout(int D, int L, int k_cap, 
 
 constexpr unsigned short U16_NONE = 0xFFFF;
 
-template <class R, int LC, int DC, int NT, bool GUARD = false>
+template <class R, int LC, int DC, int NT, bool GUARD = false, bool STG = false>
 __global__ void __launch_bounds__(NT, GUARD ? (FPSSFT_TEAM_GUARD_THREADS / NT > 1
                                                      ? FPSSFT_TEAM_GUARD_THREADS / NT : 1)
                                             : (512 / NT > 1 ? 512 / NT : 1))
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (FPSSFT_TEAM_GUARD_THREADS / NT > 
     __syncthreads();
 
     [[maybe_unused]] const float2 *sbase =
-        (!GUARD && kn.staged != nullptr)
+        (STG && !GUARD && kn.staged != nullptr)
             ? kn.staged + (long long)((int)inst / kn.group) * kn.staged_group_stride +
                   ((int)inst % kn.group)
             : nullptr;
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(NT, GUARD ? (FPSSFT_TEAM_GUARD_THREADS / NT > 
         it_run = it + 1;
         // staged lines: this iteration's samples of this instance (else nullptr)
         [[maybe_unused]] const float2 *sline =
-            (FPSSFT_STAGE_TEAM && sizeof(R) == 4 && !GUARD && sbase != nullptr && it < kn.stage_T)
+            (STG && sizeof(R) == 4 && !GUARD && sbase != nullptr && it < kn.stage_T)
                 ? sbase + (long long)it * (nl * L) * kn.group
                 : nullptr;
 
