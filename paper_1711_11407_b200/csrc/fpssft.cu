@@ -894,8 +894,7 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
             break;
         }
         it_run = it + 1;
-        // staged lines: this iteration's samples of this instance (else nullptr;
-        // the guarded kernel's rare exact re-evaluations still read the cube)
+        // staged lines: this iteration's samples of this instance (else nullptr)
         [[maybe_unused]] const float2 *sline =
             (STG && !PFS && !WG && sbase != nullptr && it < kn.stage_T)
                 ? sbase + (long long)it * (nl * L) * kn.group
@@ -1287,7 +1286,7 @@ __global__ void __launch_bounds__(WG > 8 ? 32 * WG : FPSSFT_WARP_NT,
                     const int sx = exact_reeval_warp<A, Roots64, LC, DC>(
                         bf, cube, g, al, ta, roots64, n_slots, slot_key, slot_live, slot_amp,
                         x0d[padi<PAD>(bf)], kn, (double)floor_a, lane, mx,
-                        FPSSFT_GUARD_CALIB == 1 ? S : nullptr);
+                        FPSSFT_GUARD_CALIB == 1 ? S : nullptr, STG ? sline : nullptr);
                     if (lane == owner) {
                         st = sx;
 #pragma unroll

@@ -199,7 +199,9 @@ __device__ __forceinline__ void exact_bin_partials(int b, const float2 *__restri
                                                    const int *slot_key,
                                                    const unsigned char *slot_live,
                                                    const cpx<AmpT> *amp64, int tid, int nth,
-                                                   cpx<double> *dft, cpx<double> *prj) {
+                                                   cpx<double> *dft, cpx<double> *prj,
+                                                   const float2 *__restrict__ sline = nullptr,
+                                                   int sG = 1) {
     const int L = g.L, D = g.D;
     const bool pow2 = (L & (L - 1)) == 0;
 #pragma unroll
@@ -230,7 +232,9 @@ __device__ __forceinline__ void exact_bin_partials(int b, const float2 *__restri
                 const int k = i - 1;  // tau + e_k: coordinate k one further, wrapping
                 const long long off = base + (n[k] + 1 == g.N[k] ? -(long long)n[k] * g.stride[k]
                                                                  : g.stride[k]);
-                const float2 x = __ldg(cube + off);
+                // sline (the STG kernels): the same sample from the staged lines
+                const float2 x = sline != nullptr ? __ldg(sline + ((long long)i * L + l) * sG)
+                                                  : __ldg(cube + off);
                 const cpx<double> xv = {(double)x.x, (double)x.y};
                 dft[k] = dft[k] + mulc(xv, r);
             }
@@ -281,14 +285,15 @@ __device__ GUARD_REEVAL_INLINE int exact_reeval_warp(int bf, const float2 *__res
                                                      const unsigned char *slot_live,
                                                      const cpx<AmpT> *amp64, cpx<double> s0,
                                                      const Knobs &kn, double floor, int lane,
-                                                     int *m, cpx<double> *S_out = nullptr) {
+                                                     int *m, cpx<double> *S_out = nullptr,
+                                                     const float2 *__restrict__ sline = nullptr) {
     Geo gc = g;  // the compile-time shape, for the callee's loops
     gc.L = LC;
     gc.D = DC;
     gc.nlines = DC + 1;
     cpx<double> dft[MAXD], prj[MAXD];
     exact_bin_partials<AmpT>(bf, cube, gc, al, ta, roots64, n_slots, slot_key, slot_live, amp64,
-                             lane, 32, dft, prj);
+                             lane, 32, dft, prj, sline, kn.group);
     cpx<double> S[MAXD + 1];
     S[0] = s0;
 #pragma unroll
