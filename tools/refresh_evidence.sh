@@ -26,6 +26,8 @@ timeout 900 $N -o $O/cfg4 $B --config 4 > $O/ncu_cfg4.log 2>&1
 timeout 900 $N -o $O/cfg5_recover $B --config 5 --batch 2048 --no-synth > $O/ncu_cfg5.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:synth -c 1 \
   -o $O/cfg5_synth python tools/synth_profile.py --reps 1 > $O/ncu_synth.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:stage_lines -s 1 -c 1 \
+  -o $O/cfg2_stage python tools/stage_profile.py 2 > $O/ncu_stage.log 2>&1
 # reports are ~25 MB each (gpurun brings back <= 64 MiB): keep CSV exports
 for r in $O/*.ncu-rep; do
   b=${r%.ncu-rep}
