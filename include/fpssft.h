@@ -122,9 +122,11 @@ int fpssft_run_batch_grouped(const void *cubes, int64_t batch, int32_t group,
  * instead of the request-rate bound of SM loads) into
  * staging[group][t][line][l][group]; the recovery kernel reads iterations
  * t < stage_iterations from there and later (straggler) iterations from the
- * host cube.  Outputs identical to fpssft_run_batch_grouped.  float32, shapes
- * the group-gather kernel is built for (FPSSFT_EUNSUPPORTED otherwise);
- * cubes may also be device memory.
+ * host cube.  Outputs identical to fpssft_run_batch_grouped.  Served by the
+ * warp-per-instance kernels (float32; guarded float32 on the 64^3 shape; the
+ * group-gather kernel for 256 x 256 batches with group a multiple of 8) and
+ * the float32 compile-time team kernels (L = 2048, 512); other shapes and
+ * float64 return FPSSFT_EUNSUPPORTED.  cubes may also be device memory.
  *   staging: device buffer of fpssft_stage_bytes(shape, group, batch,
  *            min(stage_iterations, params->t_max)) bytes.
  */
